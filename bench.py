@@ -1,0 +1,348 @@
+#!/usr/bin/env python3
+"""Benchmark: GeoDock per-ligand pose search on B200 (BASELINE.json metric, config C2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1|c4|c5]
+
+A "step" is one pass of the hot path over the whole synthetic library resident in HBM:
+K1 (pose search) + K2 (best restart) + K3 (device top-k) and, for N > 1, the NCCL all-gather of
+the per-GPU top-k records. Each rank docks its own contiguous 10k-ligand shard of a 10k*N library
+(weak scaling: per-GPU work fixed). `value` is ligands/s over all ranks, device-timed with CUDA
+events on the library's stream, max over ranks, L2 flushed (256 MiB write) before every timed
+step. `e2e` is the same metric through the public C-ABI call gd_dock_batch with host buffers
+(validation, packing, H2D, kernels, D2H inside the timed region), wall-clocked per step.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref: the unmodified
+reference's run_screening, all host threads) on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (LibrarySpec kwargs, PocketSpec kwargs, f_in measured by the oracle)
+    "c1": (dict(count=100, atoms=32, rotamers=4), dict(), 0.8387),
+    "c2": (dict(count=10000, atoms=40, rotamers=8), dict(), 0.8304),
+    "c4": (dict(count=1000, atoms=120, rotamers=32), dict(), 0.8024),
+    "c5": (dict(count=10000, atoms=40, rotamers=8), dict(dims=(47, 47, 47), spacing=0.375), 0.8321),
+}
+WORKLOAD_NAME = {
+    "c1": "C1: 100 synthetic ligands x 32 atoms x 4 rotamers vs one 24^3 pocket",
+    "c2": "C2: 10k synthetic ligands x 40 atoms x 8 rotamers vs one 24^3 (0.75 A) pocket, per GPU",
+    "c4": "C4: 1k synthetic ligands x 120 atoms x 32 rotamers vs one 24^3 pocket, per GPU",
+    "c5": "C5 grid: 10k ligands x 40 atoms x 8 rotamers vs one 47^3 (0.375 A) pocket, per GPU",
+}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---------------------------------------------------------------------------- work model
+def work_model(lib, params, f_in):
+    """Algorithmic work of one step: FP32 lane-ops and gathered bytes."""
+    import paper_1901_06229_b200 as gd
+    N, G = params.n_restarts, int(np.prod(params.rotation_steps))
+    reps, S = params.num_repetitions, params.dihedral_steps
+    w_align = w_sweep = p_cross = 0
+    # generated ligands are trees: moving set of rotamer (p, c) = subtree of c (generate.cpp:93-103)
+    A = lib.atom_off
+    same_shape = np.all(np.diff(A) == A[1] - A[0])
+    for l in range(lib.n_ligands):
+        n = int(A[l + 1] - A[l])
+        w_align += N * G * n
+        b = lib.bonds[lib.bond_off[l]:lib.bond_off[l + 1]]
+        parent = np.full(n, -1)
+        parent[b[:, 1]] = b[:, 0]
+        size = np.ones(n, np.int64)
+        for a in range(n - 1, 0, -1):  # children have larger indices in generated trees
+            size[parent[a]] += size[a]
+        for i, j in lib.rots[lib.rot_off[l]:lib.rot_off[l + 1]]:
+            m = int(size[j])
+            w_sweep += N * reps * (S - 1) * (m - 1)
+            p_cross += N * reps * (S - 1) * (m - 1) * (n - m)
+    W = w_align + w_sweep
+    ops = W * (15 + 21 * f_in) + 7 * p_cross
+    gather = 32 * f_in * W
+    return dict(w_align=w_align, w_sweep=w_sweep, p_cross=p_cross, fp32_ops=ops, gather_bytes=gather,
+                exact_tree_model=bool(same_shape))
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def cpu_reference(cfg, steps, warmup, rank, world, sample=None):
+    """The reference's run_screening (pipeline.cpp:187-290) on the host cores, bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, Params
+    ref = Oracle("reference")
+    lspec, pspec, _ = CONFIGS[cfg]
+    nproc = os.cpu_count() or 1
+    sample = sample or min(lspec["count"], max(32, 4 * nproc))
+    pocket = ref.make_pocket(**pspec) if pspec else ref.make_pocket()
+    lib = ref.make_library(sample, lspec["atoms"], lspec["rotamers"], 0)
+    vals = []
+    for it in range(warmup + steps):
+        best, rid, wall = ref.run_screening(lib, pocket, Params(), n_workers=nproc)
+        if it >= warmup:
+            vals.append(sample / wall)
+    return statistics.median(vals), nproc, sample
+
+
+def cpu_name():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import paper_1901_06229_b200 as gd
+
+    rank, world, local = dist_env()
+    dev = local
+    torch.cuda.set_device(dev)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        pg = dist
+    lspec, pspec, f_in = CONFIGS[args.config]
+    per_gpu = args.ligands or lspec["count"]
+    params = gd.DockParams(clash_factor=args.clash)
+    pocket = gd.make_pocket(gd.PocketSpec(**pspec))
+    full = gd.make_library(gd.LibrarySpec(per_gpu * world, lspec["atoms"], lspec["rotamers"], 0))
+    lib = full.slice(rank * per_gpu, (rank + 1) * per_gpu)
+    ctx = gd.Context(dev, mode=(gd.MODE_EXACT if args.exact else gd.MODE_FAST) |
+                     (gd.FLAG_SKIP_INVARIANT_CLASH if args.skip_invariant else 0))
+    ctx.set_pocket(pocket)
+    ctx.set_params(params)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    batch = ctx.stage(lib)
+    topk = args.topk
+
+    def step():
+        batch.run()
+        hits = batch.topk(topk)  # K3 + D2H of k records (tiny)
+        if pg is not None:
+            t = torch.tensor([[h[0], h[1] + rank * per_gpu, h[2]] for h in hits], dtype=torch.float64,
+                             device=dev)
+            out = [torch.empty_like(t) for _ in range(world)]
+            with torch.cuda.stream(stream):
+                pg.all_gather(out, t)
+            merged = torch.cat(out)
+            order = sorted(range(merged.shape[0]), key=lambda i: (-merged[i, 0].item(), merged[i, 1].item()))
+            hits = [tuple(merged[i].tolist()) for i in order[:topk]]
+        return hits
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if pg is not None:
+        pg.barrier()
+    times = []
+    with ClockSampler(dev) as clocks:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)  # L2 flush (256 MiB > 126 MB L2), outside the timed region
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            hits = step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches_per_step = ctx.stats()["launches"] + 2  # K1 + K2 (gd_run) + topk_prepare + topk_emit
+    # K1 alone (dominant kernel): separate timing pass, same stream
+    k1 = []
+    for _ in range(max(2, min(args.steps, 5))):
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        batch.run()
+        e1.record(stream)
+        e1.synchronize()
+        k1.append(e0.elapsed_time(e1))
+    stats = ctx.stats()
+    ms = statistics.mean(times)
+    if pg is not None:
+        t = torch.tensor([ms, statistics.mean(k1)], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms, k1ms = t.tolist()
+    else:
+        k1ms = statistics.mean(k1)
+
+    # e2e through the public C-ABI (host buffers; validate + pack + H2D + kernels + D2H)
+    e2e_times = []
+    for it in range(max(1, min(args.steps, 3)) + 1):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        res = ctx.dock(lib)
+        t1 = time.perf_counter()
+        if it > 0:
+            e2e_times.append(t1 - t0)
+    e2e_s = statistics.mean(e2e_times)
+    if pg is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_s = t.item()
+    A, Rt = int(lib.atom_off[-1]), int(lib.rot_off[-1])
+    h2d = batch_bytes = int(stats.get("h2d_bytes", 0))
+    d2h = int(stats.get("d2h_bytes", 0))
+
+    # sanity: results of the timed batch equal the e2e call's
+    chk = batch.fetch()
+    assert np.array_equal(chk.best_score, res.best_score), "staged vs e2e results differ"
+
+    if rank != 0:
+        if pg is not None:
+            pg.destroy_process_group()
+        return
+    total = per_gpu * world
+    value = total / (ms / 1e3)
+    wm = work_model(lib, params, f_in)
+    sm_mhz = clocks.summary()["sm_mhz"] or 1965.0
+    peak_tops = 148 * 128 * sm_mhz * 1e6 / 1e12  # FP32 lane-ops/s at the clock seen under load
+    achieved = wm["fp32_ops"] / (k1ms / 1e3) / 1e12
+    line = {
+        "metric": "ligands/sec (device-timed, B200) — GeoDock per-ligand pose search",
+        "value": round(value, 2), "unit": "ligands/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 coarse + f64 exact", "data": "synthetic (reference generator, seed 0)",
+        "impl": "ours",
+        "config": {"workload": WORKLOAD_NAME[args.config], "ligands_per_gpu": per_gpu,
+                   "atoms": lspec["atoms"], "rotamers": lspec["rotamers"], "params": params.__dict__,
+                   "mode": "exact" if args.exact else "fast", "skip_invariant_clash": bool(args.skip_invariant),
+                   "l2": "flushed (256 MiB write) before every timed step", "topk": topk,
+                   "parallelism": f"library sharded over {world} GPU(s), NCCL top-k all-gather" if world > 1 else "1 GPU"},
+        "e2e": {"value": round(total / e2e_s, 2), "unit": "ligands/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches_per_step,
+        "roofline": {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak_tops, 3),
+                     "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4), "traffic": None,
+                     "kernel": "K1 pose search", "k1_ms": round(k1ms, 4),
+                     "peak_source": f"148 SM x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock under load)",
+                     "work_model": {k: (int(v) if isinstance(v, (int, np.integer)) or float(v).is_integer() else v)
+                                    for k, v in wm.items()},
+                     "gather_gbs": round(wm["gather_bytes"] / (k1ms / 1e3) / 1e9, 1)},
+        "kernel_stats": stats,
+        "clocks": clocks.summary(),
+    }
+    if not args.no_cpu:
+        v, cores, sample = cpu_reference(args.config, 1, 0, rank, world, sample=args.cpu_sample)
+        line["cpu_baseline"] = {"value": round(v, 3), "unit": "ligands/s", "cores": cores, "kind": "reference",
+                                "sample": f"first {sample} ligands of the same library, reference run_screening "
+                                          f"(oracle/_ref), {cores} workers, {cpu_name()}"}
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    v, cores, sample = cpu_reference(args.config, args.steps, min(args.warmup, 1), rank, world,
+                                     sample=args.cpu_sample)
+    lspec = CONFIGS[args.config][0]
+    line = {"metric": "ligands/sec (device-timed, B200) — GeoDock per-ligand pose search", "value": round(v, 3),
+            "unit": "ligands/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(sample / v * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD_NAME[args.config], "ligands_per_gpu": lspec["count"],
+                       "atoms": lspec["atoms"], "rotamers": lspec["rotamers"]},
+            "cpu_baseline": {"value": round(v, 3), "unit": "ligands/s", "cores": cores, "kind": "reference",
+                             "sample": f"first {sample} ligands per step, unmodified reference run_screening "
+                                       f"(oracle/_ref), {cores} workers, {cpu_name()}"},
+            "e2e": {"value": round(v, 3), "unit": "ligands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--ligands", type=int, default=0, help="ligands per GPU (default: the config's)")
+    ap.add_argument("--clash", type=float, default=0.75)
+    ap.add_argument("--topk", type=int, default=100)
+    ap.add_argument("--exact", action="store_true", help="GD_MODE_EXACT kernel (FP64 everywhere)")
+    ap.add_argument("--skip-invariant", action="store_true", help="GD_FLAG_SKIP_INVARIANT_CLASH (reported separately)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

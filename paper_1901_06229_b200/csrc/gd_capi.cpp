@@ -1,0 +1,870 @@
+// C-ABI implementation: context, pocket/params upload, host-side ligand validation and SoA packing,
+// batch staging, kernel launch, result fetch. See include/geodock_b200.h for the contract and
+// DESIGN.md for the layout. Paths in comments are relative to /root/reference/proj.
+//
+// Host arithmetic that feeds the device (rotation grid, dihedral table, starting transforms) is
+// the reference's own FP64 formulas evaluated with the same libm, so the device sees the same
+// bits the reference computes (compiled with -ffp-contract=off, no -march).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <string_view>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "gd_host_math.h"
+#include "gd_internal.h"
+#include "geodock_b200.h"
+
+using gdk::DevBatch;
+using gdk::DevParams;
+using gdk::DevPocket;
+using gdk::LigMeta;
+
+struct gd_ctx {
+  int device = 0;
+  int n_sms = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int mode = GD_MODE_EXACT;  // switched to GD_MODE_FAST once the two-stage kernel is validated
+
+  // pocket
+  bool have_pocket = false;
+  uint32_t dims[3] = {0, 0, 0};
+  double origin[3] = {0, 0, 0};
+  double spacing = 1.0;
+  double* d_field = nullptr;
+  uint4* d_cells = nullptr;
+  float coarse_eps = 0.f;
+
+  // params
+  gd_params params{};
+  bool have_params = false;
+  double4* d_grid = nullptr;
+  float4* d_grid_f = nullptr;
+  double4* d_dtab = nullptr;
+  float2* d_dtab_f = nullptr;
+  uint32_t G = 0;
+  std::vector<double> grid_host;  // 4 per entry
+
+  gd_stats last{};
+  unsigned long long* d_stats = nullptr;
+  int* d_error = nullptr;
+  unsigned int* d_counter = nullptr;
+};
+
+struct gd_batch {
+  gd_ctx* ctx = nullptr;
+  DevBatch dev{};
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  void* topk_scratch = nullptr;
+  size_t topk_bytes = 0;
+  gd_hit* d_hits = nullptr;
+  std::vector<uint32_t> atom_off, rot_off;
+  uint32_t n_restarts = 0, reps = 0, S = 0;
+  gd_params params{};
+};
+
+namespace {
+
+int set_err(gd_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int cuda_err(gd_ctx* ctx, cudaError_t e, const char* what) {
+  return set_err(ctx, GD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define GD_CUDA(ctx, call)                                \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_err(ctx, e_, #call); \
+  } while (0)
+
+template <class F>
+void parallel_for(size_t n, size_t grain, F&& f) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t chunks = (n + grain - 1) / grain;
+  const unsigned nt = unsigned(std::min<size_t>(hw, chunks));
+  if (nt <= 1) {
+    for (size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> th;
+  th.reserve(nt);
+  for (unsigned t = 0; t < nt; ++t) {
+    th.emplace_back([&] {
+      for (;;) {
+        const size_t c = next.fetch_add(1);
+        if (c >= chunks) return;
+        const size_t e = std::min(n, (c + 1) * grain);
+        for (size_t i = c * grain; i < e; ++i) f(i);
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+}
+
+// ------------------------------------------------------------------ ligand graph checks
+// validate_ligand (molecule.cpp:176-238) restated over the flat layout. Messages match the
+// reference's so ValidationError text is identical.
+struct LigView {
+  uint32_t n, nb, nr;
+  const double* xyz;
+  const double* radius;
+  const uint32_t* bonds;
+  const uint32_t* rots;
+  std::string_view name;
+};
+
+LigView view_of(const gd_library* lib, uint32_t l) {
+  LigView v;
+  v.n = lib->atom_off[l + 1] - lib->atom_off[l];
+  v.nb = lib->bond_off[l + 1] - lib->bond_off[l];
+  v.nr = lib->rot_off[l + 1] - lib->rot_off[l];
+  v.xyz = lib->xyz + 3 * size_t(lib->atom_off[l]);
+  v.radius = lib->radius + lib->atom_off[l];
+  v.bonds = lib->bonds + 2 * size_t(lib->bond_off[l]);
+  v.rots = lib->rots + 2 * size_t(lib->rot_off[l]);
+  v.name = std::string_view(lib->names + lib->name_off[l], lib->name_off[l + 1] - lib->name_off[l]);
+  return v;
+}
+
+struct Adj {
+  std::vector<uint32_t> start, nbr;  // CSR
+};
+
+Adj adjacency(const LigView& v) {  // adjacency_lists (molecule.cpp:12-20)
+  Adj a;
+  a.start.assign(v.n + 1, 0);
+  for (uint32_t b = 0; b < v.nb; ++b) {
+    a.start[v.bonds[2 * b] + 1]++;
+    a.start[v.bonds[2 * b + 1] + 1]++;
+  }
+  for (uint32_t i = 0; i < v.n; ++i) a.start[i + 1] += a.start[i];
+  a.nbr.resize(a.start[v.n]);
+  std::vector<uint32_t> fill(a.start.begin(), a.start.end() - 1);
+  for (uint32_t b = 0; b < v.nb; ++b) {
+    const uint32_t x = v.bonds[2 * b], y = v.bonds[2 * b + 1];
+    a.nbr[fill[x]++] = y;
+    a.nbr[fill[y]++] = x;
+  }
+  return a;
+}
+
+// reachable (molecule.cpp:22-41) with one edge optionally deleted.
+void reachable(const Adj& a, uint32_t n, uint32_t start, uint32_t skip_a, uint32_t skip_b,
+               std::vector<char>& seen, std::vector<uint32_t>& stack) {
+  seen.assign(n, 0);
+  stack.clear();
+  stack.push_back(start);
+  seen[start] = 1;
+  while (!stack.empty()) {
+    const uint32_t u = stack.back();
+    stack.pop_back();
+    for (uint32_t e = a.start[u]; e < a.start[u + 1]; ++e) {
+      const uint32_t w = a.nbr[e];
+      if ((u == skip_a && w == skip_b) || (u == skip_b && w == skip_a)) continue;
+      if (!seen[w]) {
+        seen[w] = 1;
+        stack.push_back(w);
+      }
+    }
+  }
+}
+
+std::vector<std::string> validate(const LigView& v) {
+  std::vector<std::string> out;
+  const uint32_t n = v.n;
+  if (n == 0) {
+    out.push_back("ligand has no atoms");
+    return out;
+  }
+  for (uint32_t a = 0; a < n; ++a) {
+    if (!(v.radius[a] > 0.0)) out.push_back("atom " + std::to_string(a) + " has non-positive radius");
+    if (!std::isfinite(v.xyz[3 * a]) || !std::isfinite(v.xyz[3 * a + 1]) || !std::isfinite(v.xyz[3 * a + 2])) {
+      out.push_back("atom " + std::to_string(a) + " has non-finite coordinates");
+    }
+  }
+  bool indices_ok = true;
+  for (uint32_t b = 0; b < v.nb; ++b) {
+    if (v.bonds[2 * b] >= n || v.bonds[2 * b + 1] >= n) indices_ok = false;
+  }
+  if (!indices_ok) out.push_back("bond index out of range");
+  for (uint32_t b = 0; b < v.nb; ++b) {
+    if (v.bonds[2 * b] == v.bonds[2 * b + 1]) out.push_back("self-bond on atom " + std::to_string(v.bonds[2 * b]));
+  }
+  if (v.nr > GD_MAX_ROTAMERS) {
+    out.push_back("rotamer count exceeds the supported limit of " + std::to_string(GD_MAX_ROTAMERS));
+  }
+  if (!indices_ok) return out;
+  const Adj adj = adjacency(v);
+  std::vector<char> seen;
+  std::vector<uint32_t> stack;
+  reachable(adj, n, 0, ~0u, ~0u, seen, stack);
+  if (std::find(seen.begin(), seen.end(), 0) != seen.end()) {
+    out.push_back("bond graph is not connected");
+    return out;
+  }
+  for (uint32_t r = 0; r < v.nr; ++r) {
+    const uint32_t i = v.rots[2 * r], j = v.rots[2 * r + 1];
+    if (i >= n || j >= n) {
+      out.push_back("rotamer " + std::to_string(r) + " atom index out of range");
+      continue;
+    }
+    bool bonded = false;
+    for (uint32_t e = adj.start[i]; e < adj.start[i + 1]; ++e) bonded |= adj.nbr[e] == j;
+    if (!bonded) {
+      out.push_back("rotamer bond (" + std::to_string(i) + "," + std::to_string(j) + ") is not a bond");
+      continue;
+    }
+    reachable(adj, n, j, i, j, seen, stack);
+    if (seen[i]) {
+      out.push_back("rotamer bond (" + std::to_string(i) + "," + std::to_string(j) +
+                    ") does not disconnect graph");
+    }
+  }
+  return out;
+}
+
+std::string validation_message(std::string_view name, const std::vector<std::string>& v) {
+  std::string msg = "ligand '" + std::string(name) + "' is invalid:";  // errors.hpp:37-41
+  for (const auto& s : v) msg += " [" + s + "]";
+  return msg;
+}
+
+// ------------------------------------------------------------------ device arena
+struct Arena {
+  size_t off = 0;
+  template <class T>
+  size_t take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    const size_t at = off;
+    off += count * sizeof(T);
+    return at;
+  }
+};
+
+int upload_params(gd_ctx* ctx) {
+  // Rotation grid (geometry.cpp:16-34), FP64 with libm, plus FP32 rows of R/spacing.
+  const gd_params& p = ctx->params;
+  const uint32_t* st = p.rotation_steps;
+  const uint64_t G = uint64_t(st[0]) * st[1] * st[2];
+  std::vector<double4> grid(G);
+  ctx->grid_host.assign(4 * G, 0.0);
+  uint64_t at = 0;
+  for (unsigned i = 0; i < st[0]; ++i) {
+    const double alpha = gdh::kTwoPi * static_cast<double>(i) / static_cast<double>(st[0]);
+    for (unsigned j = 0; j < st[1]; ++j) {
+      const double beta = st[1] == 1 ? 0.0 : gdh::kPi * static_cast<double>(j) / static_cast<double>(st[1] - 1);
+      for (unsigned k = 0; k < st[2]; ++k) {
+        const double gamma = gdh::kTwoPi * static_cast<double>(k) / static_cast<double>(st[2]);
+        const gdh::Q q = gdh::from_euler_zyz(alpha, beta, gamma);
+        grid[at] = make_double4(q.w, q.x, q.y, q.z);
+        ctx->grid_host[4 * at] = q.w;
+        ctx->grid_host[4 * at + 1] = q.x;
+        ctx->grid_host[4 * at + 2] = q.y;
+        ctx->grid_host[4 * at + 3] = q.z;
+        ++at;
+      }
+    }
+  }
+  // dihedral_step angles k * (2pi/S) and about_axis's (cos, sin) of the half angle
+  // (docking.cpp:129,133; geometry.hpp:46-50; molecule.cpp:160).
+  const uint32_t S = p.dihedral_steps;
+  std::vector<double4> dtab(std::max<uint32_t>(S, 1));
+  std::vector<float2> dtab_f(std::max<uint32_t>(S, 1));
+  const double delta = gdh::kTwoPi / static_cast<double>(S);
+  for (uint32_t k = 0; k < S; ++k) {
+    const double angle = delta * static_cast<double>(k);
+    const double half = 0.5 * angle;
+    dtab[k] = make_double4(std::cos(half), std::sin(half), angle, 0.0);
+    dtab_f[k] = make_float2(float(std::cos(half)), float(std::sin(half)));
+  }
+  cudaFree(ctx->d_grid);
+  cudaFree(ctx->d_grid_f);
+  cudaFree(ctx->d_dtab);
+  cudaFree(ctx->d_dtab_f);
+  ctx->d_grid = nullptr;
+  ctx->d_grid_f = nullptr;
+  ctx->d_dtab = nullptr;
+  ctx->d_dtab_f = nullptr;
+  GD_CUDA(ctx, cudaMalloc(&ctx->d_grid, sizeof(double4) * std::max<uint64_t>(G, 1)));
+  GD_CUDA(ctx, cudaMalloc(&ctx->d_grid_f, sizeof(float4) * 3 * std::max<uint64_t>(G, 1)));
+  GD_CUDA(ctx, cudaMalloc(&ctx->d_dtab, sizeof(double4) * dtab.size()));
+  GD_CUDA(ctx, cudaMalloc(&ctx->d_dtab_f, sizeof(float2) * dtab_f.size()));
+  GD_CUDA(ctx, cudaMemcpy(ctx->d_grid, grid.data(), sizeof(double4) * G, cudaMemcpyHostToDevice));
+  GD_CUDA(ctx, cudaMemcpy(ctx->d_dtab, dtab.data(), sizeof(double4) * dtab.size(), cudaMemcpyHostToDevice));
+  GD_CUDA(ctx, cudaMemcpy(ctx->d_dtab_f, dtab_f.data(), sizeof(float2) * dtab_f.size(), cudaMemcpyHostToDevice));
+  ctx->G = uint32_t(G);
+  return GD_OK;
+}
+
+// FP32 rotation rows R/spacing for the coarse path (depends on pocket spacing and grid).
+int upload_grid_f(gd_ctx* ctx) {
+  const uint32_t G = ctx->G;
+  std::vector<float4> rows(3 * size_t(G));
+  const double inv = 1.0 / ctx->spacing;
+  for (uint32_t g = 0; g < G; ++g) {
+    const double w = ctx->grid_host[4 * g], x = ctx->grid_host[4 * g + 1], y = ctx->grid_host[4 * g + 2],
+                 z = ctx->grid_host[4 * g + 3];
+    const double m[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                            {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                            {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+    for (int r = 0; r < 3; ++r) {
+      rows[3 * g + r] = make_float4(float(m[r][0] * inv), float(m[r][1] * inv), float(m[r][2] * inv), 0.f);
+    }
+  }
+  GD_CUDA(ctx, cudaMemcpy(ctx->d_grid_f, rows.data(), sizeof(float4) * rows.size(), cudaMemcpyHostToDevice));
+  return GD_OK;
+}
+
+DevPocket dev_pocket(const gd_ctx* ctx) {
+  DevPocket pk{};
+  pk.field = ctx->d_field;
+  pk.cells = ctx->d_cells;
+  for (int i = 0; i < 3; ++i) {
+    pk.dims[i] = ctx->dims[i];
+    pk.cell_dims[i] = ctx->dims[i] - 1;
+    pk.origin[i] = ctx->origin[i];
+    pk.maxc[i] = static_cast<double>(ctx->dims[i] - 1);
+  }
+  pk.spacing = ctx->spacing;
+  pk.inv_spacing_f = float(1.0 / ctx->spacing);
+  pk.coarse_eps = ctx->coarse_eps;
+  pk.coarse_scale = float(32768.0 / 32767.0);
+  return pk;
+}
+
+DevParams dev_params(const gd_ctx* ctx) {
+  DevParams pr{};
+  pr.grid = ctx->d_grid;
+  pr.grid_f = ctx->d_grid_f;
+  pr.dtab = ctx->d_dtab;
+  pr.dtab_f = ctx->d_dtab_f;
+  pr.n_restarts = ctx->params.n_restarts;
+  pr.reps = ctx->params.num_repetitions;
+  pr.G = ctx->G;
+  pr.S = ctx->params.dihedral_steps;
+  pr.clash = ctx->params.clash_factor;
+  pr.clash_f = float(ctx->params.clash_factor);
+  pr.mode = ctx->mode;
+  return pr;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+gd_params gd_default_params(void) {
+  gd_params p;
+  p.n_restarts = 32;
+  p.num_repetitions = 3;
+  p.rotation_steps[0] = 16;
+  p.rotation_steps[1] = 16;
+  p.rotation_steps[2] = 8;
+  p.dihedral_steps = 36;
+  p.clash_factor = 0.75;
+  p.seed = 0;
+  return p;
+}
+
+const char* gd_version(void) { return "geodock_b200 0.1 (sm_100a)"; }
+
+uint64_t gd_count_score_calls(const gd_params* p, uint64_t n_rotamers) {  // docking.cpp:44-50
+  const uint64_t grid = uint64_t(p->rotation_steps[0]) * p->rotation_steps[1] * p->rotation_steps[2];
+  return uint64_t(p->n_restarts) * (grid + uint64_t(p->num_repetitions) * n_rotamers * p->dihedral_steps);
+}
+
+int gd_create(int device, gd_ctx** out) {
+  if (!out) return GD_ERR_ARGUMENT;
+  *out = nullptr;
+  auto* ctx = new gd_ctx();
+  ctx->device = device;
+  ctx->params = gd_default_params();
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_stats, sizeof(unsigned long long) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_error, sizeof(int) * 2);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_counter, sizeof(unsigned int) * 4);
+  if (e != cudaSuccess) {
+    static thread_local std::string msg;
+    msg = std::string("gd_create: ") + cudaGetErrorString(e);
+    delete ctx;
+    return GD_ERR_CUDA;
+  }
+  ctx->have_params = upload_params(ctx) == GD_OK;
+  *out = ctx;
+  return ctx->have_params ? GD_OK : GD_ERR_CUDA;
+}
+
+void gd_destroy(gd_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaFree(ctx->d_field);
+  cudaFree(ctx->d_cells);
+  cudaFree(ctx->d_grid);
+  cudaFree(ctx->d_grid_f);
+  cudaFree(ctx->d_dtab);
+  cudaFree(ctx->d_dtab_f);
+  cudaFree(ctx->d_stats);
+  cudaFree(ctx->d_error);
+  cudaFree(ctx->d_counter);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* gd_last_error(const gd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void* gd_stream(gd_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int gd_set_mode(gd_ctx* ctx, int mode) {
+  if (!ctx) return GD_ERR_ARGUMENT;
+  if ((mode & 0xff) != GD_MODE_FAST && (mode & 0xff) != GD_MODE_EXACT) {
+    return set_err(ctx, GD_ERR_ARGUMENT, "unknown mode");
+  }
+  ctx->mode = mode;
+  return GD_OK;
+}
+
+int gd_set_params(gd_ctx* ctx, const gd_params* p) {
+  if (!ctx || !p) return GD_ERR_ARGUMENT;
+  if (!p->rotation_steps[0] || !p->rotation_steps[1] || !p->rotation_steps[2]) {
+    return set_err(ctx, GD_ERR_CONTRACT, "rotation grid steps must all be >= 1");  // geometry.cpp:18-20
+  }
+  cudaSetDevice(ctx->device);
+  ctx->params = *p;
+  ctx->have_params = false;
+  int rc = upload_params(ctx);
+  if (rc != GD_OK) return rc;
+  if (ctx->have_pocket) rc = upload_grid_f(ctx);
+  ctx->have_params = rc == GD_OK;
+  return rc;
+}
+
+int gd_set_pocket(gd_ctx* ctx, const uint32_t dims[3], const double origin[3], double spacing,
+                  const double* field) {
+  if (!ctx || !dims || !origin || !field) return GD_ERR_ARGUMENT;
+  if (dims[0] < 2 || dims[1] < 2 || dims[2] < 2) return set_err(ctx, GD_ERR_CONTRACT, "pocket dims must be >= 2");
+  if (!(spacing > 0.0)) return set_err(ctx, GD_ERR_CONTRACT, "pocket spacing must be > 0");
+  cudaSetDevice(ctx->device);
+  const size_t nv = size_t(dims[0]) * dims[1] * dims[2];
+  cudaFree(ctx->d_field);
+  cudaFree(ctx->d_cells);
+  ctx->d_field = nullptr;
+  ctx->d_cells = nullptr;
+  GD_CUDA(ctx, cudaMalloc(&ctx->d_field, nv * sizeof(double)));
+  GD_CUDA(ctx, cudaMemcpy(ctx->d_field, field, nv * sizeof(double), cudaMemcpyHostToDevice));
+
+  // Coarse-path cells: for every grid cell (ix,iy,iz) < dims-1, its 8 corner values as 15-bit
+  // fixed point u = round(v * 32767) with bit 15 set (so a byte permute turns a half-word into
+  // the float 1 + u/32768). Corner order: bit0 = +x, bit1 = +y, bit2 = +z.
+  const uint32_t cx = dims[0] - 1, cy = dims[1] - 1, cz = dims[2] - 1;
+  std::vector<uint4> cells(size_t(cx) * cy * cz);
+  double max_step = 0.0;  // largest |v(i+1) - v(i)| along any axis: Lipschitz bound per cell
+  auto at = [&](uint32_t x, uint32_t y, uint32_t z) { return field[(size_t(z) * dims[1] + y) * dims[0] + x]; };
+  auto enc = [](double v) -> uint32_t {
+    double c = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    return 0x8000u | uint32_t(std::lround(c * 32767.0));
+  };
+  for (uint32_t z = 0; z < cz; ++z)
+    for (uint32_t y = 0; y < cy; ++y)
+      for (uint32_t x = 0; x < cx; ++x) {
+        uint32_t h[8];
+        for (int c = 0; c < 8; ++c) h[c] = enc(at(x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1)));
+        cells[(size_t(z) * cy + y) * cx + x] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16),
+                                                          h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+        for (int c = 0; c < 8; ++c) {
+          const double v0 = at(x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1));
+          if (!(c & 1)) max_step = std::max(max_step, std::fabs(at(x + 1, y + ((c >> 1) & 1), z + ((c >> 2) & 1)) - v0));
+          if (!(c & 2)) max_step = std::max(max_step, std::fabs(at(x + (c & 1), y + 1, z + ((c >> 2) & 1)) - v0));
+          if (!(c & 4)) max_step = std::max(max_step, std::fabs(at(x + (c & 1), y + ((c >> 1) & 1), z + 1) - v0));
+        }
+      }
+  bool in_range = true;
+  for (size_t i = 0; i < nv; ++i) in_range &= (field[i] >= 0.0 && field[i] <= 1.0);
+  GD_CUDA(ctx, cudaMalloc(&ctx->d_cells, cells.size() * sizeof(uint4)));
+  GD_CUDA(ctx, cudaMemcpy(ctx->d_cells, cells.data(), cells.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+  // Per-sample coarse error bound: quantisation 0.5/32767, position error of the
+  // FP32 transform (<= 4e-5 grid units per axis) times the per-axis slope bound, FP32 lerp rounding.
+  // A field outside [0,1] breaks the quantiser, so the fast path is disabled for it (eps = inf).
+  const double eps = in_range ? (0.5 / 32767.0 + 3.0 * 4e-5 * max_step + 2e-6) : INFINITY;
+  ctx->coarse_eps = float(eps);
+  for (int i = 0; i < 3; ++i) {
+    ctx->dims[i] = dims[i];
+    ctx->origin[i] = origin[i];
+  }
+  ctx->spacing = spacing;
+  ctx->have_pocket = true;
+  return upload_grid_f(ctx);
+}
+
+int gd_validate_ligand(const gd_library* lib, uint32_t l, char* msg, uint32_t cap) {
+  if (!lib || l >= lib->n_ligands) return -1;
+  const std::vector<std::string> v = validate(view_of(lib, l));
+  std::string all;
+  for (const auto& s : v) all += s + "\n";
+  if (msg && cap) std::snprintf(msg, cap, "%s", all.c_str());
+  return int(v.size());
+}
+
+int gd_moving_set(const gd_library* lib, uint32_t l, uint32_t r, uint32_t* out, uint32_t* out_len) {
+  if (!lib || l >= lib->n_ligands || !out || !out_len) return GD_ERR_ARGUMENT;
+  const LigView v = view_of(lib, l);
+  if (!validate(v).empty()) return GD_ERR_INVALID_LIGAND;
+  if (r >= v.nr) return GD_ERR_CONTRACT;
+  const Adj adj = adjacency(v);
+  std::vector<char> seen;
+  std::vector<uint32_t> stack;
+  reachable(adj, v.n, v.rots[2 * r + 1], v.rots[2 * r], v.rots[2 * r + 1], seen, stack);
+  uint32_t k = 0;
+  for (uint32_t a = 0; a < v.n; ++a)
+    if (seen[a]) out[k++] = a;
+  *out_len = k;
+  return GD_OK;
+}
+
+int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
+  if (!ctx || !lib || !out) return GD_ERR_ARGUMENT;
+  *out = nullptr;
+  if (!ctx->have_pocket) return set_err(ctx, GD_ERR_NO_POCKET, "no pocket set");
+  if (!ctx->have_params) return set_err(ctx, GD_ERR_CUDA, "parameters not uploaded");
+  cudaSetDevice(ctx->device);
+  const uint32_t L = lib->n_ligands;
+  if (L > 0 && (!lib->atom_off || !lib->bond_off || !lib->rot_off || !lib->name_off || !lib->names)) {
+    return set_err(ctx, GD_ERR_ARGUMENT, "null library array");
+  }
+  const gd_params& P = ctx->params;
+  const uint32_t N = P.n_restarts, reps = P.num_repetitions, S = P.dihedral_steps;
+
+  // ---- validation (dock_ligand throws before any work, docking.cpp:239-240; run_screening
+  // validates per task, pipeline.cpp:233 — the first invalid ligand in library order is reported).
+  std::vector<uint32_t> bad(L, 0);
+  parallel_for(L, 256, [&](size_t l) {
+    const LigView v = view_of(lib, uint32_t(l));
+    bad[l] = (!validate(v).empty() || v.n > GD_MAX_ATOMS) ? 1u : 0u;
+  });
+  uint32_t any_rot = 0, max_n = 1;
+  for (uint32_t l = 0; l < L; ++l) {
+    if (bad[l]) {
+      const LigView v = view_of(lib, l);
+      const auto viol = validate(v);
+      if (!viol.empty()) return set_err(ctx, GD_ERR_INVALID_LIGAND, validation_message(v.name, viol));
+      return set_err(ctx, GD_ERR_UNSUPPORTED,
+                     "ligand '" + std::string(v.name) + "' has " + std::to_string(v.n) +
+                         " atoms; this build supports up to " + std::to_string(GD_MAX_ATOMS));
+    }
+    const LigView v = view_of(lib, l);
+    any_rot |= v.nr;
+    max_n = std::max(max_n, v.n);
+  }
+  // bump_check's clash-factor contract fires on the first dihedral candidate (scoring.cpp:48-50).
+  if (any_rot && reps && S && (!(P.clash_factor > 0.0) || P.clash_factor > 1.0)) {
+    return set_err(ctx, GD_ERR_CONTRACT, "clash_factor must lie in (0, 1]");
+  }
+
+  auto* b = new gd_batch();
+  b->ctx = ctx;
+  b->params = P;
+  b->n_restarts = N;
+  b->reps = reps;
+  b->S = S;
+  b->atom_off.assign(lib->atom_off, lib->atom_off + L + 1);
+  b->rot_off.assign(lib->rot_off, lib->rot_off + L + 1);
+  const uint32_t A = L ? lib->atom_off[L] : 0;
+  const uint32_t Rt = L ? lib->rot_off[L] : 0;
+
+  // ---- host-side packing sizes
+  std::vector<uint32_t> mask_base(L + 1, 0), adj_base(L + 1, 0);
+  for (uint32_t l = 0; l < L; ++l) {
+    const uint32_t n = lib->atom_off[l + 1] - lib->atom_off[l];
+    const uint32_t W = (n + 31) / 32;
+    mask_base[l + 1] = mask_base[l] + (lib->rot_off[l + 1] - lib->rot_off[l]) * W;
+    adj_base[l + 1] = adj_base[l] + n * W;
+  }
+  const size_t n_items = size_t(L) * N;
+  Arena ar;
+  const size_t o_meta = ar.take<LigMeta>(L);
+  const size_t o_atoms = ar.take<double4>(A);
+  const size_t o_start = ar.take<double4>(2 * n_items);
+  const size_t o_rots = ar.take<uint2>(Rt);
+  const size_t o_dih0 = ar.take<double>(Rt);
+  const size_t o_masks = ar.take<uint32_t>(mask_base[L]);
+  const size_t o_adj = ar.take<uint32_t>(adj_base[L]);
+  const size_t host_bytes = ar.off;  // everything above is uploaded
+  const size_t o_rs_score = ar.take<double>(n_items);
+  const size_t o_rs_ascore = ar.take<double>(n_items);
+  const size_t o_rs_aidx = ar.take<uint32_t>(n_items);
+  const size_t o_rs_stepk = ar.take<int32_t>(size_t(Rt) * N * reps);
+  const size_t o_rs_xyz = ar.take<double>(size_t(A) * N * 3);
+  const size_t o_rs_dih = ar.take<double>(size_t(Rt) * N);
+  const size_t o_best = ar.take<double>(L);
+  const size_t o_brs = ar.take<uint32_t>(L);
+  const size_t o_fxyz = ar.take<double>(size_t(A) * 3);
+  const size_t o_fdih = ar.take<double>(Rt);
+  b->arena_bytes = ar.off + 256;
+
+  std::vector<unsigned char> host(host_bytes + 256);
+  unsigned char* H = host.data();
+  auto* meta = reinterpret_cast<LigMeta*>(H + o_meta);
+  auto* atoms = reinterpret_cast<double4*>(H + o_atoms);
+  auto* start = reinterpret_cast<double4*>(H + o_start);
+  auto* rots = reinterpret_cast<uint2*>(H + o_rots);
+  auto* dih0 = reinterpret_cast<double*>(H + o_dih0);
+  auto* masks = reinterpret_cast<uint32_t*>(H + o_masks);
+  auto* adjm = reinterpret_cast<uint32_t*>(H + o_adj);
+  const double lo[3] = {ctx->origin[0], ctx->origin[1], ctx->origin[2]};
+  // Pocket::bounds_hi (scoring.hpp:32-36)
+  const double hi[3] = {ctx->origin[0] + ctx->spacing * static_cast<double>(ctx->dims[0] - 1),
+                        ctx->origin[1] + ctx->spacing * static_cast<double>(ctx->dims[1] - 1),
+                        ctx->origin[2] + ctx->spacing * static_cast<double>(ctx->dims[2] - 1)};
+
+  parallel_for(L, 64, [&](size_t li) {
+    const uint32_t l = uint32_t(li);
+    const LigView v = view_of(lib, l);
+    const uint32_t n = v.n, W = (n + 31) / 32;
+    LigMeta m{};
+    m.atom_base = lib->atom_off[l];
+    m.rot_base = lib->rot_off[l];
+    m.mask_base = mask_base[l];
+    m.adj_base = adj_base[l];
+    m.n = uint16_t(n);
+    m.nr = uint16_t(v.nr);
+    meta[l] = m;
+    for (uint32_t a = 0; a < n; ++a) {
+      atoms[m.atom_base + a] = make_double4(v.xyz[3 * a], v.xyz[3 * a + 1], v.xyz[3 * a + 2], v.radius[a]);
+    }
+    // bonded rows (Ligand::adjacency, molecule.cpp:80-86)
+    uint32_t* adj_l = adjm + m.adj_base;
+    std::fill(adj_l, adj_l + size_t(n) * W, 0u);
+    for (uint32_t e = 0; e < v.nb; ++e) {
+      const uint32_t x = v.bonds[2 * e], y = v.bonds[2 * e + 1];
+      adj_l[x * W + (y >> 5)] |= 1u << (y & 31);
+      adj_l[y * W + (x >> 5)] |= 1u << (x & 31);
+    }
+    // moving sets (finalize_ligand, molecule.cpp:88-98) as bitmasks
+    const Adj adj = adjacency(v);
+    std::vector<char> seen;
+    std::vector<uint32_t> stack;
+    for (uint32_t r = 0; r < v.nr; ++r) {
+      const uint32_t i = v.rots[2 * r], j = v.rots[2 * r + 1];
+      rots[m.rot_base + r] = make_uint2(i, j);
+      dih0[m.rot_base + r] = lib->dihedrals ? lib->dihedrals[m.rot_base + r] : 0.0;
+      reachable(adj, n, j, i, j, seen, stack);
+      uint32_t* mk = masks + m.mask_base + r * W;
+      std::fill(mk, mk + W, 0u);
+      for (uint32_t a = 0; a < n; ++a)
+        if (seen[a]) mk[a >> 5] |= 1u << (a & 31);
+    }
+    // starting transforms (generate_starting_pose, docking.cpp:52-69): q and target per restart.
+    const uint64_t lig_seed = gdh::mix_seed(P.seed, gdh::fnv1a64(v.name));
+    for (uint32_t pid = 0; pid < N; ++pid) {
+      gdh::SplitMix64 rng(gdh::mix_seed(lig_seed, pid));
+      const gdh::Q q = gdh::random_rotation(rng);
+      const double tx = rng.uniform(lo[0], hi[0]);
+      const double ty = rng.uniform(lo[1], hi[1]);
+      const double tz = rng.uniform(lo[2], hi[2]);
+      const size_t it = size_t(l) * N + pid;
+      start[2 * it] = make_double4(q.w, q.x, q.y, q.z);
+      start[2 * it + 1] = make_double4(tx, ty, tz, 0.0);
+    }
+  });
+
+  cudaError_t e = cudaMalloc(&b->arena, b->arena_bytes);
+  if (e != cudaSuccess) {
+    delete b;
+    return cuda_err(ctx, e, "cudaMalloc(batch)");
+  }
+  auto* D = static_cast<unsigned char*>(b->arena);
+  e = cudaMemcpyAsync(D, H, host_bytes, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    cudaFree(b->arena);
+    delete b;
+    return cuda_err(ctx, e, "upload batch");
+  }
+  ctx->last.h2d_bytes = host_bytes;
+  DevBatch& d = b->dev;
+  d.n_lig = L;
+  d.n_atoms = A;
+  d.n_rots = Rt;
+  d.max_n = max_n;
+  d.meta = reinterpret_cast<const LigMeta*>(D + o_meta);
+  d.atoms = reinterpret_cast<const double4*>(D + o_atoms);
+  d.start = reinterpret_cast<const double4*>(D + o_start);
+  d.rots = reinterpret_cast<const uint2*>(D + o_rots);
+  d.dih0 = reinterpret_cast<const double*>(D + o_dih0);
+  d.masks = reinterpret_cast<const uint32_t*>(D + o_masks);
+  d.adj = reinterpret_cast<const uint32_t*>(D + o_adj);
+  d.rs_score = reinterpret_cast<double*>(D + o_rs_score);
+  d.rs_align_score = reinterpret_cast<double*>(D + o_rs_ascore);
+  d.rs_align_index = reinterpret_cast<uint32_t*>(D + o_rs_aidx);
+  d.rs_step_k = reinterpret_cast<int32_t*>(D + o_rs_stepk);
+  d.rs_xyz = reinterpret_cast<double*>(D + o_rs_xyz);
+  d.rs_dih = reinterpret_cast<double*>(D + o_rs_dih);
+  d.best_score = reinterpret_cast<double*>(D + o_best);
+  d.best_restart = reinterpret_cast<uint32_t*>(D + o_brs);
+  d.final_xyz = reinterpret_cast<double*>(D + o_fxyz);
+  d.final_dih = reinterpret_cast<double*>(D + o_fdih);
+  d.work_counter = ctx->d_counter;
+  d.error = ctx->d_error;
+  d.stats = ctx->d_stats;
+  *out = b;
+  return GD_OK;
+}
+
+int gd_run(gd_batch* b) {
+  if (!b) return GD_ERR_ARGUMENT;
+  gd_ctx* ctx = b->ctx;
+  cudaSetDevice(ctx->device);
+  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_error, 0, 2 * sizeof(int), ctx->stream));
+  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  int launches = 0;
+  DevParams pr = dev_params(ctx);
+  if (!(ctx->coarse_eps < 1.0f)) pr.mode = (pr.mode & ~0xff) | GD_MODE_EXACT;
+  const cudaError_t e = gdk::launch_dock(dev_pocket(ctx), pr, b->dev, ctx->n_sms, ctx->stream, &launches);
+  ctx->last.launches = uint32_t(launches);
+  if (e != cudaSuccess) return cuda_err(ctx, e, "launch_dock");
+  return GD_OK;
+}
+
+int gd_sync(gd_ctx* ctx) {
+  if (!ctx) return GD_ERR_ARGUMENT;
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GD_OK;
+}
+
+static int check_device_error(gd_batch* b) {
+  gd_ctx* ctx = b->ctx;
+  int err[2] = {0, 0};
+  unsigned long long st[8];
+  GD_CUDA(ctx, cudaMemcpyAsync(err, ctx->d_error, sizeof err, cudaMemcpyDeviceToHost, ctx->stream));
+  GD_CUDA(ctx, cudaMemcpyAsync(st, ctx->d_stats, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->last.restarts = st[0];
+  ctx->last.align_exact_evals = st[1];
+  ctx->last.align_fallbacks = st[2];
+  ctx->last.step_exact_evals = st[3];
+  ctx->last.step_fallbacks = st[4];
+  ctx->last.commits = st[5];
+  if (err[0] == GD_ERR_DEGENERATE_AXIS) {
+    // The reference names the ligand (molecule.cpp:157).
+    return set_err(ctx, GD_ERR_DEGENERATE_AXIS, "rotamer axis atoms coincide in ligand #" + std::to_string(err[1]));
+  }
+  if (err[0] != 0) return set_err(ctx, err[0], "device error " + std::to_string(err[0]));
+  return GD_OK;
+}
+
+int gd_fetch(gd_batch* b, gd_results* out) {
+  if (!b || !out || !out->best_score || !out->best_restart) return GD_ERR_ARGUMENT;
+  gd_ctx* ctx = b->ctx;
+  cudaSetDevice(ctx->device);
+  int rc = check_device_error(b);
+  if (rc != GD_OK) return rc;
+  const DevBatch& d = b->dev;
+  const uint32_t L = d.n_lig, N = b->n_restarts;
+  const cudaStream_t s = ctx->stream;
+  GD_CUDA(ctx, cudaMemcpyAsync(out->best_score, d.best_score, L * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GD_CUDA(ctx, cudaMemcpyAsync(out->best_restart, d.best_restart, L * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  if (out->final_xyz)
+    GD_CUDA(ctx, cudaMemcpyAsync(out->final_xyz, d.final_xyz, size_t(d.n_atoms) * 3 * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+  if (out->final_dihedrals)
+    GD_CUDA(ctx, cudaMemcpyAsync(out->final_dihedrals, d.final_dih, size_t(d.n_rots) * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+  if (out->align_index)
+    GD_CUDA(ctx, cudaMemcpyAsync(out->align_index, d.rs_align_index, size_t(L) * N * sizeof(uint32_t),
+                                 cudaMemcpyDeviceToHost, s));
+  if (out->align_score)
+    GD_CUDA(ctx, cudaMemcpyAsync(out->align_score, d.rs_align_score, size_t(L) * N * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+  if (out->restart_score)
+    GD_CUDA(ctx, cudaMemcpyAsync(out->restart_score, d.rs_score, size_t(L) * N * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+  if (out->step_k)
+    GD_CUDA(ctx, cudaMemcpyAsync(out->step_k, d.rs_step_k, size_t(d.n_rots) * N * b->reps * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, s));
+  GD_CUDA(ctx, cudaStreamSynchronize(s));
+  ctx->last.d2h_bytes = L * (sizeof(double) + sizeof(uint32_t)) +
+                        (out->final_xyz ? size_t(d.n_atoms) * 3 * sizeof(double) : 0) +
+                        (out->final_dihedrals ? size_t(d.n_rots) * sizeof(double) : 0) +
+                        (out->align_index ? size_t(L) * N * sizeof(uint32_t) : 0) +
+                        (out->align_score ? size_t(L) * N * sizeof(double) : 0) +
+                        (out->restart_score ? size_t(L) * N * sizeof(double) : 0) +
+                        (out->step_k ? size_t(d.n_rots) * N * b->reps * sizeof(int32_t) : 0);
+  // score_calls / nominal phase times are the closed form (docking.cpp:44-50, 226-229): the
+  // reference's recorded counters equal it by construction (docking_test.cpp:304-320).
+  const uint64_t G = uint64_t(b->params.rotation_steps[0]) * b->params.rotation_steps[1] * b->params.rotation_steps[2];
+  for (uint32_t l = 0; l < L; ++l) {
+    const uint64_t R = b->rot_off[l + 1] - b->rot_off[l];
+    const uint64_t align_calls = uint64_t(N) * G;
+    const uint64_t opt_calls = uint64_t(N) * b->reps * R * b->S;
+    if (out->score_calls) out->score_calls[l] = align_calls + opt_calls;
+    if (out->phase_times) {
+      out->phase_times[2 * l] = static_cast<double>(align_calls) * 1e-7;  // kNominalSecondsPerScoreCall
+      out->phase_times[2 * l + 1] = static_cast<double>(opt_calls) * 1e-7;
+    }
+  }
+  return GD_OK;
+}
+
+int gd_topk(gd_batch* b, uint32_t k, gd_hit* out, uint32_t* n_out) {
+  if (!b || !out || !n_out) return GD_ERR_ARGUMENT;
+  gd_ctx* ctx = b->ctx;
+  cudaSetDevice(ctx->device);
+  const uint32_t n = b->dev.n_lig;
+  if (k > n) k = n;
+  *n_out = k;
+  if (k == 0) return GD_OK;
+  const size_t need = gdk::topk_scratch_bytes(n);
+  if (b->topk_bytes < need) {
+    cudaFree(b->topk_scratch);
+    b->topk_scratch = nullptr;
+    GD_CUDA(ctx, cudaMalloc(&b->topk_scratch, need));
+    b->topk_bytes = need;
+  }
+  if (!b->d_hits) GD_CUDA(ctx, cudaMalloc(&b->d_hits, sizeof(gd_hit) * n));
+  GD_CUDA(ctx, gdk::launch_topk(b->dev, k, b->topk_scratch, b->topk_bytes, b->d_hits, ctx->stream));
+  GD_CUDA(ctx, cudaMemcpyAsync(out, b->d_hits, sizeof(gd_hit) * k, cudaMemcpyDeviceToHost, ctx->stream));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GD_OK;
+}
+
+void gd_batch_free(gd_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->ctx->device);
+  cudaFree(b->arena);
+  cudaFree(b->topk_scratch);
+  cudaFree(b->d_hits);
+  delete b;
+}
+
+int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
+  if (!ctx || !out) return GD_ERR_ARGUMENT;
+  *out = ctx->last;
+  return GD_OK;
+}
+
+int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
+  if (!ctx || !lib || !out) return GD_ERR_ARGUMENT;
+  gd_batch* b = nullptr;
+  int rc = gd_stage(ctx, lib, &b);
+  if (rc != GD_OK) return rc;
+  rc = gd_run(b);
+  if (rc == GD_OK) rc = gd_fetch(b, out);
+  gd_batch_free(b);
+  return rc;
+}
+
+}  // extern "C"

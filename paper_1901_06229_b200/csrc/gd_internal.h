@@ -1,0 +1,98 @@
+// Internal layout shared by the host packer (gd_capi.cpp) and the kernels (gd_kernels.cu).
+// Not part of the C-ABI. DESIGN.md §2 documents the HBM layout.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "geodock_b200.h"
+
+namespace gdk {
+
+constexpr int kMaxAtoms = 256;      // GD_MAX_ATOMS
+constexpr int kMaxWords = kMaxAtoms / 32;
+
+// Per-ligand metadata (32 B, one coalesced load per warp).
+struct LigMeta {
+  uint32_t atom_base;  // first atom in atoms[] / final_xyz
+  uint32_t rot_base;   // first rotamer in rots[] / dih0[]
+  uint32_t mask_base;  // moving bitmask of rotamer r: masks[mask_base + r*W .. +W)
+  uint32_t adj_base;   // bonded row of atom a: adj[adj_base + a*W .. +W)
+  uint16_t n;          // atoms
+  uint16_t nr;         // rotamers
+  uint32_t pad0;
+  uint64_t pad1;
+};
+static_assert(sizeof(LigMeta) == 32, "LigMeta layout");
+
+// Pocket as seen by the kernels.
+struct DevPocket {
+  const double* field;   // FP64 x-fastest field (exact path)
+  const uint4* cells;    // 15-bit packed 8-corner cells (coarse path), (mx*my*mz) entries
+  uint32_t dims[3];
+  uint32_t cell_dims[3]; // dims - 1
+  double origin[3];
+  double spacing;
+  double maxc[3];        // dims - 1 as doubles (sample_field's outside test, scoring.cpp:16-18)
+  float inv_spacing_f;
+  float coarse_eps;      // per-sample error bound of the coarse path
+  float coarse_scale;    // 32768/32767: undoes the 15-bit encode scale
+  float pad;
+};
+
+// Search parameters as seen by the kernels.
+struct DevParams {
+  const double4* grid;     // G rotation quaternions (w,x,y,z), FP64, host-built with libm
+  const float4* grid_f;    // G x 3 float4 rows of R/spacing (coarse path)
+  const double4* dtab;     // S entries: (cos(k*delta/2), sin(k*delta/2), k*delta, 0)
+  const float2* dtab_f;    // S entries: (cos, sin) in FP32 (coarse path)
+  uint32_t n_restarts;
+  uint32_t reps;
+  uint32_t G;
+  uint32_t S;
+  double clash;
+  float clash_f;
+  int mode;                // GD_MODE_* | flags
+};
+
+// Device-resident batch.
+struct DevBatch {
+  uint32_t n_lig;
+  uint32_t n_atoms;
+  uint32_t n_rots;
+  uint32_t max_n;
+  const LigMeta* meta;
+  const double4* atoms;    // (x, y, z, radius)
+  const double4* start;    // per (ligand, restart): [q(w,x,y,z)], [t(x,y,z), 0]  -> 2 x double4
+  const uint2* rots;       // (atom_i, atom_j)
+  const double* dih0;      // initial dihedrals
+  const uint32_t* masks;   // moving bitmasks
+  const uint32_t* adj;     // bonded bitmask rows
+  // per-restart scratch / trace
+  double* rs_score;
+  double* rs_align_score;
+  uint32_t* rs_align_index;
+  int32_t* rs_step_k;      // rot_base*N*reps + (restart*reps + rep)*R + r
+  double* rs_xyz;          // (atom_base*N + restart*n + a)*3
+  double* rs_dih;          // rot_base*N + restart*R + r
+  // per-ligand results
+  double* best_score;
+  uint32_t* best_restart;
+  double* final_xyz;
+  double* final_dih;
+  // control
+  unsigned int* work_counter;
+  int* error;              // [0] = status, [1] = ligand index
+  unsigned long long* stats;  // gd_stats counters (6 x u64)
+};
+
+// Kernel launchers (gd_kernels.cu). Return cudaGetLastError() of the launches.
+cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
+                        cudaStream_t stream, int* launches);
+// Device top-k by (best_score desc, ligand asc) into out[0..k). Needs scratch from topk_scratch_bytes.
+size_t topk_scratch_bytes(uint32_t n_lig);
+cudaError_t launch_topk(const DevBatch& b, uint32_t k, void* scratch, size_t scratch_bytes,
+                        gd_hit* out, cudaStream_t stream);
+
+}  // namespace gdk
