@@ -32,7 +32,7 @@ struct gd_ctx {
   int n_sms = 0;
   cudaStream_t stream = nullptr;
   std::string err;
-  int mode = GD_MODE_EXACT;  // switched to GD_MODE_FAST once the two-stage kernel is validated
+  int mode = GD_MODE_FAST;
 
   // pocket
   bool have_pocket = false;
@@ -41,7 +41,8 @@ struct gd_ctx {
   double spacing = 1.0;
   double* d_field = nullptr;
   uint4* d_cells = nullptr;
-  float coarse_eps = 0.f;
+  float q_eps = 0.f;
+  float max_step = 0.f;
 
   // params
   gd_params params{};
@@ -340,7 +341,8 @@ DevPocket dev_pocket(const gd_ctx* ctx) {
   }
   pk.spacing = ctx->spacing;
   pk.inv_spacing_f = float(1.0 / ctx->spacing);
-  pk.coarse_eps = ctx->coarse_eps;
+  pk.q_eps = ctx->q_eps;
+  pk.max_step = ctx->max_step;
   pk.coarse_scale = float(32768.0 / 32767.0);
   return pk;
 }
@@ -496,11 +498,11 @@ int gd_set_pocket(gd_ctx* ctx, const uint32_t dims[3], const double origin[3], d
   for (size_t i = 0; i < nv; ++i) in_range &= (field[i] >= 0.0 && field[i] <= 1.0);
   GD_CUDA(ctx, cudaMalloc(&ctx->d_cells, cells.size() * sizeof(uint4)));
   GD_CUDA(ctx, cudaMemcpy(ctx->d_cells, cells.data(), cells.size() * sizeof(uint4), cudaMemcpyHostToDevice));
-  // Per-sample coarse error bound: quantisation 0.5/32767, position error of the
-  // FP32 transform (<= 4e-5 grid units per axis) times the per-axis slope bound, FP32 lerp rounding.
-  // A field outside [0,1] breaks the quantiser, so the fast path is disabled for it (eps = inf).
-  const double eps = in_range ? (0.5 / 32767.0 + 3.0 * 4e-5 * max_step + 2e-6) : INFINITY;
-  ctx->coarse_eps = float(eps);
+  // Coarse error model: quantisation 0.5/32767 per corner value; the kernel adds
+  // 3 * max_step * (its FP32 position bound). A field outside [0,1] breaks the quantiser, so the
+  // fast path is disabled for it (q_eps = inf -> exact kernel).
+  ctx->q_eps = in_range ? float(0.5 / 32767.0) : INFINITY;
+  ctx->max_step = float(max_step);
   for (int i = 0; i < 3; ++i) {
     ctx->dims[i] = dims[i];
     ctx->origin[i] = origin[i];
@@ -602,6 +604,9 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
   const size_t o_dih0 = ar.take<double>(Rt);
   const size_t o_masks = ar.take<uint32_t>(mask_base[L]);
   const size_t o_adj = ar.take<uint32_t>(adj_base[L]);
+  const size_t o_dfs = ar.take<uint16_t>(A);
+  const size_t o_rdfs = ar.take<ushort4>(Rt);
+  const size_t o_adjd = ar.take<uint32_t>(adj_base[L]);
   const size_t host_bytes = ar.off;  // everything above is uploaded
   const size_t o_rs_score = ar.take<double>(n_items);
   const size_t o_rs_ascore = ar.take<double>(n_items);
@@ -624,6 +629,9 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
   auto* dih0 = reinterpret_cast<double*>(H + o_dih0);
   auto* masks = reinterpret_cast<uint32_t*>(H + o_masks);
   auto* adjm = reinterpret_cast<uint32_t*>(H + o_adj);
+  auto* dfs = reinterpret_cast<uint16_t*>(H + o_dfs);
+  auto* rdfs = reinterpret_cast<ushort4*>(H + o_rdfs);
+  auto* adjd = reinterpret_cast<uint32_t*>(H + o_adjd);
   const double lo[3] = {ctx->origin[0], ctx->origin[1], ctx->origin[2]};
   // Pocket::bounds_hi (scoring.hpp:32-36)
   const double hi[3] = {ctx->origin[0] + ctx->spacing * static_cast<double>(ctx->dims[0] - 1),
@@ -667,6 +675,67 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
       for (uint32_t a = 0; a < n; ++a)
         if (seen[a]) mk[a >> 5] |= 1u << (a & 31);
     }
+    // DFS preorder from an atom outside every moving set: each moving set (the component of atom_j
+    // behind the bridge (i,j)) is then entered only through j and occupies one contiguous range
+    // [pos(j), pos(j) + |M|) — the layout the fast sweep's range loops need.
+    {
+      std::vector<char> in_any(n, 0);
+      std::vector<uint32_t> msize(v.nr, 0);
+      for (uint32_t r = 0; r < v.nr; ++r) {
+        const uint32_t* mk = masks + m.mask_base + r * W;
+        for (uint32_t a = 0; a < n; ++a)
+          if ((mk[a >> 5] >> (a & 31)) & 1u) {
+            in_any[a] = 1;
+            ++msize[r];
+          }
+      }
+      uint32_t root = 0;
+      while (root < n && in_any[root]) ++root;
+      bool ok = root < n && n <= 128;
+      if (root >= n) root = 0;
+      std::vector<uint32_t> order;
+      order.reserve(n);
+      std::vector<char> vis(n, 0);
+      std::vector<std::pair<uint32_t, uint32_t>> st;  // (atom, next neighbour slot)
+      st.push_back({root, adj.start[root]});
+      vis[root] = 1;
+      order.push_back(root);
+      while (!st.empty()) {
+        auto& top = st.back();
+        if (top.second == adj.start[top.first + 1]) {
+          st.pop_back();
+          continue;
+        }
+        const uint32_t w = adj.nbr[top.second++];
+        if (!vis[w]) {
+          vis[w] = 1;
+          order.push_back(w);
+          st.push_back({w, adj.start[w]});
+        }
+      }
+      std::vector<uint16_t> pos(n, 0);
+      for (uint32_t p = 0; p < order.size(); ++p) pos[order[p]] = uint16_t(p);
+      for (uint32_t a = 0; a < n; ++a) dfs[m.atom_base + a] = pos[a];
+      for (uint32_t r = 0; r < v.nr; ++r) {
+        const uint32_t i = v.rots[2 * r], j = v.rots[2 * r + 1];
+        const uint32_t s0 = pos[j], e0 = pos[j] + msize[r];
+        const uint32_t* mk = masks + m.mask_base + r * W;
+        for (uint32_t a = 0; a < n && ok; ++a) {
+          const bool mv = (mk[a >> 5] >> (a & 31)) & 1u;
+          ok = mv == (pos[a] >= s0 && pos[a] < e0);
+        }
+        rdfs[m.rot_base + r] = make_ushort4(uint16_t(s0), uint16_t(e0), uint16_t(pos[i]), 0);
+      }
+      uint32_t* ad = adjd + m.adj_base;
+      std::fill(ad, ad + size_t(n) * W, 0u);
+      for (uint32_t e = 0; e < v.nb; ++e) {
+        const uint32_t x = pos[v.bonds[2 * e]], y = pos[v.bonds[2 * e + 1]];
+        ad[x * W + (y >> 5)] |= 1u << (y & 31);
+        ad[y * W + (x >> 5)] |= 1u << (x & 31);
+      }
+      meta[l].fast_ok = ok ? 1u : 0u;
+      meta[l].npad = (n + 3) & ~3u;
+    }
     // starting transforms (generate_starting_pose, docking.cpp:52-69): q and target per restart.
     const uint64_t lig_seed = gdh::mix_seed(P.seed, gdh::fnv1a64(v.name));
     for (uint32_t pid = 0; pid < N; ++pid) {
@@ -707,6 +776,9 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
   d.dih0 = reinterpret_cast<const double*>(D + o_dih0);
   d.masks = reinterpret_cast<const uint32_t*>(D + o_masks);
   d.adj = reinterpret_cast<const uint32_t*>(D + o_adj);
+  d.dfs_pos = reinterpret_cast<const uint16_t*>(D + o_dfs);
+  d.rdfs = reinterpret_cast<const ushort4*>(D + o_rdfs);
+  d.adjd = reinterpret_cast<const uint32_t*>(D + o_adjd);
   d.rs_score = reinterpret_cast<double*>(D + o_rs_score);
   d.rs_align_score = reinterpret_cast<double*>(D + o_rs_ascore);
   d.rs_align_index = reinterpret_cast<uint32_t*>(D + o_rs_aidx);
@@ -732,7 +804,7 @@ int gd_run(gd_batch* b) {
   GD_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, 8 * sizeof(unsigned long long), ctx->stream));
   int launches = 0;
   DevParams pr = dev_params(ctx);
-  if (!(ctx->coarse_eps < 1.0f)) pr.mode = (pr.mode & ~0xff) | GD_MODE_EXACT;
+  if (!(ctx->q_eps < 1.0f)) pr.mode = (pr.mode & ~0xff) | GD_MODE_EXACT;
   const cudaError_t e = gdk::launch_dock(dev_pocket(ctx), pr, b->dev, ctx->n_sms, ctx->stream, &launches);
   ctx->last.launches = uint32_t(launches);
   if (e != cudaSuccess) return cuda_err(ctx, e, "launch_dock");

@@ -1,10 +1,806 @@
-// Two-stage fast path (placeholder until the coarse kernel lands).
+// K1 fast: two-stage pose search. DESIGN.md §3 has the derivation; paths are relative to
+// /root/reference/proj.
+//
+// Every decision the reference makes — the alignment argmax (docking.cpp:71-91), each dihedral
+// step's eligibility and argmax (docking.cpp:127-149) — is taken here in two stages:
+//   1. a coarse FP32 screen over ALL candidates (the faithful sweep: every rotation of every restart,
+//      every dihedral candidate's moved atoms and cross pairs), reading the pocket as 15-bit
+//      fixed-point 8-corner cells staged once per CTA in shared memory (one LDS.128 per sample);
+//   2. an exact FP64 re-evaluation, in the reference's arithmetic and summation order, of the few
+//      candidates whose coarse score lies within the rigorous error bound 2*eps of the best (plus
+//      any sample within the position bound of a grid face, plus any bump pair within its bound of
+//      the threshold). The argmax over the exact scores is therefore the reference's argmax.
+// Every pose, score and dihedral that leaves the kernel is FP64 and bit-identical to the reference.
+//
+// Work decomposition: persistent CTAs (one per SM), the pocket cells loaded once per CTA; each
+// warp claims (ligand, restart) items from a global counter. Lane layout: alignment = lanes over
+// rotations; dihedral sweep = lanes over candidate angles k (32 per pass, the remainder split
+// 2..32 lanes per candidate over the fixed atoms); FP64 master pose = atom a lives in lane a%32,
+// register slot a/32.
+#include "gd_exact.cuh"
 #include "gd_fast.cuh"
 
 namespace gdk {
+namespace {
 
-cudaError_t launch_fast(const DevPocket&, const DevParams&, const DevBatch&, int, cudaStream_t) {
-  return cudaErrorNotSupported;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr float kMagic = 8388608.0f;  // 2^23: RZ-add leaves floor(g) in the mantissa
+constexpr int KTOP = 4;               // per-lane top coarse alignment candidates kept
+constexpr int KAMB = 2;               // per-lane face-ambiguous rotations kept
+constexpr double kTwoPiD = 2.0 * 3.14159265358979323846;
+
+// status bits of a coarse dihedral candidate
+constexpr uint32_t ST_CLASH = 1, ST_OK = 2, ST_XAMB = 4, ST_SAMB = 8;
+
+struct CoarseGrid {
+  const uint4* cells;  // shared (or global) 8-corner cells
+  float hx, hy, hz;    // half extents (dims-1)/2 in grid units
+  uint32_t cx, cxy;    // cells per row / per plane
+};
+
+// One coarse sample at grid coordinates g. Returns 1 + v' (v' = trilinear of the
+// 15-bit codes u/32768) when strictly inside the grid, else exactly 1.0. amin tracks the smallest
+// L-inf distance of any sample to the grid boundary: a sample within the position bound of a face
+// may be classified differently from the FP64 reference, so its candidate is re-scored exactly.
+__device__ __forceinline__ float coarse_sample(const CoarseGrid& cg, float gx, float gy, float gz,
+                                               float& amin) {
+  const float e = fmaxf(fabsf(gx - cg.hx) - cg.hx, fmaxf(fabsf(gy - cg.hy) - cg.hy, fabsf(gz - cg.hz) - cg.hz));
+  amin = fminf(amin, fabsf(e));
+  const bool inside = e < 0.0f;
+  const float rx = __fadd_rz(gx, kMagic), ry = __fadd_rz(gy, kMagic), rz = __fadd_rz(gz, kMagic);
+  const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic), fz = gz - (rz - kMagic);
+  const uint32_t cell = (__float_as_uint(rx) - 0x4B000000u) + (__float_as_uint(ry) - 0x4B000000u) * cg.cx +
+                        (__float_as_uint(rz) - 0x4B000000u) * cg.cxy;
+  uint4 w = make_uint4(0x80008000u, 0x80008000u, 0x80008000u, 0x80008000u);
+  if (inside) w = cg.cells[cell];
+  // byte permute: half-word 0x8000|u -> float bits 0x3F800000 | u<<8 = 1 + u/32768
+  const float c000 = __uint_as_float(__byte_perm(w.x, 0x3F000000u, 0x7104));
+  const float c100 = __uint_as_float(__byte_perm(w.x, 0x3F000000u, 0x7324));
+  const float c010 = __uint_as_float(__byte_perm(w.y, 0x3F000000u, 0x7104));
+  const float c110 = __uint_as_float(__byte_perm(w.y, 0x3F000000u, 0x7324));
+  const float c001 = __uint_as_float(__byte_perm(w.z, 0x3F000000u, 0x7104));
+  const float c101 = __uint_as_float(__byte_perm(w.z, 0x3F000000u, 0x7324));
+  const float c011 = __uint_as_float(__byte_perm(w.w, 0x3F000000u, 0x7104));
+  const float c111 = __uint_as_float(__byte_perm(w.w, 0x3F000000u, 0x7324));
+  const float c00 = fmaf(fx, c100 - c000, c000);
+  const float c10 = fmaf(fx, c110 - c010, c010);
+  const float c01 = fmaf(fx, c101 - c001, c001);
+  const float c11 = fmaf(fx, c111 - c011, c011);
+  const float c0 = fmaf(fy, c10 - c00, c00);
+  const float c1 = fmaf(fy, c11 - c01, c01);
+  const float v = fmaf(fz, c1 - c0, c0);
+  return inside ? v : 1.0f;
+}
+
+// ------------------------------------------------------------------ FP64 register pose helpers
+template <int NS>
+struct Pose {
+  double x[NS], y[NS], z[NS];
+};
+
+template <int NS>
+__device__ __forceinline__ V3d own(const Pose<NS>& P, int s) {
+  return V3d{P.x[s], P.y[s], P.z[s]};
+}
+
+template <int NS>
+__device__ __forceinline__ void set_own(Pose<NS>& P, int s, V3d v) {
+  P.x[s] = v.x;
+  P.y[s] = v.y;
+  P.z[s] = v.z;
+}
+
+// Position of atom a (warp-uniform a) from its owner lane.
+template <int NS>
+__device__ __forceinline__ V3d fetch(const Pose<NS>& P, uint32_t a) {
+  const int slot = int(a >> 5), src = int(a & 31);
+  double vx = P.x[0], vy = P.y[0], vz = P.z[0];
+#pragma unroll
+  for (int s = 1; s < NS; ++s)
+    if (slot == s) {
+      vx = P.x[s];
+      vy = P.y[s];
+      vz = P.z[s];
+    }
+  return V3d{__shfl_sync(FULL, vx, src), __shfl_sync(FULL, vy, src), __shfl_sync(FULL, vz, src)};
+}
+
+// Index-order sum of per-atom values (the reference's left-to-right accumulation); every lane
+// performs the same additions in the same order, so every lane holds the same bits.
+template <int NS>
+__device__ __forceinline__ double ordered_sum(const double (&v)[NS], uint32_t n) {
+  double sum = 0.0;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    for (uint32_t l = 0; l < 32; ++l) {
+      if (uint32_t(s) * 32 + l >= n) break;
+      sum = __dadd_rn(sum, __shfl_sync(FULL, v[s], l));
+    }
+  }
+  return sum;
+}
+
+template <int NS>
+__device__ __forceinline__ V3d centroid_reg(const Pose<NS>& P, uint32_t n) {  // geometry.cpp:40-46
+  const V3d sum{ordered_sum<NS>(P.x, n), ordered_sum<NS>(P.y, n), ordered_sum<NS>(P.z, n)};
+  return vscale(__ddiv_rn(1.0, double(n)), sum);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+template <int NW>
+__device__ __forceinline__ bool bit4(const uint32_t (&m)[NW], uint32_t a) { return (m[a >> 5] >> (a & 31)) & 1u; }
+
+__device__ __forceinline__ Qd frag_quat(const double4& dt, V3d axis) {  // about_axis, geometry.hpp:46-50
+  return Qd{dt.x, __dmul_rn(axis.x, dt.y), __dmul_rn(axis.y, dt.y), __dmul_rn(axis.z, dt.y)};
+}
+
+struct Item {
+  uint32_t n, W, lig, rs;
+  LigMeta m;
+};
+
+// Exact FP64 test of the non-bonded pairs of candidate k (rotate: M' atoms rotated by q about pi).
+// cross_only: only pairs with exactly one atom in M' (the invariant pairs are known exactly).
+template <int NS>
+__device__ bool exact_clash(const DevBatch& b, const Item& it, const Pose<NS>& P, const double (&rad)[NS],
+                            const uint32_t (&mo)[NS], bool rotate, V3d pi, const Qd& q, double clash,
+                            bool cross_only, uint32_t lane) {
+  V3d pa[NS];
+#pragma unroll
+  for (int t = 0; t < NS; ++t) {
+    const uint32_t a = lane + 32 * t;
+    pa[t] = own(P, t);
+    if (rotate && a < it.n && bit4(mo, a)) pa[t] = rotated_about(pa[t], pi, q);
+  }
+  bool hit = false;
+  for (uint32_t bb = 0; bb < it.n; ++bb) {
+    V3d pb = fetch<NS>(P, bb);
+    const bool bm = bit4(mo, bb);
+    if (rotate && bm) pb = rotated_about(pb, pi, q);
+    const double rb = b.atoms[it.m.atom_base + bb].w;
+    const uint32_t* row = b.adj + it.m.adj_base + bb * it.W;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const uint32_t a = lane + 32 * t;
+      if (a >= it.n || a <= bb) continue;
+      if (cross_only && bit4(mo, a) == bm) continue;
+      if ((__ldg(row + (a >> 5)) >> (a & 31)) & 1u) continue;
+      hit |= pair_clash_exact(pa[t], pb, rad[t], rb, clash);
+    }
+  }
+  return __any_sync(FULL, hit);
+}
+
+// Exact score of dihedral candidate k > 0 (score_pose, scoring.cpp:40-45): M' atoms rotated and
+// sampled in FP64, the others from the exact per-atom cache, summed in atom order.
+template <int NS>
+__device__ double exact_candidate_score(const DevPocket& pk, const Item& it, const Pose<NS>& P,
+                                        const double (&es)[NS], const uint32_t (&mo)[NS], V3d pi,
+                                        const Qd& q, uint32_t lane) {
+  double ns[NS];
+#pragma unroll
+  for (int t = 0; t < NS; ++t) {
+    const uint32_t a = lane + 32 * t;
+    ns[t] = es[t];
+    if (a < it.n && bit4(mo, a)) ns[t] = sample_exact(pk, rotated_about(own(P, t), pi, q));
+  }
+  return __ddiv_rn(ordered_sum<NS>(ns, it.n), double(it.n));
+}
+
+}  // namespace
+
+// ============================================================================ the kernel
+template <int NS>
+__global__ void __launch_bounds__(1024, 1)
+    dock_fast_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t slot_floats, uint32_t cells_in_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
+  const uint4* cells = pk.cells;
+  float* slots = reinterpret_cast<float*>(smem_raw);
+  if (cells_in_smem) {  // stage the pocket once per CTA; every warp of every work item reads it
+    uint4* sc = reinterpret_cast<uint4*>(smem_raw);
+    for (uint32_t i = threadIdx.x; i < n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
+    cells = sc;
+    slots = reinterpret_cast<float*>(sc + n_cells);
+    __syncthreads();
+  }
+  float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
+  const CoarseGrid cg{cells, 0.5f * float(pk.cell_dims[0]), 0.5f * float(pk.cell_dims[1]),
+                      0.5f * float(pk.cell_dims[2]), pk.cell_dims[0], pk.cell_dims[0] * pk.cell_dims[1]};
+  const uint32_t N = pr.n_restarts;
+  const uint64_t total = uint64_t(b.n_lig) * N;
+  const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
+  unsigned long long st_aexact = 0, st_afall = 0, st_sexact = 0, st_sfall = 0, st_commit = 0, st_items = 0;
+
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(b.work_counter, 1u);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= total) break;
+    if (*(volatile int*)b.error != 0) break;
+    ++st_items;
+    Item it;
+    it.lig = item / N;
+    it.rs = item - it.lig * N;
+    it.m = b.meta[it.lig];
+    it.n = it.m.n;
+    it.W = (it.n + 31) >> 5;
+    const uint32_t n = it.n, R = it.m.nr;
+    double* gpose = b.rs_xyz + (size_t(it.m.atom_base) * N + size_t(it.rs) * n) * 3;
+
+    // ------------------------------------------------ starting pose (docking.cpp:52-69), FP64
+    Pose<NS> P;
+    uint32_t pos[NS];
+    double rad[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const uint32_t a = lane + 32 * s;
+      double4 at = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (a < n) at = b.atoms[it.m.atom_base + a];
+      set_own(P, s, V3d{at.x, at.y, at.z});
+      rad[s] = at.w;
+      pos[s] = a < n ? b.dfs_pos[it.m.atom_base + a] : 0;
+    }
+    {
+      const V3d c0 = centroid_reg<NS>(P, n);
+      const double4 q4 = b.start[2 * size_t(item)];
+      const double4 t4 = b.start[2 * size_t(item) + 1];
+      const Qd qs{q4.x, q4.y, q4.z, q4.w};
+      const V3d tgt{t4.x, t4.y, t4.z};
+#pragma unroll
+      for (int s = 0; s < NS; ++s) set_own(P, s, vadd(qapply(qs, vsub(own(P, s), c0)), tgt));
+    }
+    const V3d cen = centroid_reg<NS>(P, n);  // best_rotation_in_range's centroid (docking.cpp:76)
+    // FP64 start pose to global (read back by the exact refinement); FP32 coordinates relative to
+    // the centroid (A, DFS order) into this warp's shared slot.
+    float ext = 0.f;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const uint32_t a = lane + 32 * s;
+      if (a < n) {
+        gpose[3 * a] = P.x[s];
+        gpose[3 * a + 1] = P.y[s];
+        gpose[3 * a + 2] = P.z[s];
+        const V3d v = vsub(own(P, s), cen);
+        A[pos[s]] = make_float4(float(v.x), float(v.y), float(v.z), 0.f);
+        ext = fmaxf(ext, float(__dsqrt_rn(vdot(v, v))));
+      } else if (a < it.m.npad) {
+        A[a] = make_float4(1e6f, 1e6f, 1e6f, 0.f);  // padding: far outside, contributes exactly 1.0
+      }
+    }
+    __syncwarp();
+    // Position error bound (grid units, per axis) of every FP32 coordinate this item produces:
+    // rounding of coordinates up to the grid size, plus the rotation error of the FP32 frames
+    // (the dihedral axis from FP32 endpoints is good to ~1e-6 rad) times the ligand extent.
+    // DESIGN.md §3.2 derives the constants.
+    const float ext_g = warp_max(ext) * pk.inv_spacing_f;
+    const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
+    const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
+    const float eps = pk.q_eps + 3.0f * pk.max_step * ptol + 4e-6f;  // coarse score error bound
+    const float inv_n_scale = pk.coarse_scale / float(n);
+
+    // ------------------------------------------------ coarse alignment sweep (all G rotations)
+    const float tx = float(__ddiv_rn(__dsub_rn(cen.x, pk.origin[0]), pk.spacing));
+    const float ty = float(__ddiv_rn(__dsub_rn(cen.y, pk.origin[1]), pk.spacing));
+    const float tz = float(__ddiv_rn(__dsub_rn(cen.z, pk.origin[2]), pk.spacing));
+    float top_s[KTOP];
+    uint32_t top_g[KTOP];
+#pragma unroll
+    for (int t = 0; t < KTOP; ++t) {
+      top_s[t] = -1e30f;
+      top_g[t] = 0xffffffffu;
+    }
+    float dropped = -1e30f;
+    uint32_t amb_g[KAMB] = {0xffffffffu, 0xffffffffu};
+    uint32_t n_amb = 0;
+    const uint32_t npad = it.m.npad;
+    for (uint32_t g = lane; g < pr.G; g += 32) {
+      const float4 r0 = __ldg(pr.grid_f + 3 * g), r1 = __ldg(pr.grid_f + 3 * g + 1), r2 = __ldg(pr.grid_f + 3 * g + 2);
+      float acc0 = 0.f, acc1 = 0.f, amin = 1e30f;
+#pragma unroll 2
+      for (uint32_t a = 0; a < npad; a += 4) {
+        const float4 v0 = A[a], v1 = A[a + 1], v2 = A[a + 2], v3 = A[a + 3];
+        acc0 += coarse_sample(cg, fmaf(r0.x, v0.x, fmaf(r0.y, v0.y, fmaf(r0.z, v0.z, tx))),
+                              fmaf(r1.x, v0.x, fmaf(r1.y, v0.y, fmaf(r1.z, v0.z, ty))),
+                              fmaf(r2.x, v0.x, fmaf(r2.y, v0.y, fmaf(r2.z, v0.z, tz))), amin);
+        acc1 += coarse_sample(cg, fmaf(r0.x, v1.x, fmaf(r0.y, v1.y, fmaf(r0.z, v1.z, tx))),
+                              fmaf(r1.x, v1.x, fmaf(r1.y, v1.y, fmaf(r1.z, v1.z, ty))),
+                              fmaf(r2.x, v1.x, fmaf(r2.y, v1.y, fmaf(r2.z, v1.z, tz))), amin);
+        acc0 += coarse_sample(cg, fmaf(r0.x, v2.x, fmaf(r0.y, v2.y, fmaf(r0.z, v2.z, tx))),
+                              fmaf(r1.x, v2.x, fmaf(r1.y, v2.y, fmaf(r1.z, v2.z, ty))),
+                              fmaf(r2.x, v2.x, fmaf(r2.y, v2.y, fmaf(r2.z, v2.z, tz))), amin);
+        acc1 += coarse_sample(cg, fmaf(r0.x, v3.x, fmaf(r0.y, v3.y, fmaf(r0.z, v3.z, tx))),
+                              fmaf(r1.x, v3.x, fmaf(r1.y, v3.y, fmaf(r1.z, v3.z, ty))),
+                              fmaf(r2.x, v3.x, fmaf(r2.y, v3.y, fmaf(r2.z, v3.z, tz))), amin);
+      }
+      const float sc = ((acc0 - float(npad >> 1)) + (acc1 - float(npad >> 1))) * inv_n_scale;
+      if (amin <= ptol) {
+        if (n_amb < KAMB) amb_g[n_amb] = g;
+        ++n_amb;
+      } else if (sc > top_s[KTOP - 1]) {
+        dropped = fmaxf(dropped, top_s[KTOP - 1]);
+        float vs = sc;
+        uint32_t vg = g;
+#pragma unroll
+        for (int t = 0; t < KTOP; ++t) {  // sorted insert, descending
+          if (vs > top_s[t]) {
+            const float ts = top_s[t];
+            const uint32_t tg = top_g[t];
+            top_s[t] = vs;
+            top_g[t] = vg;
+            vs = ts;
+            vg = tg;
+          }
+        }
+      } else {
+        dropped = fmaxf(dropped, sc);
+      }
+    }
+    // warp merge: best coarse score B over face-unambiguous rotations; every rotation whose exact
+    // score can reach the exact maximum has coarse score >= B - 2 eps.
+    const float B = warp_max(top_s[0]);
+    const float thr = B - 2.0f * eps;
+    const bool overflow = __any_sync(FULL, dropped >= thr || n_amb > KAMB) || B < -1e29f;
+    double best_s = -1.0;
+    uint32_t best_g = 0xffffffffu;
+    if (overflow) {
+      ++st_afall;  // fallback: exact sweep of every rotation
+      for (uint32_t g = lane; g < pr.G; g += 32) {
+        const double4 gq = pr.grid[g];
+        const Qd q{gq.x, gq.y, gq.z, gq.w};
+        double sum = 0.0;
+        for (uint32_t a = 0; a < n; ++a) {
+          const V3d p{gpose[3 * a], gpose[3 * a + 1], gpose[3 * a + 2]};
+          sum = __dadd_rn(sum, sample_exact(pk, rotated_about(p, cen, q)));
+        }
+        const double s = __ddiv_rn(sum, double(n));
+        if (s > best_s || best_g == 0xffffffffu) {
+          best_s = s;
+          best_g = g;
+        }
+      }
+    } else {
+      uint32_t cand[KTOP + KAMB];
+#pragma unroll
+      for (int t = 0; t < KTOP; ++t) cand[t] = top_s[t] >= thr ? top_g[t] : 0xffffffffu;
+#pragma unroll
+      for (int t = 0; t < KAMB; ++t) cand[KTOP + t] = amb_g[t];
+#pragma unroll
+      for (int t = 0; t < KTOP + KAMB; ++t) {
+        const uint32_t g = cand[t];
+        if (g == 0xffffffffu) continue;
+        ++st_aexact;
+        const double4 gq = pr.grid[g];
+        const Qd q{gq.x, gq.y, gq.z, gq.w};
+        double sum = 0.0;
+        for (uint32_t a = 0; a < n; ++a) {
+          const V3d p{gpose[3 * a], gpose[3 * a + 1], gpose[3 * a + 2]};
+          sum = __dadd_rn(sum, sample_exact(pk, rotated_about(p, cen, q)));
+        }
+        const double s = __ddiv_rn(sum, double(n));
+        if (best_g == 0xffffffffu || s > best_s || (s == best_s && g < best_g)) {
+          best_s = s;
+          best_g = g;
+        }
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {  // combine (docking.cpp:93-108)
+      const double os = __shfl_xor_sync(FULL, best_s, off);
+      const uint32_t og = __shfl_xor_sync(FULL, best_g, off);
+      if (og != 0xffffffffu && (best_g == 0xffffffffu || os > best_s || (os == best_s && og < best_g))) {
+        best_s = os;
+        best_g = og;
+      }
+    }
+    {  // apply_rotation_choice (docking.cpp:110-118); the start pose is re-read from global so
+       // that no FP64 pose registers stay live across the alignment loop
+      const double4 gq = pr.grid[best_g];
+      const Qd q{gq.x, gq.y, gq.z, gq.w};
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const uint32_t a = lane + 32 * s;
+        V3d p{0.0, 0.0, 0.0};
+        if (a < n) p = V3d{gpose[3 * a], gpose[3 * a + 1], gpose[3 * a + 2]};
+        set_own(P, s, rotated_about(p, cen, q));
+        rad[s] = a < n ? b.atoms[it.m.atom_base + a].w : 0.0;
+        pos[s] = a < n ? b.dfs_pos[it.m.atom_base + a] : 0;
+      }
+    }
+    double score = best_s;
+    if (lane == 0) {
+      b.rs_align_index[item] = best_g;
+      b.rs_align_score[item] = best_s;
+    }
+    double* dih = b.rs_dih + size_t(it.m.rot_base) * N + size_t(it.rs) * R;
+    for (uint32_t r = lane; r < R; r += 32) dih[r] = b.dih0[it.m.rot_base + r];
+
+    // ------------------------------------------------ dihedral sweep (docking.cpp:155-167, 197-215)
+    if (R > 0 && pr.reps > 0 && pr.S > 0) {
+      // Per-pose caches, rebuilt after alignment and after every k != 0 commit:
+      //   A[pos]     FP32 (gx, gy, gz, rho = cf*r/spacing) in DFS order,
+      //   es, cs     exact FP64 and coarse per-atom samples, samb: coarse sample near a face,
+      //   crow       exact clash partners (DFS bit rows), arow: pairs within tau of the threshold.
+      double es[NS];
+      float cs[NS];
+      bool samb[NS];
+      uint32_t crow[NS][NS], arow[NS][NS];
+      float rho[NS];
+      float rmax = 0.f;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        rho[s] = float(__ddiv_rn(__dmul_rn(pr.clash, rad[s]), pk.spacing));
+        if (lane + 32 * s < n) rmax = fmaxf(rmax, rho[s]);
+      }
+      rmax = warp_max(rmax);
+      // |computed - exact| of d^2 - t^2 for pairs near the threshold (d ~ t <= 2 rmax):
+      // 2 d |dd| with |dd| <= 2 sqrt(3) ptol, plus FP32 rounding of t^2 and the chain.
+      const float tau = 16.0f * rmax * ptol + 4e-6f * rmax * rmax + 1e-6f;
+
+      auto refresh = [&](bool all, const uint32_t (&mo)[NS]) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const uint32_t a = lane + 32 * s;
+          if (a < n && (all || bit4(mo, a))) {
+            const float gx = float(__ddiv_rn(__dsub_rn(P.x[s], pk.origin[0]), pk.spacing));
+            const float gy = float(__ddiv_rn(__dsub_rn(P.y[s], pk.origin[1]), pk.spacing));
+            const float gz = float(__ddiv_rn(__dsub_rn(P.z[s], pk.origin[2]), pk.spacing));
+            A[pos[s]] = make_float4(gx, gy, gz, rho[s]);
+            es[s] = sample_exact(pk, own(P, s));
+            float am = 1e30f;
+            cs[s] = coarse_sample(cg, gx, gy, gz, am) - 1.0f;
+            samb[s] = am <= ptol;
+          }
+        }
+        __syncwarp();
+        bool any_amb = false;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+#pragma unroll
+          for (int w = 0; w < NS; ++w) {
+            crow[s][w] = 0u;
+            arow[s][w] = 0u;
+          }
+          const uint32_t a = lane + 32 * s;
+          if (a >= n) continue;
+          const float4 pa = A[pos[s]];
+          const uint32_t* adrow = b.adjd + it.m.adj_base + pos[s] * it.W;
+          for (uint32_t q = 0; q < n; ++q) {
+            const float4 pb = A[q];
+            const float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
+            const float t = pa.w + pb.w;
+            const float mg = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -t * t)));
+            if (q == pos[s] || ((__ldg(adrow + (q >> 5)) >> (q & 31)) & 1u)) continue;
+            if (mg < -tau) {
+              crow[s][q >> 5] |= 1u << (q & 31);
+            } else if (mg <= tau) {
+              arow[s][q >> 5] |= 1u << (q & 31);
+              any_amb = true;
+            }
+          }
+        }
+        if (__any_sync(FULL, any_amb)) {  // near-threshold pairs: exact FP64 verdict
+          for (uint32_t bb = 0; bb < n; ++bb) {
+            const V3d pb = fetch<NS>(P, bb);
+            const uint32_t q = b.dfs_pos[it.m.atom_base + bb];
+            const double rb = b.atoms[it.m.atom_base + bb].w;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+              if ((arow[s][q >> 5] >> (q & 31)) & 1u) {
+                if (pair_clash_exact(own(P, s), pb, rad[s], rb, pr.clash)) crow[s][q >> 5] |= 1u << (q & 31);
+              }
+            }
+          }
+        }
+      };
+      {
+        uint32_t none[NS];
+#pragma unroll
+        for (int w = 0; w < NS; ++w) none[w] = 0u;
+        refresh(true, none);
+      }
+
+      for (uint32_t rep = 0; rep < pr.reps; ++rep) {
+        for (uint32_t r = 0; r < R; ++r) {
+          const uint2 ij = b.rots[it.m.rot_base + r];
+          const ushort4 rd = b.rdfs[it.m.rot_base + r];
+          const uint32_t s0 = rd.x, e0 = rd.y, ipos = rd.z;
+          // M' = moving set minus atom_j (molecule.cpp:166-169), original and DFS bit spaces
+          uint32_t mo[NS], md[NS];
+#pragma unroll
+          for (int w = 0; w < NS; ++w) {
+            mo[w] = uint32_t(w) < it.W ? __ldg(b.masks + it.m.mask_base + r * it.W + w) : 0u;
+            md[w] = 0u;
+          }
+          mo[ij.y >> 5] &= ~(1u << (ij.y & 31));
+          bool inm[NS];
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const uint32_t a = lane + 32 * s;
+            inm[s] = a < n && bit4(mo, a);
+#pragma unroll
+            for (int w = 0; w < NS; ++w)
+              if (inm[s] && (pos[s] >> 5) == uint32_t(w)) md[w] |= 1u << (pos[s] & 31);
+          }
+#pragma unroll
+          for (int w = 0; w < NS; ++w)
+            for (int o = 16; o > 0; o >>= 1) md[w] |= __shfl_xor_sync(FULL, md[w], o);
+          // invariant pairs (both in M' or both outside) of the current pose: exact from crow
+          bool inv_l = false, frag_l = false, cne_l = false, famb_l = false;
+          float fsum = 0.f;
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            if (lane + 32 * s >= n) continue;
+#pragma unroll
+            for (int w = 0; w < NS; ++w) {
+              const uint32_t lo = 32u * w;
+              const uint32_t valid = lo + 32u <= n ? FULL : (lo >= n ? 0u : ((1u << (n - lo)) - 1u));
+              inv_l |= (crow[s][w] & (inm[s] ? md[w] : (~md[w] & valid))) != 0u;
+              if (inm[s]) frag_l |= (arow[s][w] & md[w]) != 0u;
+              cne_l |= crow[s][w] != 0u;
+            }
+            if (!inm[s]) {
+              fsum += cs[s];
+              famb_l |= samb[s];
+            }
+          }
+          const bool inv = __any_sync(FULL, inv_l);
+          const bool frag = __any_sync(FULL, frag_l);
+          const bool elig0 = !__any_sync(FULL, cne_l);  // k = 0: the current pose passes bump_check
+          const bool famb = __any_sync(FULL, famb_l);
+          fsum = warp_sum(fsum);
+          // FP64 axis (rotate_fragment, molecule.cpp:150-160) and DegenerateAxisError semantics
+          const V3d pi = fetch<NS>(P, ij.x);
+          const V3d pj = fetch<NS>(P, ij.y);
+          const V3d delta = vsub(pj, pi);
+          const double len = __dsqrt_rn(vdot(delta, delta));
+          const V3d axis = vscale(__ddiv_rn(1.0, len), delta);
+          if (pr.S > 1 && len < 1e-12) {
+            if (lane == 0 && atomicCAS(b.error, 0, GD_ERR_DEGENERATE_AXIS) == 0) b.error[1] = int(it.lig);
+            break;
+          }
+          int32_t step_k = -1;
+          const size_t trace_at = size_t(it.m.rot_base) * N * pr.reps + (size_t(it.rs) * pr.reps + rep) * R + r;
+          bool committed = false;
+          uint32_t bk = 0;
+          double bs = 0.0;
+
+          if (!it.m.fast_ok || frag || pr.S > 64 || pr.S < 2) {
+            // ---------------- slow path: every candidate exactly (non-tree layouts, pairs of the
+            // moving fragment within tau of the threshold, or unusual S)
+            ++st_sfall;
+            for (uint32_t k = 0; k < pr.S; ++k) {
+              const Qd q = frag_quat(pr.dtab[k], axis);
+              const double sk = k == 0 ? __ddiv_rn(ordered_sum<NS>(es, n), double(n))
+                                       : exact_candidate_score<NS>(pk, it, P, es, mo, pi, q, lane);
+              bool clash;
+              if (k == 0) clash = !elig0;
+              else if (frag) clash = exact_clash<NS>(b, it, P, rad, mo, true, pi, q, pr.clash, false, lane);
+              else clash = inv || exact_clash<NS>(b, it, P, rad, mo, true, pi, q, pr.clash, true, lane);
+              if (!clash && (!committed || sk > bs)) {
+                committed = true;
+                bk = k;
+                bs = sk;
+              }
+            }
+          } else if (!(skip_inv && inv)) {
+            // ---------------- coarse evaluation of every candidate k = 1 .. S-1 (faithful sweep)
+            const float4 fpi = A[ipos];
+            const float4 fpj = A[s0];
+            float ax = fpj.x - fpi.x, ay = fpj.y - fpi.y, az = fpj.z - fpi.z;
+            {
+              const float il = rsqrtf(fmaxf(ax * ax + ay * ay + az * az, 1e-30f));
+              ax *= il;
+              ay *= il;
+              az *= il;
+            }
+            float res_s[2] = {-1e30f, -1e30f};
+            uint32_t res_st[2] = {0u, 0u};
+            const uint32_t n_cand = pr.S - 1;  // k = 1 .. S-1
+            const uint32_t rem = n_cand > 32 ? n_cand - 32 : 0;
+            const uint32_t lg2 = rem <= 1 ? 5 : rem <= 2 ? 4 : rem <= 4 ? 3 : rem <= 8 ? 2 : rem <= 16 ? 1 : 0;
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass) {
+              if (pass == 1 && rem == 0) break;
+              const uint32_t sh = pass == 0 ? 0u : lg2;  // log2 of lanes per candidate
+              const uint32_t gs = 1u << sh;
+              const uint32_t grp = lane >> sh, sub = lane & (gs - 1);
+              const uint32_t k = pass == 0 ? lane + 1 : 33 + grp;
+              const bool active = pass == 0 ? (k <= n_cand) : (grp < rem);
+              float part = 0.f, amin = 1e30f, mmin = 1e30f;
+              if (active) {
+                const float2 cq = __ldg(pr.dtab_f + k);
+                const float qw = cq.x, qx = ax * cq.y, qy = ay * cq.y, qz = az * cq.y;
+                const float xx = qx * qx, yy = qy * qy, zz = qz * qz, xy = qx * qy, xz = qx * qz, yz = qy * qz;
+                const float wx = qw * qx, wy = qw * qy, wz = qw * qz;
+                const float m00 = 1.f - 2.f * (yy + zz), m01 = 2.f * (xy - wz), m02 = 2.f * (xz + wy);
+                const float m10 = 2.f * (xy + wz), m11 = 1.f - 2.f * (xx + zz), m12 = 2.f * (yz - wx);
+                const float m20 = 2.f * (xz - wy), m21 = 2.f * (yz + wx), m22 = 1.f - 2.f * (xx + yy);
+                const float tvx = fpi.x - fmaf(m00, fpi.x, fmaf(m01, fpi.y, m02 * fpi.z));
+                const float tvy = fpi.y - fmaf(m10, fpi.x, fmaf(m11, fpi.y, m12 * fpi.z));
+                const float tvz = fpi.z - fmaf(m20, fpi.x, fmaf(m21, fpi.y, m22 * fpi.z));
+                for (uint32_t mq = s0 + 1; mq < e0; ++mq) {
+                  const float4 pm = A[mq];
+                  const float gx = fmaf(m00, pm.x, fmaf(m01, pm.y, fmaf(m02, pm.z, tvx)));
+                  const float gy = fmaf(m10, pm.x, fmaf(m11, pm.y, fmaf(m12, pm.z, tvy)));
+                  const float gz = fmaf(m20, pm.x, fmaf(m21, pm.y, fmaf(m22, pm.z, tvz)));
+                  if (((mq - s0 - 1) & (gs - 1)) == sub) part += coarse_sample(cg, gx, gy, gz, amin) - 1.0f;
+                  // cross pairs with the fixed side [0, s0) U [e0, n) and with atom_j unless bonded
+                  for (uint32_t f = sub; f < s0; f += gs) {
+                    const float4 pf = A[f];
+                    const float dx = gx - pf.x, dy = gy - pf.y, dz = gz - pf.z, tt = pm.w + pf.w;
+                    mmin = fminf(mmin, fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -tt * tt))));
+                  }
+                  for (uint32_t f = e0 + sub; f < n; f += gs) {
+                    const float4 pf = A[f];
+                    const float dx = gx - pf.x, dy = gy - pf.y, dz = gz - pf.z, tt = pm.w + pf.w;
+                    mmin = fminf(mmin, fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -tt * tt))));
+                  }
+                  if (sub == 0 && !((__ldg(b.adjd + it.m.adj_base + mq * it.W + (s0 >> 5)) >> (s0 & 31)) & 1u)) {
+                    const float dx = gx - fpj.x, dy = gy - fpj.y, dz = gz - fpj.z, tt = pm.w + fpj.w;
+                    mmin = fminf(mmin, fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -tt * tt))));
+                  }
+                }
+              }
+              for (uint32_t o = 1; o < gs; o <<= 1) {  // group reduction (pass 2)
+                part += __shfl_xor_sync(FULL, part, o);
+                amin = fminf(amin, __shfl_xor_sync(FULL, amin, o));
+                mmin = fminf(mmin, __shfl_xor_sync(FULL, mmin, o));
+              }
+              uint32_t st = 0;
+              if (active) {
+                st = mmin < -tau ? ST_CLASH : (mmin >= tau ? ST_OK : ST_XAMB);
+                if (amin <= ptol || famb) st |= ST_SAMB;
+              }
+              const float sc = (fsum + part) * inv_n_scale;
+              if (pass == 0) {
+                res_s[0] = sc;
+                res_st[0] = st;
+              } else {
+                const float s2 = __shfl_sync(FULL, sc, (lane << sh) & 31);
+                const uint32_t t2 = __shfl_sync(FULL, st, (lane << sh) & 31);
+                if (lane < rem) {
+                  res_s[1] = s2;
+                  res_st[1] = t2;
+                }
+              }
+            }
+
+            // ---------------- exact decisions (reference semantics, docking.cpp:131-147)
+            if (!inv) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {  // cross pairs within tau of the threshold: exact
+                uint32_t pend = __ballot_sync(FULL, (res_st[h] & ST_XAMB) != 0u);
+                while (pend) {
+                  const uint32_t src = __ffs(pend) - 1;
+                  pend &= pend - 1;
+                  const uint32_t k = (h == 0 ? 1u : 33u) + src;
+                  ++st_sexact;
+                  const bool cl = exact_clash<NS>(b, it, P, rad, mo, true, pi, frag_quat(pr.dtab[k], axis),
+                                                  pr.clash, true, lane);
+                  if (lane == src) res_st[h] = (res_st[h] & ST_SAMB) | (cl ? ST_CLASH : ST_OK);
+                }
+              }
+              // coarse best over eligible, face-unambiguous candidates; lower bound on the exact max
+              float Bl = -1e30f;
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                if ((res_st[h] & ST_OK) && !(res_st[h] & ST_SAMB)) Bl = fmaxf(Bl, res_s[h]);
+              Bl = warp_max(Bl);
+              float lb = Bl - eps;
+              if (elig0) {  // k = 0: the current pose, score_pose(current) == the carried score
+                committed = true;
+                bk = 0;
+                bs = score;
+                lb = fmaxf(lb, float(score) - 1e-6f);
+              }
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const bool need = (res_st[h] & ST_OK) && ((res_st[h] & ST_SAMB) || res_s[h] + eps >= lb);
+                uint32_t pend = __ballot_sync(FULL, need);
+                while (pend) {
+                  const uint32_t src = __ffs(pend) - 1;
+                  pend &= pend - 1;
+                  const uint32_t k = (h == 0 ? 1u : 33u) + src;
+                  ++st_sexact;
+                  const double sk = exact_candidate_score<NS>(pk, it, P, es, mo, pi, frag_quat(pr.dtab[k], axis), lane);
+                  if (!committed || sk > bs || (sk == bs && k < bk)) {
+                    committed = true;
+                    bk = k;
+                    bs = sk;
+                  }
+                }
+              }
+            }
+          }
+          if (committed) {
+            step_k = int32_t(bk);
+            score = bs;
+            ++st_commit;
+            if (bk != 0) {  // commit = rotate_fragment(current, r, k*delta), FP64
+              const double4 dt = pr.dtab[bk];
+              const Qd q = frag_quat(dt, axis);
+#pragma unroll
+              for (int s = 0; s < NS; ++s)
+                if (inm[s]) set_own(P, s, rotated_about(own(P, s), pi, q));
+              if (lane == 0) {  // molecule.cpp:170-172
+                double d = fmod(__dadd_rn(dih[r], dt.z), kTwoPiD);
+                if (d < 0.0) d = __dadd_rn(d, kTwoPiD);
+                dih[r] = d;
+              }
+              refresh(false, mo);
+            }
+          }
+          if (lane == 0) b.rs_step_k[trace_at] = step_k;
+        }
+        if (*(volatile int*)b.error != 0) break;
+      }
+    }
+    if (*(volatile int*)b.error != 0) break;
+    // ------------------------------------------------ restart result
+    if (lane == 0) b.rs_score[item] = score;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const uint32_t a = lane + 32 * s;
+      if (a < n) {
+        gpose[3 * a] = P.x[s];
+        gpose[3 * a + 1] = P.y[s];
+        gpose[3 * a + 2] = P.z[s];
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    atomicAdd(b.stats + 0, st_items);
+    atomicAdd(b.stats + 1, st_aexact);
+    atomicAdd(b.stats + 2, st_afall);
+    atomicAdd(b.stats + 3, st_sexact);
+    atomicAdd(b.stats + 4, st_sfall);
+    atomicAdd(b.stats + 5, st_commit);
+  }
+}
+
+template <int NS>
+static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
+                             cudaStream_t stream) {
+  const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
+  const size_t cell_bytes = size_t(n_cells) * sizeof(uint4);
+  const uint32_t npad_max = (b.max_n + 3) & ~3u;
+  const uint32_t slot_floats = 4 * npad_max;
+  const size_t slot_bytes = size_t(slot_floats) * sizeof(float);
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const uint32_t cells_in_smem = cell_bytes + 8 * slot_bytes <= size_t(optin) ? 1u : 0u;
+  const size_t avail = size_t(optin) - (cells_in_smem ? cell_bytes : 0);
+  int warps = int(avail / slot_bytes);
+  if (warps > 32) warps = 32;
+  if (warps < 1) return cudaErrorInvalidConfiguration;
+  const size_t smem = (cells_in_smem ? cell_bytes : 0) + slot_bytes * warps;
+  cudaError_t e = cudaFuncSetAttribute(dock_fast_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  dock_fast_kernel<NS><<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, slot_floats, cells_in_smem);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
+                        cudaStream_t stream) {
+  if (b.max_n <= 32) return launch_ns<1>(pk, pr, b, n_sms, stream);
+  if (b.max_n <= 64) return launch_ns<2>(pk, pr, b, n_sms, stream);
+  if (b.max_n <= 128) return launch_ns<4>(pk, pr, b, n_sms, stream);
+  return cudaErrorNotSupported;  // launch_dock routes > 128 atoms to the exact kernel
 }
 
 }  // namespace gdk

@@ -21,8 +21,9 @@ struct LigMeta {
   uint32_t adj_base;   // bonded row of atom a: adj[adj_base + a*W .. +W)
   uint16_t n;          // atoms
   uint16_t nr;         // rotamers
-  uint32_t pad0;
-  uint64_t pad1;
+  uint32_t fast_ok;    // 1: every rotamer's moving set is a contiguous DFS range (fast sweep)
+  uint32_t npad;       // atoms rounded up to a multiple of 4 (coarse alignment loop)
+  uint32_t pad1;
 };
 static_assert(sizeof(LigMeta) == 32, "LigMeta layout");
 
@@ -36,9 +37,9 @@ struct DevPocket {
   double spacing;
   double maxc[3];        // dims - 1 as doubles (sample_field's outside test, scoring.cpp:16-18)
   float inv_spacing_f;
-  float coarse_eps;      // per-sample error bound of the coarse path
+  float q_eps;           // quantisation bound of the 15-bit cells: 0.5/32767 (inf: fast path off)
   float coarse_scale;    // 32768/32767: undoes the 15-bit encode scale
-  float pad;
+  float max_step;        // max |v(i+1) - v(i)| along any axis: slope bound per grid unit
 };
 
 // Search parameters as seen by the kernels.
@@ -68,7 +69,11 @@ struct DevBatch {
   const uint2* rots;       // (atom_i, atom_j)
   const double* dih0;      // initial dihedrals
   const uint32_t* masks;   // moving bitmasks
-  const uint32_t* adj;     // bonded bitmask rows
+  const uint32_t* adj;     // bonded bitmask rows (original atom order)
+  // fast-path layout: atoms in DFS preorder so every moving set is a contiguous range
+  const uint16_t* dfs_pos; // original atom -> DFS position
+  const ushort4* rdfs;     // per rotamer: (s = DFS pos of j, e = end of moving range, DFS pos of i, 0)
+  const uint32_t* adjd;    // bonded bitmask rows in DFS space: adjd[adj_base + pos*W + w]
   // per-restart scratch / trace
   double* rs_score;
   double* rs_align_score;

@@ -263,7 +263,7 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
   if (e != cudaSuccess) return e;
   if (b.n_lig == 0) return cudaSuccess;
   const int mode = pr.mode & 0xff;
-  if (mode == GD_MODE_EXACT) {
+  if (mode == GD_MODE_EXACT || b.max_n > 128) {  // the fast kernel keeps <= 128 atoms in registers
     const uint32_t stride = 7 * b.max_n;  // doubles per warp
     const size_t per_warp = size_t(stride) * sizeof(double);
     int warps = int((200 * 1024) / per_warp);
