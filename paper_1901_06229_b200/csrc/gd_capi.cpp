@@ -924,6 +924,16 @@ void gd_batch_free(gd_batch* b) {
 
 int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
   if (!ctx || !out) return GD_ERR_ARGUMENT;
+  // device counters of the last gd_run (synchronises the context stream)
+  unsigned long long st[8];
+  GD_CUDA(ctx, cudaMemcpyAsync(st, ctx->d_stats, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->last.restarts = st[0];
+  ctx->last.align_exact_evals = st[1];
+  ctx->last.align_fallbacks = st[2];
+  ctx->last.step_exact_evals = st[3];
+  ctx->last.step_fallbacks = st[4];
+  ctx->last.commits = st[5];
   *out = ctx->last;
   return GD_OK;
 }

@@ -26,8 +26,18 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr float kMagic = 8388608.0f;  // 2^23: RZ-add leaves floor(g) in the mantissa
 constexpr int KTOP = 4;               // per-lane top coarse alignment candidates kept
-constexpr int KAMB = 2;               // per-lane face-ambiguous rotations kept
 constexpr double kTwoPiD = 2.0 * 3.14159265358979323846;
+
+#ifndef GD_ALIGN_UNROLL
+#define GD_ALIGN_UNROLL 1
+#endif
+#ifndef GD_FAST_THREADS
+#define GD_FAST_THREADS 512
+#endif
+constexpr int kAlignUnroll = GD_ALIGN_UNROLL;
+#ifndef GD_FAST_THREADS_NS4
+#define GD_FAST_THREADS_NS4 512
+#endif
 
 // status bits of a coarse dihedral candidate
 constexpr uint32_t ST_CLASH = 1, ST_OK = 2, ST_XAMB = 4, ST_SAMB = 8;
@@ -51,8 +61,7 @@ __device__ __forceinline__ float coarse_sample(const CoarseGrid& cg, float gx, f
   const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic), fz = gz - (rz - kMagic);
   const uint32_t cell = (__float_as_uint(rx) - 0x4B000000u) + (__float_as_uint(ry) - 0x4B000000u) * cg.cx +
                         (__float_as_uint(rz) - 0x4B000000u) * cg.cxy;
-  uint4 w = make_uint4(0x80008000u, 0x80008000u, 0x80008000u, 0x80008000u);
-  if (inside) w = cg.cells[cell];
+  const uint4 w = cg.cells[inside ? cell : 0u];
   // byte permute: half-word 0x8000|u -> float bits 0x3F800000 | u<<8 = 1 + u/32768
   const float c000 = __uint_as_float(__byte_perm(w.x, 0x3F000000u, 0x7104));
   const float c100 = __uint_as_float(__byte_perm(w.x, 0x3F000000u, 0x7324));
@@ -70,6 +79,21 @@ __device__ __forceinline__ float coarse_sample(const CoarseGrid& cg, float gx, f
   const float c1 = fmaf(fy, c11 - c01, c01);
   const float v = fmaf(fz, c1 - c0, c0);
   return inside ? v : 1.0f;
+}
+
+// Interval form of coarse_sample for rotations with a sample near a face: a sample within ptol of
+// the boundary may be inside or outside in FP64, so it contributes [0, v_in] with v_in sampled at
+// the point clamped onto the grid (the clamp moves it by <= ptol, covered by one more eps).
+__device__ __forceinline__ void coarse_sample_iv(const CoarseGrid& cg, float gx, float gy, float gz, float ptol,
+                                                 float& lo, float& hi) {
+  const float e = fmaxf(fabsf(gx - cg.hx) - cg.hx, fmaxf(fabsf(gy - cg.hy) - cg.hy, fabsf(gz - cg.hz) - cg.hz));
+  if (e > ptol) return;
+  float am = 0.f;
+  const float v = coarse_sample(cg, fminf(fmaxf(gx, 0.f), 2.f * cg.hx - 1e-3f),
+                                fminf(fmaxf(gy, 0.f), 2.f * cg.hy - 1e-3f),
+                                fminf(fmaxf(gz, 0.f), 2.f * cg.hz - 1e-3f), am) - 1.0f;
+  hi += v;
+  if (e < -ptol) lo += v;
 }
 
 // ------------------------------------------------------------------ FP64 register pose helpers
@@ -112,6 +136,7 @@ __device__ __forceinline__ double ordered_sum(const double (&v)[NS], uint32_t n)
   double sum = 0.0;
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
+#pragma unroll 1
     for (uint32_t l = 0; l < 32; ++l) {
       if (uint32_t(s) * 32 + l >= n) break;
       sum = __dadd_rn(sum, __shfl_sync(FULL, v[s], l));
@@ -149,6 +174,21 @@ struct Item {
   uint32_t n, W, lig, rs;
   LigMeta m;
 };
+
+// The exact FP64 sampler and whole-rotation scorer are out-of-line: they run on rare paths and
+// inlining them at every call site blew the kernel past the instruction cache.
+__device__ __noinline__ double sample_exact_ni(const DevPocket& pk, V3d p) { return sample_exact(pk, p); }
+
+// best_rotation_in_range's score of rotation q (docking.cpp:77-83), atoms in index order.
+__device__ __noinline__ double exact_rotation_score(const DevPocket& pk, const double* gpose, uint32_t n, V3d cen,
+                                                    Qd q) {
+  double sum = 0.0;
+  for (uint32_t a = 0; a < n; ++a) {
+    const V3d p{gpose[3 * a], gpose[3 * a + 1], gpose[3 * a + 2]};
+    sum = __dadd_rn(sum, sample_exact(pk, rotated_about(p, cen, q)));
+  }
+  return __ddiv_rn(sum, double(n));
+}
 
 // Exact FP64 test of the non-bonded pairs of candidate k (rotate: M' atoms rotated by q about pi).
 // cross_only: only pairs with exactly one atom in M' (the invariant pairs are known exactly).
@@ -193,7 +233,7 @@ __device__ double exact_candidate_score(const DevPocket& pk, const Item& it, con
   for (int t = 0; t < NS; ++t) {
     const uint32_t a = lane + 32 * t;
     ns[t] = es[t];
-    if (a < it.n && bit4(mo, a)) ns[t] = sample_exact(pk, rotated_about(own(P, t), pi, q));
+    if (a < it.n && bit4(mo, a)) ns[t] = sample_exact_ni(pk, rotated_about(own(P, t), pi, q));
   }
   return __ddiv_rn(ordered_sum<NS>(ns, it.n), double(it.n));
 }
@@ -201,8 +241,10 @@ __device__ double exact_candidate_score(const DevPocket& pk, const Item& it, con
 }  // namespace
 
 // ============================================================================ the kernel
-template <int NS>
-__global__ void __launch_bounds__(1024, 1)
+// NT = threads per CTA (launch bound): 64 registers at 1024 threads spilled the smem bases inside
+// the hot loops, so the kernel trades warps for registers.
+template <int NS, int NT>
+__global__ void __launch_bounds__(NT, 1)
     dock_fast_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t slot_floats, uint32_t cells_in_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = threadIdx.x & 31;
@@ -293,6 +335,11 @@ __global__ void __launch_bounds__(1024, 1)
     const float inv_n_scale = pk.coarse_scale / float(n);
 
     // ------------------------------------------------ coarse alignment sweep (all G rotations)
+    // Lane l scores rotations g = l + 32 j. Per rotation the exact FP64 score lies in
+    // [key_lo - eps, key_hi + eps] (key = coarse score, or for a rotation with a sample within ptol
+    // of a face, the interval bounds from the second pass). Kept per lane: the KTOP largest key_hi,
+    // the largest key_hi that was dropped, the largest key_lo. A rotation can be the exact argmax
+    // only if key_hi >= max(key_lo) - 2 eps.
     const float tx = float(__ddiv_rn(__dsub_rn(cen.x, pk.origin[0]), pk.spacing));
     const float ty = float(__ddiv_rn(__dsub_rn(cen.y, pk.origin[1]), pk.spacing));
     const float tz = float(__ddiv_rn(__dsub_rn(cen.z, pk.origin[2]), pk.spacing));
@@ -303,14 +350,34 @@ __global__ void __launch_bounds__(1024, 1)
       top_s[t] = -1e30f;
       top_g[t] = 0xffffffffu;
     }
-    float dropped = -1e30f;
-    uint32_t amb_g[KAMB] = {0xffffffffu, 0xffffffffu};
-    uint32_t n_amb = 0;
+    float dropped = -1e30f, lkey = -1e30f;
+    unsigned long long amb_mask = 0ull;  // rotations j (g = lane + 32 j) with a face-ambiguous sample
     const uint32_t npad = it.m.npad;
-    for (uint32_t g = lane; g < pr.G; g += 32) {
+    const bool big_grid = pr.G > 64u * 32u;
+    auto insert = [&](float key_hi, uint32_t g) {
+      if (key_hi > top_s[KTOP - 1]) {
+        dropped = fmaxf(dropped, top_s[KTOP - 1]);
+        float vs = key_hi;
+        uint32_t vg = g;
+#pragma unroll
+        for (int t = 0; t < KTOP; ++t) {  // sorted insert, descending
+          if (vs > top_s[t]) {
+            const float ts = top_s[t];
+            const uint32_t tg = top_g[t];
+            top_s[t] = vs;
+            top_g[t] = vg;
+            vs = ts;
+            vg = tg;
+          }
+        }
+      } else {
+        dropped = fmaxf(dropped, key_hi);
+      }
+    };
+    for (uint32_t g = lane, j = 0; g < pr.G; g += 32, ++j) {
       const float4 r0 = __ldg(pr.grid_f + 3 * g), r1 = __ldg(pr.grid_f + 3 * g + 1), r2 = __ldg(pr.grid_f + 3 * g + 2);
       float acc0 = 0.f, acc1 = 0.f, amin = 1e30f;
-#pragma unroll 2
+#pragma unroll kAlignUnroll
       for (uint32_t a = 0; a < npad; a += 4) {
         const float4 v0 = A[a], v1 = A[a + 1], v2 = A[a + 2], v3 = A[a + 3];
         acc0 += coarse_sample(cg, fmaf(r0.x, v0.x, fmaf(r0.y, v0.y, fmaf(r0.z, v0.z, tx))),
@@ -328,73 +395,51 @@ __global__ void __launch_bounds__(1024, 1)
       }
       const float sc = ((acc0 - float(npad >> 1)) + (acc1 - float(npad >> 1))) * inv_n_scale;
       if (amin <= ptol) {
-        if (n_amb < KAMB) amb_g[n_amb] = g;
-        ++n_amb;
-      } else if (sc > top_s[KTOP - 1]) {
-        dropped = fmaxf(dropped, top_s[KTOP - 1]);
-        float vs = sc;
-        uint32_t vg = g;
-#pragma unroll
-        for (int t = 0; t < KTOP; ++t) {  // sorted insert, descending
-          if (vs > top_s[t]) {
-            const float ts = top_s[t];
-            const uint32_t tg = top_g[t];
-            top_s[t] = vs;
-            top_g[t] = vg;
-            vs = ts;
-            vg = tg;
-          }
-        }
+        amb_mask |= (j < 64 ? 1ull << j : 0ull);
+        if (j >= 64) lkey = 1e30f;  // cannot track: forces the exact fallback below
       } else {
-        dropped = fmaxf(dropped, sc);
+        insert(sc, g);
+        lkey = fmaxf(lkey, sc);
       }
     }
-    // warp merge: best coarse score B over face-unambiguous rotations; every rotation whose exact
-    // score can reach the exact maximum has coarse score >= B - 2 eps.
-    const float B = warp_max(top_s[0]);
+    // second pass over face-ambiguous rotations: interval bounds (rare; z-face ambiguities come
+    // in groups of 16 rotations that share (beta, gamma) and therefore the z coordinate)
+    for (unsigned long long mk = amb_mask; mk; mk &= mk - 1) {
+      const uint32_t g = lane + 32u * uint32_t(__ffsll(static_cast<long long>(mk)) - 1);
+      const float4 r0 = __ldg(pr.grid_f + 3 * g), r1 = __ldg(pr.grid_f + 3 * g + 1), r2 = __ldg(pr.grid_f + 3 * g + 2);
+      float lo = 0.f, hi = 0.f;
+#pragma unroll 1
+      for (uint32_t a = 0; a < npad; ++a) {
+        const float4 v = A[a];
+        coarse_sample_iv(cg, fmaf(r0.x, v.x, fmaf(r0.y, v.y, fmaf(r0.z, v.z, tx))),
+                         fmaf(r1.x, v.x, fmaf(r1.y, v.y, fmaf(r1.z, v.z, ty))),
+                         fmaf(r2.x, v.x, fmaf(r2.y, v.y, fmaf(r2.z, v.z, tz))), ptol, lo, hi);
+      }
+      insert(hi * inv_n_scale + eps, g);  // one extra eps for the clamp
+      lkey = fmaxf(lkey, lo * inv_n_scale);
+    }
+    const float B = warp_max(lkey);
     const float thr = B - 2.0f * eps;
-    const bool overflow = __any_sync(FULL, dropped >= thr || n_amb > KAMB) || B < -1e29f;
+    const bool overflow = __any_sync(FULL, dropped >= thr) || B < -1e29f || B > 1e29f || big_grid;
+    // exact FP64 re-scoring: the candidates, or (overflow) every rotation; one code path
+    unsigned long long todo = 0ull;
+    if (overflow) {
+      ++st_afall;
+    } else {
+#pragma unroll
+      for (int t = 0; t < KTOP; ++t)
+        if (top_s[t] >= thr) todo |= 1ull << ((top_g[t] - lane) >> 5);
+    }
     double best_s = -1.0;
     uint32_t best_g = 0xffffffffu;
-    if (overflow) {
-      ++st_afall;  // fallback: exact sweep of every rotation
-      for (uint32_t g = lane; g < pr.G; g += 32) {
-        const double4 gq = pr.grid[g];
-        const Qd q{gq.x, gq.y, gq.z, gq.w};
-        double sum = 0.0;
-        for (uint32_t a = 0; a < n; ++a) {
-          const V3d p{gpose[3 * a], gpose[3 * a + 1], gpose[3 * a + 2]};
-          sum = __dadd_rn(sum, sample_exact(pk, rotated_about(p, cen, q)));
-        }
-        const double s = __ddiv_rn(sum, double(n));
-        if (s > best_s || best_g == 0xffffffffu) {
-          best_s = s;
-          best_g = g;
-        }
-      }
-    } else {
-      uint32_t cand[KTOP + KAMB];
-#pragma unroll
-      for (int t = 0; t < KTOP; ++t) cand[t] = top_s[t] >= thr ? top_g[t] : 0xffffffffu;
-#pragma unroll
-      for (int t = 0; t < KAMB; ++t) cand[KTOP + t] = amb_g[t];
-#pragma unroll
-      for (int t = 0; t < KTOP + KAMB; ++t) {
-        const uint32_t g = cand[t];
-        if (g == 0xffffffffu) continue;
-        ++st_aexact;
-        const double4 gq = pr.grid[g];
-        const Qd q{gq.x, gq.y, gq.z, gq.w};
-        double sum = 0.0;
-        for (uint32_t a = 0; a < n; ++a) {
-          const V3d p{gpose[3 * a], gpose[3 * a + 1], gpose[3 * a + 2]};
-          sum = __dadd_rn(sum, sample_exact(pk, rotated_about(p, cen, q)));
-        }
-        const double s = __ddiv_rn(sum, double(n));
-        if (best_g == 0xffffffffu || s > best_s || (s == best_s && g < best_g)) {
-          best_s = s;
-          best_g = g;
-        }
+    for (uint32_t g = lane, j = 0; g < pr.G; g += 32, ++j) {
+      if (!overflow && (j >= 64 || !((todo >> j) & 1ull))) continue;
+      if (!overflow) ++st_aexact;
+      const double4 gq = pr.grid[g];
+      const double s = exact_rotation_score(pk, gpose, n, cen, Qd{gq.x, gq.y, gq.z, gq.w});
+      if (best_g == 0xffffffffu || s > best_s) {  // g ascending within a lane: first max wins
+        best_s = s;
+        best_g = g;
       }
     }
     for (int off = 16; off > 0; off >>= 1) {  // combine (docking.cpp:93-108)
@@ -458,7 +503,7 @@ __global__ void __launch_bounds__(1024, 1)
             const float gy = float(__ddiv_rn(__dsub_rn(P.y[s], pk.origin[1]), pk.spacing));
             const float gz = float(__ddiv_rn(__dsub_rn(P.z[s], pk.origin[2]), pk.spacing));
             A[pos[s]] = make_float4(gx, gy, gz, rho[s]);
-            es[s] = sample_exact(pk, own(P, s));
+            es[s] = sample_exact_ni(pk, own(P, s));
             float am = 1e30f;
             cs[s] = coarse_sample(cg, gx, gy, gz, am) - 1.0f;
             samb[s] = am <= ptol;
@@ -772,7 +817,7 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
-template <int NS>
+template <int NS, int NT>
 static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                              cudaStream_t stream) {
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
@@ -786,20 +831,20 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   const uint32_t cells_in_smem = cell_bytes + 8 * slot_bytes <= size_t(optin) ? 1u : 0u;
   const size_t avail = size_t(optin) - (cells_in_smem ? cell_bytes : 0);
   int warps = int(avail / slot_bytes);
-  if (warps > 32) warps = 32;
+  if (warps > NT / 32) warps = NT / 32;
   if (warps < 1) return cudaErrorInvalidConfiguration;
   const size_t smem = (cells_in_smem ? cell_bytes : 0) + slot_bytes * warps;
-  cudaError_t e = cudaFuncSetAttribute(dock_fast_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaError_t e = cudaFuncSetAttribute(dock_fast_kernel<NS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  dock_fast_kernel<NS><<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, slot_floats, cells_in_smem);
+  dock_fast_kernel<NS, NT><<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, slot_floats, cells_in_smem);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                         cudaStream_t stream) {
-  if (b.max_n <= 32) return launch_ns<1>(pk, pr, b, n_sms, stream);
-  if (b.max_n <= 64) return launch_ns<2>(pk, pr, b, n_sms, stream);
-  if (b.max_n <= 128) return launch_ns<4>(pk, pr, b, n_sms, stream);
+  if (b.max_n <= 32) return launch_ns<1, GD_FAST_THREADS>(pk, pr, b, n_sms, stream);
+  if (b.max_n <= 64) return launch_ns<2, GD_FAST_THREADS>(pk, pr, b, n_sms, stream);
+  if (b.max_n <= 128) return launch_ns<4, GD_FAST_THREADS_NS4>(pk, pr, b, n_sms, stream);
   return cudaErrorNotSupported;  // launch_dock routes > 128 atoms to the exact kernel
 }
 
