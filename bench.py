@@ -187,15 +187,10 @@ def run_ours(args):
     def step():
         batch.run()
         hits = batch.topk(topk)  # K3 + D2H of k records (tiny)
-        if pg is not None:
-            t = torch.tensor([[h[0], h[1] + rank * per_gpu, h[2]] for h in hits], dtype=torch.float64,
-                             device=dev)
-            out = [torch.empty_like(t) for _ in range(world)]
+        if pg is not None:  # the one exchange: all-gather of every rank's top-k (NCCL)
+            from paper_1901_06229_b200.distributed import gather_topk
             with torch.cuda.stream(stream):
-                pg.all_gather(out, t)
-            merged = torch.cat(out)
-            order = sorted(range(merged.shape[0]), key=lambda i: (-merged[i, 0].item(), merged[i, 1].item()))
-            hits = [tuple(merged[i].tolist()) for i in order[:topk]]
+                hits = gather_topk([(s, i + rank * per_gpu, r) for s, i, r in hits], topk, torch.device("cuda", dev))
         return hits
 
     for _ in range(args.warmup):
@@ -249,9 +244,9 @@ def run_ours(args):
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         e2e_s = t.item()
-    A, Rt = int(lib.atom_off[-1]), int(lib.rot_off[-1])
-    h2d = batch_bytes = int(stats.get("h2d_bytes", 0))
-    d2h = int(stats.get("d2h_bytes", 0))
+    e2e_stats = ctx.stats()
+    h2d = int(e2e_stats.get("h2d_bytes", 0))
+    d2h = int(e2e_stats.get("d2h_bytes", 0))
 
     # sanity: results of the timed batch equal the e2e call's
     chk = batch.fetch()
