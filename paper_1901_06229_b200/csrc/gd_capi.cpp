@@ -49,6 +49,7 @@ struct gd_ctx {
   bool have_params = false;
   double4* d_grid = nullptr;
   float4* d_grid_f = nullptr;
+  float4* d_frames = nullptr;
   double4* d_dtab = nullptr;
   float2* d_dtab_f = nullptr;
   uint32_t G = 0;
@@ -326,6 +327,28 @@ int upload_grid_f(gd_ctx* ctx) {
     }
   }
   GD_CUDA(ctx, cudaMemcpy(ctx->d_grid_f, rows.data(), sizeof(float4) * rows.size(), cudaMemcpyHostToDevice));
+  // frames F_jk = Ry(beta_j) Rz(gamma_k) / spacing: R_g = Rz(alpha_i) F_jk for g = (i*b + j)*c + k
+  const uint32_t* st = ctx->params.rotation_steps;
+  const uint32_t nf = st[1] * st[2];
+  std::vector<float4> fr(3 * size_t(std::max<uint32_t>(nf, 1)));
+  for (unsigned j = 0; j < st[1]; ++j) {
+    const double beta = st[1] == 1 ? 0.0 : gdh::kPi * static_cast<double>(j) / static_cast<double>(st[1] - 1);
+    for (unsigned k = 0; k < st[2]; ++k) {
+      const double gamma = gdh::kTwoPi * static_cast<double>(k) / static_cast<double>(st[2]);
+      const gdh::Q q = gdh::compose(gdh::about_axis(0.0, 1.0, 0.0, beta), gdh::about_axis(0.0, 0.0, 1.0, gamma));
+      const double w = q.w, x = q.x, y = q.y, z = q.z;
+      const double m[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                              {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                              {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+      const size_t f = size_t(j) * st[2] + k;
+      for (int r = 0; r < 3; ++r)
+        fr[3 * f + r] = make_float4(float(m[r][0] * inv), float(m[r][1] * inv), float(m[r][2] * inv), 0.f);
+    }
+  }
+  cudaFree(ctx->d_frames);
+  ctx->d_frames = nullptr;
+  GD_CUDA(ctx, cudaMalloc(&ctx->d_frames, sizeof(float4) * fr.size()));
+  GD_CUDA(ctx, cudaMemcpy(ctx->d_frames, fr.data(), sizeof(float4) * fr.size(), cudaMemcpyHostToDevice));
   return GD_OK;
 }
 
@@ -353,6 +376,12 @@ DevParams dev_params(const gd_ctx* ctx) {
   pr.grid_f = ctx->d_grid_f;
   pr.dtab = ctx->d_dtab;
   pr.dtab_f = ctx->d_dtab_f;
+  pr.frames = ctx->d_frames;
+  for (int i = 0; i < 3; ++i) pr.steps[i] = ctx->params.rotation_steps[i];
+  for (uint32_t i = 0; i < 16; ++i) {
+    const double alpha = i < pr.steps[0] ? gdh::kTwoPi * static_cast<double>(i) / static_cast<double>(pr.steps[0]) : 0.0;
+    pr.acs[i] = make_float2(float(std::cos(alpha)), float(std::sin(alpha)));
+  }
   pr.n_restarts = ctx->params.n_restarts;
   pr.reps = ctx->params.num_repetitions;
   pr.G = ctx->G;
@@ -418,6 +447,7 @@ void gd_destroy(gd_ctx* ctx) {
   cudaFree(ctx->d_cells);
   cudaFree(ctx->d_grid);
   cudaFree(ctx->d_grid_f);
+  cudaFree(ctx->d_frames);
   cudaFree(ctx->d_dtab);
   cudaFree(ctx->d_dtab_f);
   cudaFree(ctx->d_stats);

@@ -35,6 +35,10 @@ constexpr double kTwoPiD = 2.0 * 3.14159265358979323846;
 #define GD_FAST_THREADS 512
 #endif
 constexpr int kAlignUnroll = GD_ALIGN_UNROLL;
+#ifndef GD_ALPHA_CHUNK
+#define GD_ALPHA_CHUNK 4
+#endif
+constexpr int kAlphaChunk = GD_ALPHA_CHUNK;
 #ifndef GD_FAST_THREADS_NS4
 #define GD_FAST_THREADS_NS4 512
 #endif
@@ -46,22 +50,11 @@ struct CoarseGrid {
   const uint4* cells;  // shared (or global) 8-corner cells
   float hx, hy, hz;    // half extents (dims-1)/2 in grid units
   uint32_t cx, cxy;    // cells per row / per plane
+  uint32_t koff;       // 0x4B000000 * (1 + cx + cxy): removes the 2^23 exponent bits of the three floors
 };
 
-// One coarse sample at grid coordinates g (DESIGN.md §3.2). Returns 1 + v' (v' = trilinear of the
-// 15-bit codes u/32768) when strictly inside the grid, else exactly 1.0. amin tracks the smallest
-// L-inf distance of any sample to the grid boundary: a sample within the position bound of a face
-// may be classified differently from the FP64 reference, so its candidate is re-scored exactly.
-__device__ __forceinline__ float coarse_sample(const CoarseGrid& cg, float gx, float gy, float gz,
-                                               float& amin) {
-  const float e = fmaxf(fabsf(gx - cg.hx) - cg.hx, fmaxf(fabsf(gy - cg.hy) - cg.hy, fabsf(gz - cg.hz) - cg.hz));
-  amin = fminf(amin, fabsf(e));
-  const bool inside = e < 0.0f;
-  const float rx = __fadd_rz(gx, kMagic), ry = __fadd_rz(gy, kMagic), rz = __fadd_rz(gz, kMagic);
-  const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic), fz = gz - (rz - kMagic);
-  const uint32_t cell = (__float_as_uint(rx) - 0x4B000000u) + (__float_as_uint(ry) - 0x4B000000u) * cg.cx +
-                        (__float_as_uint(rz) - 0x4B000000u) * cg.cxy;
-  const uint4 w = cg.cells[inside ? cell : 0u];
+// Decode of one 8-corner cell and the trilinear interpolation in the [1, 2) domain.
+__device__ __forceinline__ float cell_lerp(const uint4 w, float fx, float fy, float fz) {
   // byte permute: half-word 0x8000|u -> float bits 0x3F800000 | u<<8 = 1 + u/32768
   const float c000 = __uint_as_float(__byte_perm(w.x, 0x3F000000u, 0x7104));
   const float c100 = __uint_as_float(__byte_perm(w.x, 0x3F000000u, 0x7324));
@@ -77,7 +70,38 @@ __device__ __forceinline__ float coarse_sample(const CoarseGrid& cg, float gx, f
   const float c11 = fmaf(fx, c111 - c011, c011);
   const float c0 = fmaf(fy, c10 - c00, c00);
   const float c1 = fmaf(fy, c11 - c01, c01);
-  const float v = fmaf(fz, c1 - c0, c0);
+  return fmaf(fz, c1 - c0, c0);
+}
+
+// One coarse sample at grid coordinates g (DESIGN.md §3.2). Returns 1 + v' (v' = trilinear of the
+// 15-bit codes u/32768) when strictly inside the grid, else exactly 1.0. amin tracks the smallest
+// L-inf distance of any sample to the grid boundary: a sample within the position bound of a face
+// may be classified differently from the FP64 reference, so its candidate is re-scored exactly.
+__device__ __forceinline__ float coarse_sample(const CoarseGrid& cg, float gx, float gy, float gz,
+                                               float& amin) {
+  const float e = fmaxf(fabsf(gx - cg.hx) - cg.hx, fmaxf(fabsf(gy - cg.hy) - cg.hy, fabsf(gz - cg.hz) - cg.hz));
+  amin = fminf(amin, fabsf(e));
+  const bool inside = e < 0.0f;
+  const float rx = __fadd_rz(gx, kMagic), ry = __fadd_rz(gy, kMagic), rz = __fadd_rz(gz, kMagic);
+  const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic), fz = gz - (rz - kMagic);
+  const uint32_t cell = __float_as_uint(rx) + __float_as_uint(ry) * cg.cx + __float_as_uint(rz) * cg.cxy - cg.koff;
+  const uint4 w = cg.cells[inside ? cell : 0u];
+  const float v = cell_lerp(w, fx, fy, fz);
+  return inside ? v : 1.0f;
+}
+
+// coarse_sample for the separable alignment: the z coordinate's box term ez, fraction fz and cell
+// plane offset zoff (already carrying -koff) are shared by the 16 alpha rotations of a frame.
+__device__ __forceinline__ float coarse_sample_z(const CoarseGrid& cg, float gx, float gy, float ez, float fz,
+                                                 uint32_t zoff, float& amin) {
+  const float e = fmaxf(fmaxf(fabsf(gx - cg.hx) - cg.hx, fabsf(gy - cg.hy) - cg.hy), ez);
+  amin = fminf(amin, fabsf(e));
+  const bool inside = e < 0.0f;
+  const float rx = __fadd_rz(gx, kMagic), ry = __fadd_rz(gy, kMagic);
+  const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic);
+  const uint32_t cell = __float_as_uint(rx) + __float_as_uint(ry) * cg.cx + zoff;
+  const uint4 w = cg.cells[inside ? cell : 0u];
+  const float v = cell_lerp(w, fx, fy, fz);
   return inside ? v : 1.0f;
 }
 
@@ -243,25 +267,30 @@ __device__ double exact_candidate_score(const DevPocket& pk, const Item& it, con
 // ============================================================================ the kernel
 // NT = threads per CTA (launch bound): 64 registers at 1024 threads spilled the smem bases inside
 // the hot loops, so the kernel trades warps for registers.
-template <int NS, int NT>
+template <int NS, int NT, bool SC>
 __global__ void __launch_bounds__(NT, 1)
-    dock_fast_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t slot_floats, uint32_t cells_in_smem) {
+    dock_fast_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t slot_floats) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
-  const uint4* cells = pk.cells;
-  float* slots = reinterpret_cast<float*>(smem_raw);
-  if (cells_in_smem) {  // stage the pocket once per CTA; every warp of every work item reads it
-    uint4* sc = reinterpret_cast<uint4*>(smem_raw);
+  // SC: the pocket cells are staged once per CTA into shared memory (every warp of every work item
+  // reads them; a compile-time flag so the gather is an LDS.128, not a generic load)
+  uint4* sc = reinterpret_cast<uint4*>(smem_raw);
+  const uint4* cells = SC ? sc : pk.cells;
+  float* slots = SC ? reinterpret_cast<float*>(sc + n_cells) : reinterpret_cast<float*>(smem_raw);
+  if (SC) {
     for (uint32_t i = threadIdx.x; i < n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
-    cells = sc;
-    slots = reinterpret_cast<float*>(sc + n_cells);
     __syncthreads();
   }
   float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
-  const CoarseGrid cg{cells, 0.5f * float(pk.cell_dims[0]), 0.5f * float(pk.cell_dims[1]),
-                      0.5f * float(pk.cell_dims[2]), pk.cell_dims[0], pk.cell_dims[0] * pk.cell_dims[1]};
+  const CoarseGrid cg{cells,
+                      0.5f * float(pk.cell_dims[0]),
+                      0.5f * float(pk.cell_dims[1]),
+                      0.5f * float(pk.cell_dims[2]),
+                      pk.cell_dims[0],
+                      pk.cell_dims[0] * pk.cell_dims[1],
+                      0x4B000000u * (1u + pk.cell_dims[0] + pk.cell_dims[0] * pk.cell_dims[1])};
   const uint32_t N = pr.n_restarts;
   const uint64_t total = uint64_t(b.n_lig) * N;
   const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
@@ -374,38 +403,95 @@ __global__ void __launch_bounds__(NT, 1)
         dropped = fmaxf(dropped, key_hi);
       }
     };
-    for (uint32_t g = lane, j = 0; g < pr.G; g += 32, ++j) {
-      const float4 r0 = __ldg(pr.grid_f + 3 * g), r1 = __ldg(pr.grid_f + 3 * g + 1), r2 = __ldg(pr.grid_f + 3 * g + 2);
-      float acc0 = 0.f, acc1 = 0.f, amin = 1e30f;
-#pragma unroll kAlignUnroll
-      for (uint32_t a = 0; a < npad; a += 4) {
-        const float4 v0 = A[a], v1 = A[a + 1], v2 = A[a + 2], v3 = A[a + 3];
-        acc0 += coarse_sample(cg, fmaf(r0.x, v0.x, fmaf(r0.y, v0.y, fmaf(r0.z, v0.z, tx))),
-                              fmaf(r1.x, v0.x, fmaf(r1.y, v0.y, fmaf(r1.z, v0.z, ty))),
-                              fmaf(r2.x, v0.x, fmaf(r2.y, v0.y, fmaf(r2.z, v0.z, tz))), amin);
-        acc1 += coarse_sample(cg, fmaf(r0.x, v1.x, fmaf(r0.y, v1.y, fmaf(r0.z, v1.z, tx))),
-                              fmaf(r1.x, v1.x, fmaf(r1.y, v1.y, fmaf(r1.z, v1.z, ty))),
-                              fmaf(r2.x, v1.x, fmaf(r2.y, v1.y, fmaf(r2.z, v1.z, tz))), amin);
-        acc0 += coarse_sample(cg, fmaf(r0.x, v2.x, fmaf(r0.y, v2.y, fmaf(r0.z, v2.z, tx))),
-                              fmaf(r1.x, v2.x, fmaf(r1.y, v2.y, fmaf(r1.z, v2.z, ty))),
-                              fmaf(r2.x, v2.x, fmaf(r2.y, v2.y, fmaf(r2.z, v2.z, tz))), amin);
-        acc1 += coarse_sample(cg, fmaf(r0.x, v3.x, fmaf(r0.y, v3.y, fmaf(r0.z, v3.z, tx))),
-                              fmaf(r1.x, v3.x, fmaf(r1.y, v3.y, fmaf(r1.z, v3.z, ty))),
-                              fmaf(r2.x, v3.x, fmaf(r2.y, v3.y, fmaf(r2.z, v3.z, tz))), amin);
+    // Separable form (default grids): R_g = Rz(alpha_i) F_f with frame f = j*c + k, g = i*b*c + f.
+    // Lane l owns frames f = l + 32 m and all alpha of each; the frame's z row, its box term, floor
+    // and cell plane are shared by the alpha rotations and x, y need a 2D rotation only.
+    const uint32_t n_frames = pr.steps[1] * pr.steps[2];
+    const bool separable = pr.steps[0] >= 8 && pr.steps[0] <= 16 && n_frames <= 128;
+    auto amb_to_g = [&](uint32_t bit) -> uint32_t {
+      return separable ? (bit & 15u) * n_frames + lane + 32u * (bit >> 4) : lane + 32u * bit;
+    };
+    if (separable) {
+      const uint32_t na = pr.steps[0];
+      for (uint32_t f = lane, m = 0; f < n_frames; f += 32, ++m) {
+        const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
+        // alpha in chunks of kAlphaChunk (the frame transform is redone per chunk) so the unrolled
+        // body stays small enough for the instruction cache
+#pragma unroll 1
+        for (uint32_t i0 = 0; i0 < na; i0 += kAlphaChunk) {
+          float acc[kAlphaChunk], amn[kAlphaChunk];
+          float2 cs[kAlphaChunk];
+#pragma unroll
+          for (int i = 0; i < kAlphaChunk; ++i) {
+            acc[i] = 0.f;
+            amn[i] = 1e30f;
+            cs[i] = pr.acs[(i0 + i) & 15];
+          }
+#pragma unroll 1
+          for (uint32_t a = 0; a < npad; ++a) {
+            const float4 v = A[a];
+            const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
+            const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
+            const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
+            const float ez = fabsf(gz - cg.hz) - cg.hz;
+            const float rz = __fadd_rz(gz, kMagic);
+            const float fz = gz - (rz - kMagic);
+            const uint32_t zoff = __float_as_uint(rz) * cg.cxy - cg.koff;
+#pragma unroll
+            for (int i = 0; i < kAlphaChunk; ++i) {
+              const float gx = fmaf(cs[i].x, wx, fmaf(-cs[i].y, wy, tx));
+              const float gy = fmaf(cs[i].y, wx, fmaf(cs[i].x, wy, ty));
+              acc[i] += coarse_sample_z(cg, gx, gy, ez, fz, zoff, amn[i]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < kAlphaChunk; ++i) {
+            const uint32_t ia = i0 + i;
+            if (ia >= na) break;
+            const float sc = (acc[i] - float(npad)) * inv_n_scale;
+            if (amn[i] <= ptol) {
+              amb_mask |= 1ull << (16 * m + ia);
+            } else {
+              insert(sc, ia * n_frames + f);
+              lkey = fmaxf(lkey, sc);
+            }
+          }
+        }
       }
-      const float sc = ((acc0 - float(npad >> 1)) + (acc1 - float(npad >> 1))) * inv_n_scale;
-      if (amin <= ptol) {
-        amb_mask |= (j < 64 ? 1ull << j : 0ull);
-        if (j >= 64) lkey = 1e30f;  // cannot track: forces the exact fallback below
-      } else {
-        insert(sc, g);
-        lkey = fmaxf(lkey, sc);
+    } else {
+      for (uint32_t g = lane, j = 0; g < pr.G; g += 32, ++j) {
+        const float4 r0 = __ldg(pr.grid_f + 3 * g), r1 = __ldg(pr.grid_f + 3 * g + 1), r2 = __ldg(pr.grid_f + 3 * g + 2);
+        float acc0 = 0.f, acc1 = 0.f, amin = 1e30f;
+#pragma unroll kAlignUnroll
+        for (uint32_t a = 0; a < npad; a += 4) {
+          const float4 v0 = A[a], v1 = A[a + 1], v2 = A[a + 2], v3 = A[a + 3];
+          acc0 += coarse_sample(cg, fmaf(r0.x, v0.x, fmaf(r0.y, v0.y, fmaf(r0.z, v0.z, tx))),
+                                fmaf(r1.x, v0.x, fmaf(r1.y, v0.y, fmaf(r1.z, v0.z, ty))),
+                                fmaf(r2.x, v0.x, fmaf(r2.y, v0.y, fmaf(r2.z, v0.z, tz))), amin);
+          acc1 += coarse_sample(cg, fmaf(r0.x, v1.x, fmaf(r0.y, v1.y, fmaf(r0.z, v1.z, tx))),
+                                fmaf(r1.x, v1.x, fmaf(r1.y, v1.y, fmaf(r1.z, v1.z, ty))),
+                                fmaf(r2.x, v1.x, fmaf(r2.y, v1.y, fmaf(r2.z, v1.z, tz))), amin);
+          acc0 += coarse_sample(cg, fmaf(r0.x, v2.x, fmaf(r0.y, v2.y, fmaf(r0.z, v2.z, tx))),
+                                fmaf(r1.x, v2.x, fmaf(r1.y, v2.y, fmaf(r1.z, v2.z, ty))),
+                                fmaf(r2.x, v2.x, fmaf(r2.y, v2.y, fmaf(r2.z, v2.z, tz))), amin);
+          acc1 += coarse_sample(cg, fmaf(r0.x, v3.x, fmaf(r0.y, v3.y, fmaf(r0.z, v3.z, tx))),
+                                fmaf(r1.x, v3.x, fmaf(r1.y, v3.y, fmaf(r1.z, v3.z, ty))),
+                                fmaf(r2.x, v3.x, fmaf(r2.y, v3.y, fmaf(r2.z, v3.z, tz))), amin);
+        }
+        const float sc = ((acc0 - float(npad >> 1)) + (acc1 - float(npad >> 1))) * inv_n_scale;
+        if (amin <= ptol) {
+          amb_mask |= (j < 64 ? 1ull << j : 0ull);
+          if (j >= 64) lkey = 1e30f;  // cannot track: forces the exact fallback below
+        } else {
+          insert(sc, g);
+          lkey = fmaxf(lkey, sc);
+        }
       }
     }
     // second pass over face-ambiguous rotations: interval bounds (rare; z-face ambiguities come
     // in groups of 16 rotations that share (beta, gamma) and therefore the z coordinate)
     for (unsigned long long mk = amb_mask; mk; mk &= mk - 1) {
-      const uint32_t g = lane + 32u * uint32_t(__ffsll(static_cast<long long>(mk)) - 1);
+      const uint32_t g = amb_to_g(uint32_t(__ffsll(static_cast<long long>(mk)) - 1));
       const float4 r0 = __ldg(pr.grid_f + 3 * g), r1 = __ldg(pr.grid_f + 3 * g + 1), r2 = __ldg(pr.grid_f + 3 * g + 2);
       float lo = 0.f, hi = 0.f;
 #pragma unroll 1
@@ -421,25 +507,31 @@ __global__ void __launch_bounds__(NT, 1)
     const float B = warp_max(lkey);
     const float thr = B - 2.0f * eps;
     const bool overflow = __any_sync(FULL, dropped >= thr) || B < -1e29f || B > 1e29f || big_grid;
-    // exact FP64 re-scoring: the candidates, or (overflow) every rotation; one code path
-    unsigned long long todo = 0ull;
-    if (overflow) {
-      ++st_afall;
-    } else {
-#pragma unroll
-      for (int t = 0; t < KTOP; ++t)
-        if (top_s[t] >= thr) todo |= 1ull << ((top_g[t] - lane) >> 5);
-    }
+    // exact FP64 re-scoring of the candidates, or (overflow) of every rotation
     double best_s = -1.0;
     uint32_t best_g = 0xffffffffu;
-    for (uint32_t g = lane, j = 0; g < pr.G; g += 32, ++j) {
-      if (!overflow && (j >= 64 || !((todo >> j) & 1ull))) continue;
-      if (!overflow) ++st_aexact;
-      const double4 gq = pr.grid[g];
-      const double s = exact_rotation_score(pk, gpose, n, cen, Qd{gq.x, gq.y, gq.z, gq.w});
-      if (best_g == 0xffffffffu || s > best_s) {  // g ascending within a lane: first max wins
-        best_s = s;
-        best_g = g;
+    if (overflow) {
+      ++st_afall;
+      for (uint32_t g = lane; g < pr.G; g += 32) {
+        const double4 gq = pr.grid[g];
+        const double s = exact_rotation_score(pk, gpose, n, cen, Qd{gq.x, gq.y, gq.z, gq.w});
+        if (best_g == 0xffffffffu || s > best_s) {  // g ascending within a lane: first max wins
+          best_s = s;
+          best_g = g;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < KTOP; ++t) {
+        const uint32_t g = top_g[t];
+        if (!(top_s[t] >= thr)) continue;
+        ++st_aexact;
+        const double4 gq = pr.grid[g];
+        const double s = exact_rotation_score(pk, gpose, n, cen, Qd{gq.x, gq.y, gq.z, gq.w});
+        if (best_g == 0xffffffffu || s > best_s || (s == best_s && g < best_g)) {
+          best_s = s;
+          best_g = g;
+        }
       }
     }
     for (int off = 16; off > 0; off >>= 1) {  // combine (docking.cpp:93-108)
@@ -817,6 +909,15 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
+template <int NS, int NT, bool SC>
+static cudaError_t launch_sc(int warps, size_t smem, const DevPocket& pk, const DevParams& pr, const DevBatch& b,
+                             uint32_t slot_floats, int n_sms, cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(dock_fast_kernel<NS, NT, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  dock_fast_kernel<NS, NT, SC><<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, slot_floats);
+  return cudaGetLastError();
+}
+
 template <int NS, int NT>
 static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                              cudaStream_t stream) {
@@ -828,16 +929,14 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const uint32_t cells_in_smem = cell_bytes + 8 * slot_bytes <= size_t(optin) ? 1u : 0u;
+  const bool cells_in_smem = cell_bytes + 8 * slot_bytes <= size_t(optin);
   const size_t avail = size_t(optin) - (cells_in_smem ? cell_bytes : 0);
   int warps = int(avail / slot_bytes);
   if (warps > NT / 32) warps = NT / 32;
   if (warps < 1) return cudaErrorInvalidConfiguration;
   const size_t smem = (cells_in_smem ? cell_bytes : 0) + slot_bytes * warps;
-  cudaError_t e = cudaFuncSetAttribute(dock_fast_kernel<NS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  dock_fast_kernel<NS, NT><<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, slot_floats, cells_in_smem);
-  return cudaGetLastError();
+  return cells_in_smem ? launch_sc<NS, NT, true>(warps, smem, pk, pr, b, slot_floats, n_sms, stream)
+                       : launch_sc<NS, NT, false>(warps, smem, pk, pr, b, slot_floats, n_sms, stream);
 }
 
 cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
