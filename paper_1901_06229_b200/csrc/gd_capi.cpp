@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -426,7 +427,7 @@ int gd_create(int device, gd_ctx** out) {
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_stats, sizeof(unsigned long long) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_stats, sizeof(unsigned long long) * 16);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_error, sizeof(int) * 2);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_counter, sizeof(unsigned int) * 4);
   if (e != cudaSuccess) {
@@ -831,7 +832,7 @@ int gd_run(gd_batch* b) {
   gd_ctx* ctx = b->ctx;
   cudaSetDevice(ctx->device);
   GD_CUDA(ctx, cudaMemsetAsync(ctx->d_error, 0, 2 * sizeof(int), ctx->stream));
-  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, 16 * sizeof(unsigned long long), ctx->stream));
   int launches = 0;
   DevParams pr = dev_params(ctx);
   if (!(ctx->q_eps < 1.0f)) pr.mode = (pr.mode & ~0xff) | GD_MODE_EXACT;
@@ -955,9 +956,18 @@ void gd_batch_free(gd_batch* b) {
 int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
   if (!ctx || !out) return GD_ERR_ARGUMENT;
   // device counters of the last gd_run (synchronises the context stream)
-  unsigned long long st[8];
+  unsigned long long st[16];
   GD_CUDA(ctx, cudaMemcpyAsync(st, ctx->d_stats, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (const char* env = std::getenv("GD_PRINT_PHASES")) {
+    if (env[0] == '1') {
+      const char* names[8] = {"setup", "align-coarse", "align-refine", "refresh", "step-head", "step-coarse-cand",
+                              "step-decide", "tail"};
+      unsigned long long tot = 0;
+      for (int i = 0; i < 8; ++i) tot += st[8 + i];
+      for (int i = 0; i < 8; ++i) std::fprintf(stderr, "phase %-16s %6.2f%%\n", names[i], tot ? 100.0 * st[8 + i] / tot : 0.0);
+    }
+  }
   ctx->last.restarts = st[0];
   ctx->last.align_exact_evals = st[1];
   ctx->last.align_fallbacks = st[2];

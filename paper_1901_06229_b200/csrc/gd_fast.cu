@@ -39,12 +39,20 @@ constexpr int kAlignUnroll = GD_ALIGN_UNROLL;
 #define GD_ALPHA_CHUNK 4
 #endif
 constexpr int kAlphaChunk = GD_ALPHA_CHUNK;
+// Optional device-side phase timers (build with -DGD_PHASE_TIMERS): per-warp clock64 deltas summed
+// into gd_stats-adjacent counters 8..15 (setup, align coarse, align refine, refresh, step head,
+// step coarse candidates, step decisions+commit, tail).
+#ifdef GD_PHASE_TIMERS
+#define GD_T(slot) do { const long long t_ = clock64(); ph[cur_ph] += t_ - t_ph; t_ph = t_; cur_ph = (slot); } while (0)
+#else
+#define GD_T(slot) do { } while (0)
+#endif
 #ifndef GD_FAST_THREADS_NS4
 #define GD_FAST_THREADS_NS4 512
 #endif
 
 // status bits of a coarse dihedral candidate
-constexpr uint32_t ST_CLASH = 1, ST_OK = 2, ST_XAMB = 4, ST_SAMB = 8;
+constexpr uint32_t ST_CLASH = 1, ST_OK = 2, ST_XAMB = 4, ST_SAMB = 8, ST_ALLOUT = 16;
 
 struct CoarseGrid {
   const uint4* cells;  // shared (or global) 8-corner cells
@@ -88,6 +96,14 @@ __device__ __forceinline__ float coarse_sample(const CoarseGrid& cg, float gx, f
   const uint4 w = cg.cells[inside ? cell : 0u];
   const float v = cell_lerp(w, fx, fy, fz);
   return inside ? v : 1.0f;
+}
+
+// coarse_sample that also tracks the smallest signed box distance (emin > ptol: clearly outside).
+__device__ __forceinline__ float coarse_sample_e(const CoarseGrid& cg, float gx, float gy, float gz, float& amin,
+                                                 float& emin) {
+  const float e = fmaxf(fabsf(gx - cg.hx) - cg.hx, fmaxf(fabsf(gy - cg.hy) - cg.hy, fabsf(gz - cg.hz) - cg.hz));
+  emin = fminf(emin, e);
+  return coarse_sample(cg, gx, gy, gz, amin);
 }
 
 // coarse_sample for the separable alignment: the z coordinate's box term ez, fraction fz and cell
@@ -295,6 +311,11 @@ __global__ void __launch_bounds__(NT, 1)
   const uint64_t total = uint64_t(b.n_lig) * N;
   const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
   unsigned long long st_aexact = 0, st_afall = 0, st_sexact = 0, st_sfall = 0, st_commit = 0, st_items = 0;
+#ifdef GD_PHASE_TIMERS
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_ph = clock64();
+  int cur_ph = 7;
+#endif
 
   for (;;) {
     uint32_t item = 0;
@@ -303,6 +324,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (item >= total) break;
     if (*(volatile int*)b.error != 0) break;
     ++st_items;
+    GD_T(0);
     Item it;
     it.lig = item / N;
     it.rs = item - it.lig * N;
@@ -360,9 +382,11 @@ __global__ void __launch_bounds__(NT, 1)
     const float ext_g = warp_max(ext) * pk.inv_spacing_f;
     const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
     const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
-    const float eps = pk.q_eps + 3.0f * pk.max_step * ptol + 4e-6f;  // coarse score error bound
+    const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
+    const float eps = eps_s + 4e-6f;                              // coarse score error bound
     const float inv_n_scale = pk.coarse_scale / float(n);
 
+    GD_T(1);
     // ------------------------------------------------ coarse alignment sweep (all G rotations)
     // Lane l scores rotations g = l + 32 j. Per rotation the exact FP64 score lies in
     // [key_lo - eps, key_hi + eps] (key = coarse score, or for a rotation with a sample within ptol
@@ -504,6 +528,7 @@ __global__ void __launch_bounds__(NT, 1)
       insert(hi * inv_n_scale + eps, g);  // one extra eps for the clamp
       lkey = fmaxf(lkey, lo * inv_n_scale);
     }
+    GD_T(2);
     const float B = warp_max(lkey);
     const float thr = B - 2.0f * eps;
     const bool overflow = __any_sync(FULL, dropped >= thr) || B < -1e29f || B > 1e29f || big_grid;
@@ -521,16 +546,27 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     } else {
+      // warp-cooperative exact scoring: candidates one at a time, lanes over atoms (P still holds
+      // the start pose), index-order sum through shuffles; every lane ends with the same best
 #pragma unroll
       for (int t = 0; t < KTOP; ++t) {
-        const uint32_t g = top_g[t];
-        if (!(top_s[t] >= thr)) continue;
-        ++st_aexact;
-        const double4 gq = pr.grid[g];
-        const double s = exact_rotation_score(pk, gpose, n, cen, Qd{gq.x, gq.y, gq.z, gq.w});
-        if (best_g == 0xffffffffu || s > best_s || (s == best_s && g < best_g)) {
-          best_s = s;
-          best_g = g;
+        uint32_t pend = __ballot_sync(FULL, top_s[t] >= thr);
+        while (pend) {
+          const uint32_t src = __ffs(pend) - 1;
+          pend &= pend - 1;
+          const uint32_t g = __shfl_sync(FULL, top_g[t], src);
+          ++st_aexact;
+          const double4 gq = pr.grid[g];
+          const Qd q{gq.x, gq.y, gq.z, gq.w};
+          double ns[NS];
+#pragma unroll
+          for (int s = 0; s < NS; ++s)
+            ns[s] = lane + 32 * s < n ? sample_exact_ni(pk, rotated_about(own(P, s), cen, q)) : 0.0;
+          const double sc = __ddiv_rn(ordered_sum<NS>(ns, n), double(n));
+          if (best_g == 0xffffffffu || sc > best_s || (sc == best_s && g < best_g)) {
+            best_s = sc;
+            best_g = g;
+          }
         }
       }
     }
@@ -542,16 +578,13 @@ __global__ void __launch_bounds__(NT, 1)
         best_g = og;
       }
     }
-    {  // apply_rotation_choice (docking.cpp:110-118); the start pose is re-read from global so
-       // that no FP64 pose registers stay live across the alignment loop
+    {  // apply_rotation_choice (docking.cpp:110-118)
       const double4 gq = pr.grid[best_g];
       const Qd q{gq.x, gq.y, gq.z, gq.w};
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const uint32_t a = lane + 32 * s;
-        V3d p{0.0, 0.0, 0.0};
-        if (a < n) p = V3d{gpose[3 * a], gpose[3 * a + 1], gpose[3 * a + 2]};
-        set_own(P, s, rotated_about(p, cen, q));
+        set_own(P, s, rotated_about(own(P, s), cen, q));
         rad[s] = a < n ? b.atoms[it.m.atom_base + a].w : 0.0;
         pos[s] = a < n ? b.dfs_pos[it.m.atom_base + a] : 0;
       }
@@ -646,11 +679,13 @@ __global__ void __launch_bounds__(NT, 1)
         uint32_t none[NS];
 #pragma unroll
         for (int w = 0; w < NS; ++w) none[w] = 0u;
+        GD_T(3);
         refresh(true, none);
       }
 
       for (uint32_t rep = 0; rep < pr.reps; ++rep) {
         for (uint32_t r = 0; r < R; ++r) {
+          GD_T(4);
           const uint2 ij = b.rots[it.m.rot_base + r];
           const ushort4 rd = b.rdfs[it.m.rot_base + r];
           const uint32_t s0 = rd.x, e0 = rd.y, ipos = rd.z;
@@ -698,15 +733,28 @@ __global__ void __launch_bounds__(NT, 1)
           const bool elig0 = !__any_sync(FULL, cne_l);  // k = 0: the current pose passes bump_check
           const bool famb = __any_sync(FULL, famb_l);
           fsum = warp_sum(fsum);
-          // FP64 axis (rotate_fragment, molecule.cpp:150-160) and DegenerateAxisError semantics
-          const V3d pi = fetch<NS>(P, ij.x);
-          const V3d pj = fetch<NS>(P, ij.y);
-          const V3d delta = vsub(pj, pi);
-          const double len = __dsqrt_rn(vdot(delta, delta));
-          const V3d axis = vscale(__ddiv_rn(1.0, len), delta);
-          if (pr.S > 1 && len < 1e-12) {
-            if (lane == 0 && atomicCAS(b.error, 0, GD_ERR_DEGENERATE_AXIS) == 0) b.error[1] = int(it.lig);
-            break;
+          // FP64 axis (rotate_fragment, molecule.cpp:150-160), computed when first needed; the
+          // DegenerateAxisError check (len < 1e-12) only needs FP64 when the FP32 bond is tiny
+          V3d pi{0, 0, 0}, axis{0, 0, 0};
+          bool have_axis = false;
+          auto get_axis = [&]() {
+            if (have_axis) return;
+            pi = fetch<NS>(P, ij.x);
+            const V3d delta = vsub(fetch<NS>(P, ij.y), pi);
+            axis = vscale(__ddiv_rn(1.0, __dsqrt_rn(vdot(delta, delta))), delta);
+            have_axis = true;
+          };
+          if (pr.S > 1) {
+            const float4 fi = A[it.m.fast_ok ? ipos : 0u], fj = A[it.m.fast_ok ? s0 : 0u];
+            const float dx = fj.x - fi.x, dy = fj.y - fi.y, dz = fj.z - fi.z;
+            if (!it.m.fast_ok || dx * dx + dy * dy + dz * dz < 1e-6f) {
+              const V3d qi = fetch<NS>(P, ij.x);
+              const V3d delta = vsub(fetch<NS>(P, ij.y), qi);
+              if (__dsqrt_rn(vdot(delta, delta)) < 1e-12) {
+                if (lane == 0 && atomicCAS(b.error, 0, GD_ERR_DEGENERATE_AXIS) == 0) b.error[1] = int(it.lig);
+                break;
+              }
+            }
           }
           int32_t step_k = -1;
           const size_t trace_at = size_t(it.m.rot_base) * N * pr.reps + (size_t(it.rs) * pr.reps + rep) * R + r;
@@ -718,6 +766,7 @@ __global__ void __launch_bounds__(NT, 1)
             // ---------------- slow path: every candidate exactly (non-tree layouts, pairs of the
             // moving fragment within tau of the threshold, or unusual S)
             ++st_sfall;
+            get_axis();
             for (uint32_t k = 0; k < pr.S; ++k) {
               const Qd q = frag_quat(pr.dtab[k], axis);
               const double sk = k == 0 ? __ddiv_rn(ordered_sum<NS>(es, n), double(n))
@@ -733,6 +782,7 @@ __global__ void __launch_bounds__(NT, 1)
               }
             }
           } else if (!(skip_inv && inv)) {
+            GD_T(5);
             // ---------------- coarse evaluation of every candidate k = 1 .. S-1 (faithful sweep)
             const float4 fpi = A[ipos];
             const float4 fpj = A[s0];
@@ -756,7 +806,7 @@ __global__ void __launch_bounds__(NT, 1)
               const uint32_t grp = lane >> sh, sub = lane & (gs - 1);
               const uint32_t k = pass == 0 ? lane + 1 : 33 + grp;
               const bool active = pass == 0 ? (k <= n_cand) : (grp < rem);
-              float part = 0.f, amin = 1e30f, mmin = 1e30f;
+              float part = 0.f, amin = 1e30f, mmin = 1e30f, emin = 1e30f;
               if (active) {
                 const float2 cq = __ldg(pr.dtab_f + k);
                 const float qw = cq.x, qx = ax * cq.y, qy = ay * cq.y, qz = az * cq.y;
@@ -773,7 +823,7 @@ __global__ void __launch_bounds__(NT, 1)
                   const float gx = fmaf(m00, pm.x, fmaf(m01, pm.y, fmaf(m02, pm.z, tvx)));
                   const float gy = fmaf(m10, pm.x, fmaf(m11, pm.y, fmaf(m12, pm.z, tvy)));
                   const float gz = fmaf(m20, pm.x, fmaf(m21, pm.y, fmaf(m22, pm.z, tvz)));
-                  if (((mq - s0 - 1) & (gs - 1)) == sub) part += coarse_sample(cg, gx, gy, gz, amin) - 1.0f;
+                  if (((mq - s0 - 1) & (gs - 1)) == sub) part += coarse_sample_e(cg, gx, gy, gz, amin, emin) - 1.0f;
                   // cross pairs with the fixed side [0, s0) U [e0, n) and with atom_j unless bonded
                   for (uint32_t f = sub; f < s0; f += gs) {
                     const float4 pf = A[f];
@@ -795,11 +845,13 @@ __global__ void __launch_bounds__(NT, 1)
                 part += __shfl_xor_sync(FULL, part, o);
                 amin = fminf(amin, __shfl_xor_sync(FULL, amin, o));
                 mmin = fminf(mmin, __shfl_xor_sync(FULL, mmin, o));
+                emin = fminf(emin, __shfl_xor_sync(FULL, emin, o));
               }
               uint32_t st = 0;
               if (active) {
                 st = mmin < -tau ? ST_CLASH : (mmin >= tau ? ST_OK : ST_XAMB);
-                if (amin <= ptol || famb) st |= ST_SAMB;
+                if (amin <= ptol) st |= ST_SAMB;
+                if (emin > ptol) st |= ST_ALLOUT;
               }
               const float sc = (fsum + part) * inv_n_scale;
               if (pass == 0) {
@@ -815,8 +867,15 @@ __global__ void __launch_bounds__(NT, 1)
               }
             }
 
+            GD_T(6);
             // ---------------- exact decisions (reference semantics, docking.cpp:131-147)
-            if (!inv) {
+            if (!inv && s0 + 1 >= e0) {
+              // M' empty (atom_j is a leaf): every candidate is the current pose, so k = 0 wins
+              // whenever it is eligible (lowest k on the exact tie) and nothing else can
+              committed = elig0;
+              bk = 0;
+              bs = score;
+            } else if (!inv) {
 #pragma unroll
               for (int h = 0; h < 2; ++h) {  // cross pairs within tau of the threshold: exact
                 uint32_t pend = __ballot_sync(FULL, (res_st[h] & ST_XAMB) != 0u);
@@ -825,33 +884,55 @@ __global__ void __launch_bounds__(NT, 1)
                   pend &= pend - 1;
                   const uint32_t k = (h == 0 ? 1u : 33u) + src;
                   ++st_sexact;
+                  get_axis();
                   const bool cl = exact_clash<NS>(b, it, P, rad, mo, true, pi, frag_quat(pr.dtab[k], axis),
                                                   pr.clash, true, lane);
-                  if (lane == src) res_st[h] = (res_st[h] & ST_SAMB) | (cl ? ST_CLASH : ST_OK);
+                  if (lane == src) res_st[h] = (res_st[h] & (ST_SAMB | ST_ALLOUT)) | (cl ? ST_CLASH : ST_OK);
                 }
               }
-              // coarse best over eligible, face-unambiguous candidates; lower bound on the exact max
-              float Bl = -1e30f;
+              // Relative screening: all candidates share the fixed atoms (same coarse and exact
+              // values), so two candidates' exact scores differ from their coarse difference by at
+              // most the moved atoms' error: 2 * eps_rel with eps_rel = |M'| eps_sample / n.
+              const uint32_t nm = e0 - s0 - 1;
+              const float eps_rel = float(nm) * (eps_s + 3e-7f) / float(n) + 2e-7f;
+              // k = 0 in the same coarse terms: fixed part + the cached coarse values of M'
+              float p0 = 0.f;
+              bool samb0 = false;
+#pragma unroll
+              for (int s = 0; s < NS; ++s)
+                if (inm[s]) {
+                  p0 += cs[s];
+                  samb0 |= samb[s];
+                }
+              p0 = warp_sum(p0);
+              samb0 = __any_sync(FULL, samb0);
+              float Bl = (elig0 && !samb0) ? (fsum + p0) * inv_n_scale : -1e30f;
 #pragma unroll
               for (int h = 0; h < 2; ++h)
                 if ((res_st[h] & ST_OK) && !(res_st[h] & ST_SAMB)) Bl = fmaxf(Bl, res_s[h]);
               Bl = warp_max(Bl);
-              float lb = Bl - eps;
+              const float thr_k = Bl - 2.0f * eps_rel;
               if (elig0) {  // k = 0: the current pose, score_pose(current) == the carried score
                 committed = true;
                 bk = 0;
                 bs = score;
-                lb = fmaxf(lb, float(score) - 1e-6f);
               }
+              bool allout_done = false;  // candidates with every moved atom clearly outside tie exactly
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const bool need = (res_st[h] & ST_OK) && ((res_st[h] & ST_SAMB) || res_s[h] + eps >= lb);
+                const bool need = (res_st[h] & ST_OK) && ((res_st[h] & ST_SAMB) || res_s[h] >= thr_k);
                 uint32_t pend = __ballot_sync(FULL, need);
+                const uint32_t allout = __ballot_sync(FULL, (res_st[h] & ST_ALLOUT) != 0u);
                 while (pend) {
                   const uint32_t src = __ffs(pend) - 1;
                   pend &= pend - 1;
+                  if ((allout >> src) & 1u) {
+                    if (allout_done) continue;
+                    allout_done = true;
+                  }
                   const uint32_t k = (h == 0 ? 1u : 33u) + src;
                   ++st_sexact;
+                  get_axis();
                   const double sk = exact_candidate_score<NS>(pk, it, P, es, mo, pi, frag_quat(pr.dtab[k], axis), lane);
                   if (!committed || sk > bs || (sk == bs && k < bk)) {
                     committed = true;
@@ -867,6 +948,7 @@ __global__ void __launch_bounds__(NT, 1)
             score = bs;
             ++st_commit;
             if (bk != 0) {  // commit = rotate_fragment(current, r, k*delta), FP64
+              get_axis();
               const double4 dt = pr.dtab[bk];
               const Qd q = frag_quat(dt, axis);
 #pragma unroll
@@ -886,6 +968,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     if (*(volatile int*)b.error != 0) break;
+    GD_T(7);
     // ------------------------------------------------ restart result
     if (lane == 0) b.rs_score[item] = score;
 #pragma unroll
@@ -906,6 +989,10 @@ __global__ void __launch_bounds__(NT, 1)
     atomicAdd(b.stats + 3, st_sexact);
     atomicAdd(b.stats + 4, st_sfall);
     atomicAdd(b.stats + 5, st_commit);
+#ifdef GD_PHASE_TIMERS
+    GD_T(7);
+    for (int i = 0; i < 8; ++i) atomicAdd(b.stats + 8 + i, (unsigned long long)ph[i]);
+#endif
   }
 }
 

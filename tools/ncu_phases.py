@@ -1,0 +1,68 @@
+"""Per-phase (source-region) breakdown of an ncu source page for dock_fast_kernel.
+
+usage: ncu -i X --page source --csv --print-source=cuda,sass > s.csv; python tools/ncu_phases.py s.csv
+Inlined helper lines are attributed to the phase of the call site by SASS address order: every
+SASS instruction belongs to the last gd_fast.cu kernel-body line seen before it.
+"""
+import csv
+import re
+import sys
+
+rows = list(csv.reader(open(sys.argv[1])))
+src = open(__file__.replace("tools/ncu_phases.py", "paper_1901_06229_b200/csrc/gd_fast.cu")).read().split("\n")
+
+
+def find(pat):
+    for i, l in enumerate(src):
+        if pat in l:
+            return i + 1
+    raise KeyError(pat)
+
+
+marks = [("setup/start-pose", find("dock_fast_kernel(DevPocket pk")),
+         ("align-coarse", find("coarse alignment sweep (all G rotations)")),
+         ("align-ambig-pass", find("second pass over face-ambiguous")),
+         ("align-exact", find("exact FP64 re-scoring of the candidates")),
+         ("sweep-setup+refresh", find("dihedral sweep (docking.cpp:155-167")),
+         ("step-head", find("for (uint32_t rep = 0; rep < pr.reps; ++rep)")),
+         ("step-slowpath", find("slow path: every candidate exactly")),
+         ("step-coarse-cand", find("coarse evaluation of every candidate k = 1")),
+         ("step-decisions", find("exact decisions (reference semantics")),
+         ("step-commit", find("commit = rotate_fragment(current, r, k*delta)")),
+         ("restart-tail", find("restart result"))]
+kstart = marks[0][1]
+# pass 1: collect (address, instr, samples, (file, line)) in page order
+hdr, fname, cur = None, None, None
+ins_rows = []
+for r in rows:
+    if len(r) >= 2 and r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if r and r[0] == "Line No":
+        hdr = {k: i for i, k in enumerate(r)}
+        continue
+    if hdr is None or len(r) < 6:
+        continue
+    if r[0].isdigit():
+        cur = (fname, int(r[0]))
+        continue
+    if r[0] == "" and r[2].startswith("0x"):
+        try:
+            ins = float(r[hdr["Instructions Executed"]] or 0)
+            smp = float(r[hdr["Warp Stall Sampling (All Samples)"]] or 0)
+        except ValueError:
+            continue
+        ins_rows.append((int(r[2], 16), ins, smp, cur))
+ins_rows.sort()
+phase, agg = "setup/start-pose", {}
+for addr, ins, smp, (f, l) in ins_rows:
+    if f == "gd_fast.cu" and l >= kstart:
+        phase = [m for m, ln in marks if ln <= l][-1]
+    a = agg.setdefault(phase, [0.0, 0.0])
+    a[0] += ins
+    a[1] += smp
+ti = sum(v[0] for v in agg.values()) or 1
+ts = sum(v[1] for v in agg.values()) or 1
+print(f"{'phase':24s} {'instr %':>8s} {'samples %':>10s}")
+for k, (i, s) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    print(f"{k:24s} {100 * i / ti:8.1f} {100 * s / ts:10.1f}")
