@@ -639,6 +639,8 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
   const size_t o_rdfs = ar.take<ushort4>(Rt);
   const size_t o_adjd = ar.take<uint32_t>(adj_base[L]);
   const size_t host_bytes = ar.off;  // everything above is uploaded
+  const size_t o_rs_cand = ar.take<uint16_t>(n_items * gdk::kAlignCand);
+  const size_t o_rs_ncand = ar.take<int32_t>(n_items);
   const size_t o_rs_score = ar.take<double>(n_items);
   const size_t o_rs_ascore = ar.take<double>(n_items);
   const size_t o_rs_aidx = ar.take<uint32_t>(n_items);
@@ -810,6 +812,8 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
   d.dfs_pos = reinterpret_cast<const uint16_t*>(D + o_dfs);
   d.rdfs = reinterpret_cast<const ushort4*>(D + o_rdfs);
   d.adjd = reinterpret_cast<const uint32_t*>(D + o_adjd);
+  d.rs_cand = reinterpret_cast<uint16_t*>(D + o_rs_cand);
+  d.rs_ncand = reinterpret_cast<int32_t*>(D + o_rs_ncand);
   d.rs_score = reinterpret_cast<double*>(D + o_rs_score);
   d.rs_align_score = reinterpret_cast<double*>(D + o_rs_ascore);
   d.rs_align_index = reinterpret_cast<uint32_t*>(D + o_rs_aidx);

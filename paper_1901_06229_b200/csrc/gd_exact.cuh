@@ -81,6 +81,13 @@ __device__ __forceinline__ double sample_exact(const DevPocket& pk, V3d p) {
   return __dadd_rn(__dmul_rn(c0, uz), __dmul_rn(c1, fz));
 }
 
+// d^2 - thr^2 of a pair in bump_check's arithmetic (scoring.cpp:52-58): negative iff the pair clashes.
+__device__ __forceinline__ double pair_margin_exact(V3d a, V3d b, double ra, double rb, double cf) {
+  const V3d d = vsub(a, b);
+  const double thr = __dmul_rn(cf, __dadd_rn(ra, rb));
+  return __dsub_rn(vdot(d, d), __dmul_rn(thr, thr));
+}
+
 // Non-bonded pair clash test of bump_check (scoring.cpp:52-58): d^2 < (cf (ra + rb))^2.
 __device__ __forceinline__ bool pair_clash_exact(V3d a, V3d b, double ra, double rb, double cf) {
   const V3d d = vsub(a, b);

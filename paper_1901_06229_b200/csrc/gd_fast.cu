@@ -47,6 +47,9 @@ constexpr int kAlphaChunk = GD_ALPHA_CHUNK;
 #else
 #define GD_T(slot) do { } while (0)
 #endif
+#ifndef GD_ALIGN_THREADS
+#define GD_ALIGN_THREADS 512
+#endif
 #ifndef GD_FAST_THREADS_NS4
 #define GD_FAST_THREADS_NS4 512
 #endif
@@ -169,26 +172,53 @@ __device__ __forceinline__ V3d fetch(const Pose<NS>& P, uint32_t a) {
   return V3d{__shfl_sync(FULL, vx, src), __shfl_sync(FULL, vy, src), __shfl_sync(FULL, vz, src)};
 }
 
-// Index-order sum of per-atom values (the reference's left-to-right accumulation); every lane
-// performs the same additions in the same order, so every lane holds the same bits.
-template <int NS>
-__device__ __forceinline__ double ordered_sum(const double (&v)[NS], uint32_t n) {
+// Index-order sums (the reference's left-to-right accumulation) through a per-warp shared
+// scratch, so every lane gets the same bits: lanes deposit their values, lane c
+// adds column c sequentially (LDS pipelined ahead of the dependent DADD chain), one shuffle
+// broadcasts. A shuffle per term costs ~30 cycles of latency on the chain; an LDS does not.
+__device__ __forceinline__ double serial_sum(const double* v, uint32_t n) {
   double sum = 0.0;
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
-#pragma unroll 1
-    for (uint32_t l = 0; l < 32; ++l) {
-      if (uint32_t(s) * 32 + l >= n) break;
-      sum = __dadd_rn(sum, __shfl_sync(FULL, v[s], l));
-    }
+  uint32_t a = 0;
+  for (; a + 4 <= n; a += 4) {
+    const double v0 = v[a], v1 = v[a + 1], v2 = v[a + 2], v3 = v[a + 3];
+    sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, v0), v1), v2), v3);
   }
+  for (; a < n; ++a) sum = __dadd_rn(sum, v[a]);
   return sum;
 }
 
 template <int NS>
-__device__ __forceinline__ V3d centroid_reg(const Pose<NS>& P, uint32_t n) {  // geometry.cpp:40-46
-  const V3d sum{ordered_sum<NS>(P.x, n), ordered_sum<NS>(P.y, n), ordered_sum<NS>(P.z, n)};
-  return vscale(__ddiv_rn(1.0, double(n)), sum);
+__device__ __forceinline__ double ordered_sum_smem(const double (&v)[NS], uint32_t n, double* scr, uint32_t lane) {
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (lane + 32 * s < n) scr[lane + 32 * s] = v[s];
+  __syncwarp();
+  double sum = 0.0;
+  if (lane == 0) sum = serial_sum(scr, n);
+  sum = __shfl_sync(FULL, sum, 0);
+  __syncwarp();
+  return sum;
+}
+
+// centroid (geometry.cpp:40-46): index-order sums of x, y, z (lanes 0, 1, 2 in parallel) * (1/n).
+// scr holds 3 n doubles.
+template <int NS>
+__device__ __forceinline__ V3d centroid_smem(const Pose<NS>& P, uint32_t n, double* scr, uint32_t lane) {
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const uint32_t a = lane + 32 * s;
+    if (a < n) {
+      scr[a] = P.x[s];
+      scr[n + a] = P.y[s];
+      scr[2 * n + a] = P.z[s];
+    }
+  }
+  __syncwarp();
+  double sum = 0.0;
+  if (lane < 3) sum = serial_sum(scr + lane * n, n);
+  const V3d tot{__shfl_sync(FULL, sum, 0), __shfl_sync(FULL, sum, 1), __shfl_sync(FULL, sum, 2)};
+  __syncwarp();
+  return vscale(__ddiv_rn(1.0, double(n)), tot);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -205,6 +235,13 @@ __device__ __forceinline__ float warp_max(float v) {
 
 template <int NW>
 __device__ __forceinline__ bool bit4(const uint32_t (&m)[NW], uint32_t a) { return (m[a >> 5] >> (a & 31)) & 1u; }
+
+// Bits [lo, hi) of a bit set, restricted to word w.
+__device__ __forceinline__ uint32_t range_word(uint32_t w, uint32_t lo, uint32_t hi) {
+  const int a = max(int(lo) - 32 * int(w), 0), e = min(int(hi) - 32 * int(w), 32);
+  if (e <= a) return 0u;
+  return (e >= 32 ? FULL : ((1u << e) - 1u)) & ~((1u << a) - 1u);
+}
 
 __device__ __forceinline__ Qd frag_quat(const double4& dt, V3d axis) {  // about_axis, geometry.hpp:46-50
   return Qd{dt.x, __dmul_rn(axis.x, dt.y), __dmul_rn(axis.y, dt.y), __dmul_rn(axis.z, dt.y)};
@@ -267,7 +304,7 @@ __device__ bool exact_clash(const DevBatch& b, const Item& it, const Pose<NS>& P
 template <int NS>
 __device__ double exact_candidate_score(const DevPocket& pk, const Item& it, const Pose<NS>& P,
                                         const double (&es)[NS], const uint32_t (&mo)[NS], V3d pi,
-                                        const Qd& q, uint32_t lane) {
+                                        const Qd& q, uint32_t lane, double* scr) {
   double ns[NS];
 #pragma unroll
   for (int t = 0; t < NS; ++t) {
@@ -275,23 +312,25 @@ __device__ double exact_candidate_score(const DevPocket& pk, const Item& it, con
     ns[t] = es[t];
     if (a < it.n && bit4(mo, a)) ns[t] = sample_exact_ni(pk, rotated_about(own(P, t), pi, q));
   }
-  return __ddiv_rn(ordered_sum<NS>(ns, it.n), double(it.n));
+  return __ddiv_rn(ordered_sum_smem<NS>(ns, it.n, scr, lane), double(it.n));
 }
 
 }  // namespace
 
-// ============================================================================ the kernel
-// NT = threads per CTA (launch bound): 64 registers at 1024 threads spilled the smem bases inside
-// the hot loops, so the kernel trades warps for registers (DESIGN.md §4).
+// ============================================================================ K1a: coarse alignment
+// Lean, high-occupancy kernel (no FP64 pose, no sweep state): per (ligand, restart) the FP32 start
+// pose relative to its centroid, the coarse score and error bound of every grid rotation, and the
+// list of rotations that can be the exact argmax (key_hi >= max key_lo - 2 eps),
+// handed to K1b for the FP64 re-scoring. The start pose is built in FP32 here: its error (~1e-6 A
+// for the rotation of p - c0, the centroid shift cancels in the relative coordinates) is far
+// inside ptol, and only the coarse screen sees it.
 template <int NS, int NT, bool SC>
 __global__ void __launch_bounds__(NT, 1)
-    dock_fast_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t slot_floats) {
+    align_coarse_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t slot_floats) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
-  // SC: the pocket cells are staged once per CTA into shared memory (every warp of every work item
-  // reads them; a compile-time flag so the gather is an LDS.128, not a generic load)
   uint4* sc = reinterpret_cast<uint4*>(smem_raw);
   const uint4* cells = SC ? sc : pk.cells;
   float* slots = SC ? reinterpret_cast<float*>(sc + n_cells) : reinterpret_cast<float*>(smem_raw);
@@ -309,84 +348,79 @@ __global__ void __launch_bounds__(NT, 1)
                       0x4B000000u * (1u + pk.cell_dims[0] + pk.cell_dims[0] * pk.cell_dims[1])};
   const uint32_t N = pr.n_restarts;
   const uint64_t total = uint64_t(b.n_lig) * N;
-  const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
-  unsigned long long st_aexact = 0, st_afall = 0, st_sexact = 0, st_sfall = 0, st_commit = 0, st_items = 0;
-#ifdef GD_PHASE_TIMERS
-  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long t_ph = clock64();
-  int cur_ph = 7;
-#endif
-
   for (;;) {
     uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(b.work_counter, 1u);
+    if (lane == 0) item = atomicAdd(b.work_counter + 1, 1u);
     item = __shfl_sync(FULL, item, 0);
     if (item >= total) break;
-    if (*(volatile int*)b.error != 0) break;
-    ++st_items;
-    GD_T(0);
-    Item it;
-    it.lig = item / N;
-    it.rs = item - it.lig * N;
-    it.m = b.meta[it.lig];
-    it.n = it.m.n;
-    it.W = (it.n + 31) >> 5;
-    const uint32_t n = it.n, R = it.m.nr;
-    double* gpose = b.rs_xyz + (size_t(it.m.atom_base) * N + size_t(it.rs) * n) * 3;
-
-    // ------------------------------------------------ starting pose (docking.cpp:52-69), FP64
-    Pose<NS> P;
-    uint32_t pos[NS];
-    double rad[NS];
+    const uint32_t lig = item / N;
+    const LigMeta meta = b.meta[lig];
+    const uint32_t n = meta.n;
+    // start pose (docking.cpp:52-69): R(q) (p - c0) + t; only the part relative to its centroid
+    // matters here, plus the centroid itself (t + mean of the rotated offsets, in FP64)
+    float px[NS], py[NS], pz[NS];
+    float sx = 0.f, sy = 0.f, sz = 0.f;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const uint32_t a = lane + 32 * s;
-      double4 at = make_double4(0.0, 0.0, 0.0, 0.0);
-      if (a < n) at = b.atoms[it.m.atom_base + a];
-      set_own(P, s, V3d{at.x, at.y, at.z});
-      rad[s] = at.w;
-      pos[s] = a < n ? b.dfs_pos[it.m.atom_base + a] : 0;
+      px[s] = py[s] = pz[s] = 0.f;
+      if (a < n) {
+        const double4 at = b.atoms[meta.atom_base + a];
+        px[s] = float(at.x);
+        py[s] = float(at.y);
+        pz[s] = float(at.z);
+      }
+      sx += px[s];
+      sy += py[s];
+      sz += pz[s];
     }
-    {
-      const V3d c0 = centroid_reg<NS>(P, n);
-      const double4 q4 = b.start[2 * size_t(item)];
-      const double4 t4 = b.start[2 * size_t(item) + 1];
-      const Qd qs{q4.x, q4.y, q4.z, q4.w};
-      const V3d tgt{t4.x, t4.y, t4.z};
+    const float inv_n = 1.0f / float(n);
+    const float c0x = warp_sum(sx) * inv_n, c0y = warp_sum(sy) * inv_n, c0z = warp_sum(sz) * inv_n;
+    const double4 q4 = b.start[2 * size_t(item)];
+    const double4 t4 = b.start[2 * size_t(item) + 1];
+    const float qw = float(q4.x), qx = float(q4.y), qy = float(q4.z), qz = float(q4.w);
+    const float xx = qx * qx, yy = qy * qy, zz = qz * qz, xy = qx * qy, xz = qx * qz, yz = qy * qz;
+    const float wx = qw * qx, wy = qw * qy, wz = qw * qz;
+    const float m00 = 1.f - 2.f * (yy + zz), m01 = 2.f * (xy - wz), m02 = 2.f * (xz + wy);
+    const float m10 = 2.f * (xy + wz), m11 = 1.f - 2.f * (xx + zz), m12 = 2.f * (yz - wx);
+    const float m20 = 2.f * (xz - wy), m21 = 2.f * (yz + wx), m22 = 1.f - 2.f * (xx + yy);
+    sx = sy = sz = 0.f;
 #pragma unroll
-      for (int s = 0; s < NS; ++s) set_own(P, s, vadd(qapply(qs, vsub(own(P, s), c0)), tgt));
+    for (int s = 0; s < NS; ++s) {
+      const float vx = px[s] - c0x, vy = py[s] - c0y, vz = pz[s] - c0z;
+      px[s] = fmaf(m00, vx, fmaf(m01, vy, m02 * vz));
+      py[s] = fmaf(m10, vx, fmaf(m11, vy, m12 * vz));
+      pz[s] = fmaf(m20, vx, fmaf(m21, vy, m22 * vz));
+      if (lane + 32 * s < n) {
+        sx += px[s];
+        sy += py[s];
+        sz += pz[s];
+      }
     }
-    const V3d cen = centroid_reg<NS>(P, n);  // best_rotation_in_range's centroid (docking.cpp:76)
-    // FP64 start pose to global (read back by the exact refinement); FP32 coordinates relative to
-    // the centroid (A, DFS order) into this warp's shared slot.
+    const float cmx = warp_sum(sx) * inv_n, cmy = warp_sum(sy) * inv_n, cmz = warp_sum(sz) * inv_n;
     float ext = 0.f;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const uint32_t a = lane + 32 * s;
       if (a < n) {
-        gpose[3 * a] = P.x[s];
-        gpose[3 * a + 1] = P.y[s];
-        gpose[3 * a + 2] = P.z[s];
-        const V3d v = vsub(own(P, s), cen);
-        A[pos[s]] = make_float4(float(v.x), float(v.y), float(v.z), 0.f);
-        ext = fmaxf(ext, float(__dsqrt_rn(vdot(v, v))));
-      } else if (a < it.m.npad) {
+        const float vx = px[s] - cmx, vy = py[s] - cmy, vz = pz[s] - cmz;
+        A[a] = make_float4(vx, vy, vz, 0.f);
+        ext = fmaxf(ext, sqrtf(fmaf(vx, vx, fmaf(vy, vy, vz * vz))));
+      } else if (a < meta.npad) {
         A[a] = make_float4(1e6f, 1e6f, 1e6f, 0.f);  // padding: far outside, contributes exactly 1.0
       }
     }
     __syncwarp();
-    // Position error bound (grid units, per axis) of every FP32 coordinate this item produces:
-    // rounding of coordinates up to the grid size, plus the rotation error of the FP32 frames
-    // (the dihedral axis from FP32 endpoints is good to ~1e-6 rad) times the ligand extent.
-    // DESIGN.md §3.2 derives the constants.
-    const float ext_g = warp_max(ext) * pk.inv_spacing_f;
+    const V3d cen{t4.x + double(cmx), t4.y + double(cmy), t4.z + double(cmz)};
+    // Position error bound (grid units, per axis) of every FP32 coordinate of this restart, as in
+    // K1b; the ligand extent gets a 1e-3 grid-unit allowance for FP32 rounding.
+    const float ext_g = warp_max(ext) * pk.inv_spacing_f + 1e-3f;
     const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
     const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
     const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
     const float eps = eps_s + 4e-6f;                              // coarse score error bound
     const float inv_n_scale = pk.coarse_scale / float(n);
 
-    GD_T(1);
     // ------------------------------------------------ coarse alignment sweep (all G rotations)
     // Lane l scores rotations g = l + 32 j. Per rotation the exact FP64 score lies in
     // [key_lo - eps, key_hi + eps] (key = coarse score, or for a rotation with a sample within ptol
@@ -405,7 +439,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     float dropped = -1e30f, lkey = -1e30f;
     unsigned long long amb_mask = 0ull;  // rotations j (g = lane + 32 j) with a face-ambiguous sample
-    const uint32_t npad = it.m.npad;
+    const uint32_t npad = meta.npad;
     const bool big_grid = pr.G > 64u * 32u;
     auto insert = [&](float key_hi, uint32_t g) {
       if (key_hi > top_s[KTOP - 1]) {
@@ -528,14 +562,142 @@ __global__ void __launch_bounds__(NT, 1)
       insert(hi * inv_n_scale + eps, g);  // one extra eps for the clamp
       lkey = fmaxf(lkey, lo * inv_n_scale);
     }
-    GD_T(2);
     const float B = warp_max(lkey);
     const float thr = B - 2.0f * eps;
     const bool overflow = __any_sync(FULL, dropped >= thr) || B < -1e29f || B > 1e29f || big_grid;
-    // exact FP64 re-scoring of the candidates, or (overflow) of every rotation
+    // candidate list for K1b (order irrelevant: K1b takes max exact score, lowest index)
+    uint32_t cnt = 0;
+    if (!overflow) {
+#pragma unroll
+      for (int t = 0; t < KTOP; ++t) {
+        const bool c = top_s[t] >= thr;
+        const uint32_t pend = __ballot_sync(FULL, c);
+        const uint32_t at = cnt + __popc(pend & ((1u << lane) - 1u));
+        if (c && at < uint32_t(kAlignCand)) b.rs_cand[size_t(item) * kAlignCand + at] = uint16_t(top_g[t]);
+        cnt += __popc(pend);
+      }
+    }
+    if (lane == 0) b.rs_ncand[item] = (overflow || cnt > uint32_t(kAlignCand)) ? -1 : int32_t(cnt);
+  }
+}
+
+
+// ============================================================================ the kernel
+// NT = threads per CTA (launch bound): 64 registers at 1024 threads spilled the smem bases inside
+// the hot loops, so the kernel trades warps for registers (DESIGN.md §4).
+template <int NS, int NT, bool SC>
+__global__ void __launch_bounds__(NT, 1)
+    dock_fast_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t slot_floats) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
+  // SC: the pocket cells are staged once per CTA into shared memory (every warp of every work item
+  // reads them; a compile-time flag so the gather is an LDS.128, not a generic load)
+  uint4* sc = reinterpret_cast<uint4*>(smem_raw);
+  const uint4* cells = SC ? sc : pk.cells;
+  float* slots = SC ? reinterpret_cast<float*>(sc + n_cells) : reinterpret_cast<float*>(smem_raw);
+  if (SC) {
+    for (uint32_t i = threadIdx.x; i < n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
+    __syncthreads();
+  }
+  float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
+  // Behind the atom slot, max(NS, 2) words per atom: the per-step survivor words (word t of moved
+  // atom m (DFS) at SURV[(m-s0-1)*NS+t]), reused as the FP64 scratch of the index-order sums (SCR1,
+  // n doubles, while A is live). Before the sweep A is not live yet and A + SURV hold 3 n doubles
+  // (SCR3, the centroid sums).
+  uint32_t* SURV = reinterpret_cast<uint32_t*>(A + ((b.max_n + 3) & ~3u));
+  double* SCR1 = reinterpret_cast<double*>(SURV);
+  double* SCR3 = reinterpret_cast<double*>(A);
+  const CoarseGrid cg{cells,
+                      0.5f * float(pk.cell_dims[0]),
+                      0.5f * float(pk.cell_dims[1]),
+                      0.5f * float(pk.cell_dims[2]),
+                      pk.cell_dims[0],
+                      pk.cell_dims[0] * pk.cell_dims[1],
+                      0x4B000000u * (1u + pk.cell_dims[0] + pk.cell_dims[0] * pk.cell_dims[1])};
+  const uint32_t N = pr.n_restarts;
+  const uint64_t total = uint64_t(b.n_lig) * N;
+  const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
+  unsigned long long st_aexact = 0, st_afall = 0, st_sexact = 0, st_sfall = 0, st_commit = 0, st_items = 0;
+#ifdef GD_PHASE_TIMERS
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_ph = clock64();
+  int cur_ph = 7;
+#endif
+
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(b.work_counter, 1u);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= total) break;
+    if (*(volatile int*)b.error != 0) break;
+    ++st_items;
+    GD_T(0);
+    Item it;
+    it.lig = item / N;
+    it.rs = item - it.lig * N;
+    it.m = b.meta[it.lig];
+    it.n = it.m.n;
+    it.W = (it.n + 31) >> 5;
+    const uint32_t n = it.n, R = it.m.nr;
+    double* gpose = b.rs_xyz + (size_t(it.m.atom_base) * N + size_t(it.rs) * n) * 3;
+
+    // ------------------------------------------------ starting pose (docking.cpp:52-69), FP64
+    Pose<NS> P;
+    uint32_t pos[NS];
+    double rad[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const uint32_t a = lane + 32 * s;
+      double4 at = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (a < n) at = b.atoms[it.m.atom_base + a];
+      set_own(P, s, V3d{at.x, at.y, at.z});
+      rad[s] = at.w;
+      pos[s] = a < n ? b.dfs_pos[it.m.atom_base + a] : 0;
+    }
+    {
+      const V3d c0 = centroid_smem<NS>(P, n, SCR3, lane);
+      const double4 q4 = b.start[2 * size_t(item)];
+      const double4 t4 = b.start[2 * size_t(item) + 1];
+      const Qd qs{q4.x, q4.y, q4.z, q4.w};
+      const V3d tgt{t4.x, t4.y, t4.z};
+#pragma unroll
+      for (int s = 0; s < NS; ++s) set_own(P, s, vadd(qapply(qs, vsub(own(P, s), c0)), tgt));
+    }
+    const V3d cen = centroid_smem<NS>(P, n, SCR3, lane);  // best_rotation_in_range's centroid (docking.cpp:76)
+    // FP64 start pose to global (read back by the full FP64 alignment); the ligand extent about the
+    // centroid sets the position error bound of the FP32 sweep below.
+    float ext = 0.f;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const uint32_t a = lane + 32 * s;
+      if (a < n) {
+        gpose[3 * a] = P.x[s];
+        gpose[3 * a + 1] = P.y[s];
+        gpose[3 * a + 2] = P.z[s];
+        const V3d v = vsub(own(P, s), cen);
+        ext = fmaxf(ext, float(__dsqrt_rn(vdot(v, v))));
+      }
+    }
+    __syncwarp();
+    // Position error bound (grid units, per axis) of every FP32 coordinate this item produces:
+    // rounding of coordinates up to the grid size, plus the rotation error of the FP32 frames
+    // (the dihedral axis from FP32 endpoints is good to ~1e-6 rad) times the ligand extent.
+    // DESIGN.md §3.2 derives the constants.
+    const float ext_g = warp_max(ext) * pk.inv_spacing_f;
+    const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
+    const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
+    const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
+    const float inv_n_scale = pk.coarse_scale / float(n);
+
+    GD_T(2);
+    // ------------------------------------------------ exact FP64 re-scoring (docking.cpp:71-91) of
+    // K1a's candidate rotations, or (ncand < 0: overflow / plateau) of every rotation
+    const int32_t ncand = b.rs_ncand[item];
     double best_s = -1.0;
     uint32_t best_g = 0xffffffffu;
-    if (overflow) {
+    if (ncand < 0 || pr.G > 65535u) {
       ++st_afall;
       for (uint32_t g = lane; g < pr.G; g += 32) {
         const double4 gq = pr.grid[g];
@@ -548,25 +710,20 @@ __global__ void __launch_bounds__(NT, 1)
     } else {
       // warp-cooperative exact scoring: candidates one at a time, lanes over atoms (P still holds
       // the start pose), index-order sum through shuffles; every lane ends with the same best
+      const uint32_t my_g = lane < uint32_t(ncand) ? b.rs_cand[size_t(item) * kAlignCand + lane] : 0u;
+      for (int32_t c = 0; c < ncand; ++c) {
+        const uint32_t g = __shfl_sync(FULL, my_g, c);
+        ++st_aexact;
+        const double4 gq = pr.grid[g];
+        const Qd q{gq.x, gq.y, gq.z, gq.w};
+        double ns[NS];
 #pragma unroll
-      for (int t = 0; t < KTOP; ++t) {
-        uint32_t pend = __ballot_sync(FULL, top_s[t] >= thr);
-        while (pend) {
-          const uint32_t src = __ffs(pend) - 1;
-          pend &= pend - 1;
-          const uint32_t g = __shfl_sync(FULL, top_g[t], src);
-          ++st_aexact;
-          const double4 gq = pr.grid[g];
-          const Qd q{gq.x, gq.y, gq.z, gq.w};
-          double ns[NS];
-#pragma unroll
-          for (int s = 0; s < NS; ++s)
-            ns[s] = lane + 32 * s < n ? sample_exact_ni(pk, rotated_about(own(P, s), cen, q)) : 0.0;
-          const double sc = __ddiv_rn(ordered_sum<NS>(ns, n), double(n));
-          if (best_g == 0xffffffffu || sc > best_s || (sc == best_s && g < best_g)) {
-            best_s = sc;
-            best_g = g;
-          }
+        for (int s = 0; s < NS; ++s)
+          ns[s] = lane + 32 * s < n ? sample_exact_ni(pk, rotated_about(own(P, s), cen, q)) : 0.0;
+        const double sc = __ddiv_rn(ordered_sum_smem<NS>(ns, n, SCR3, lane), double(n));
+        if (best_g == 0xffffffffu || sc > best_s || (sc == best_s && g < best_g)) {
+          best_s = sc;
+          best_g = g;
         }
       }
     }
@@ -599,6 +756,23 @@ __global__ void __launch_bounds__(NT, 1)
 
     // ------------------------------------------------ dihedral sweep (docking.cpp:155-167, 197-215)
     if (R > 0 && pr.reps > 0 && pr.S > 0) {
+      // Per-restart register caches (no global load on a step's critical path): lane r holds
+      // rotamer r's bond (i | j << 16) and DFS range (s0 | e0 << 16, pos(i)) for r < 32 (later
+      // rotamers load from global), and the FP32 half-angle (cos, sin) of its candidates k = lane + 1
+      // (pass 0) and 33 + (lane >> lg2) (pass 1).
+      uint32_t rc_ij = 0u, rc_se = 0u, rc_ip = 0u;
+      if (lane < R) {
+        const uint2 ij = b.rots[it.m.rot_base + lane];
+        const ushort4 rd = b.rdfs[it.m.rot_base + lane];
+        rc_ij = ij.x | (ij.y << 16);
+        rc_se = uint32_t(rd.x) | (uint32_t(rd.y) << 16);
+        rc_ip = rd.z;
+      }
+      const uint32_t n_cand_all = pr.S > 1 ? pr.S - 1 : 0;
+      const uint32_t rem_all = n_cand_all > 32 ? n_cand_all - 32 : 0;
+      const uint32_t lg2_all = rem_all <= 1 ? 5 : rem_all <= 2 ? 4 : rem_all <= 4 ? 3 : rem_all <= 8 ? 2 : rem_all <= 16 ? 1 : 0;
+      const float2 cq_p0 = lane + 1 <= n_cand_all ? __ldg(pr.dtab_f + lane + 1) : make_float2(1.f, 0.f);
+      const float2 cq_p1 = (lane >> lg2_all) < rem_all ? __ldg(pr.dtab_f + 33 + (lane >> lg2_all)) : make_float2(1.f, 0.f);
       // Per-pose caches, rebuilt after alignment and after every k != 0 commit:
       //   A[pos]     FP32 (gx, gy, gz, rho = cf*r/spacing) in DFS order,
       //   es, cs     exact FP64 and coarse per-atom samples, samb: coarse sample near a face,
@@ -618,6 +792,9 @@ __global__ void __launch_bounds__(NT, 1)
       // |computed - exact| of d^2 - t^2 for pairs near the threshold (d ~ t <= 2 rmax):
       // 2 d |dd| with |dd| <= 2 sqrt(3) ptol, plus FP32 rounding of t^2 and the chain.
       const float tau = 16.0f * rmax * ptol + 4e-6f * rmax * rmax + 1e-6f;
+      // survivor margin on the circle distance: (t + st)^2 - t^2 >= 4 tau, plus 1e-3 grid units for
+      // the FP32 rounding of the cylindrical coordinates (~1e-6 |w|)
+      const float st = 2.0f * sqrtf(tau) + 1e-3f;
 
       auto refresh = [&](bool all, const uint32_t (&mo)[NS]) {
 #pragma unroll
@@ -647,18 +824,25 @@ __global__ void __launch_bounds__(NT, 1)
           if (a >= n) continue;
           const float4 pa = A[pos[s]];
           const uint32_t* adrow = b.adjd + it.m.adj_base + pos[s] * it.W;
-          for (uint32_t q = 0; q < n; ++q) {
-            const float4 pb = A[q];
-            const float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
-            const float t = pa.w + pb.w;
-            const float mg = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -t * t)));
-            if (q == pos[s] || ((__ldg(adrow + (q >> 5)) >> (q & 31)) & 1u)) continue;
-            if (mg < -tau) {
-              crow[s][q >> 5] |= 1u << (q & 31);
-            } else if (mg <= tau) {
-              arow[s][q >> 5] |= 1u << (q & 31);
-              any_amb = true;
+#pragma unroll
+          for (int w = 0; w < NS; ++w) {
+            if (uint32_t(w) >= it.W) break;
+            // bonded partners and the atom itself are not bump pairs (scoring.cpp:53-55)
+            const uint32_t skip = __ldg(adrow + w) | (pos[s] >> 5 == uint32_t(w) ? 1u << (pos[s] & 31) : 0u);
+            const uint32_t qe = min(n, 32u * w + 32u);
+            uint32_t cw = 0u, aw = 0u;
+            for (uint32_t q = 32u * w; q < qe; ++q) {
+              const float4 pb = A[q];
+              const float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
+              const float t = pa.w + pb.w;
+              const float mg = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -t * t)));
+              const uint32_t bit = 1u << (q & 31);
+              cw |= mg < -tau ? bit : 0u;
+              aw |= (mg >= -tau && mg <= tau) ? bit : 0u;
             }
+            crow[s][w] = cw & ~skip;
+            arow[s][w] = aw & ~skip;
+            any_amb |= arow[s][w] != 0u;
           }
         }
         if (__any_sync(FULL, any_amb)) {  // near-threshold pairs: exact FP64 verdict
@@ -668,8 +852,14 @@ __global__ void __launch_bounds__(NT, 1)
             const double rb = b.atoms[it.m.atom_base + bb].w;
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
-              if ((arow[s][q >> 5] >> (q & 31)) & 1u) {
-                if (pair_clash_exact(own(P, s), pb, rad[s], rb, pr.clash)) crow[s][q >> 5] |= 1u << (q & 31);
+              const uint32_t bit = 1u << (q & 31);
+              if (arow[s][q >> 5] & bit) {
+                // exact verdict (scoring.cpp:52-58: clash iff d^2 < thr^2 iff d^2 - thr^2 < 0); the
+                // pair stays flagged ("razor") only if its exact margin is within 1e-8 A^2, where
+                // the FP64 rounding of a rotated candidate (~1e-12 A^2) could flip an invariant pair
+                const double mg = pair_margin_exact(own(P, s), pb, rad[s], rb, pr.clash);
+                if (mg < 0.0) crow[s][q >> 5] |= bit;
+                if (!(fabs(mg) <= 1e-8)) arow[s][q >> 5] &= ~bit;
               }
             }
           }
@@ -686,52 +876,76 @@ __global__ void __launch_bounds__(NT, 1)
       for (uint32_t rep = 0; rep < pr.reps; ++rep) {
         for (uint32_t r = 0; r < R; ++r) {
           GD_T(4);
-          const uint2 ij = b.rots[it.m.rot_base + r];
-          const ushort4 rd = b.rdfs[it.m.rot_base + r];
-          const uint32_t s0 = rd.x, e0 = rd.y, ipos = rd.z;
-          // M' = moving set minus atom_j (molecule.cpp:166-169), original and DFS bit spaces
-          uint32_t mo[NS], md[NS];
-#pragma unroll
-          for (int w = 0; w < NS; ++w) {
-            mo[w] = uint32_t(w) < it.W ? __ldg(b.masks + it.m.mask_base + r * it.W + w) : 0u;
-            md[w] = 0u;
+          uint2 ij;
+          uint32_t s0, e0, ipos;
+          if (r < 32) {
+            const uint32_t pij = __shfl_sync(FULL, rc_ij, r), pse = __shfl_sync(FULL, rc_se, r);
+            ij = make_uint2(pij & 0xffffu, pij >> 16);
+            s0 = pse & 0xffffu;
+            e0 = pse >> 16;
+            ipos = __shfl_sync(FULL, rc_ip, r);
+          } else {
+            ij = b.rots[it.m.rot_base + r];
+            const ushort4 rd = b.rdfs[it.m.rot_base + r];
+            s0 = rd.x;
+            e0 = rd.y;
+            ipos = rd.z;
           }
-          mo[ij.y >> 5] &= ~(1u << (ij.y & 31));
+          // M' = moving set minus atom_j (molecule.cpp:166-169), original (mo) and DFS (md) bit
+          // spaces. Fast layout: M' is the DFS range (s0, e0), so both follow from the range.
+          uint32_t mo[NS], md[NS];
           bool inm[NS];
+          if (it.m.fast_ok) {
 #pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            const uint32_t a = lane + 32 * s;
-            inm[s] = a < n && bit4(mo, a);
+            for (int s = 0; s < NS; ++s) {
+              inm[s] = lane + 32 * s < n && pos[s] > s0 && pos[s] < e0;
+              mo[s] = __ballot_sync(FULL, inm[s]);  // slot s holds atoms 32 s + lane
+              md[s] = range_word(uint32_t(s), s0 + 1, e0);
+            }
+          } else {
+#pragma unroll
+            for (int w = 0; w < NS; ++w) {
+              mo[w] = uint32_t(w) < it.W ? __ldg(b.masks + it.m.mask_base + r * it.W + w) : 0u;
+              md[w] = 0u;
+            }
+            mo[ij.y >> 5] &= ~(1u << (ij.y & 31));
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+              const uint32_t a = lane + 32 * s;
+              inm[s] = a < n && bit4(mo, a);
+#pragma unroll
+              for (int w = 0; w < NS; ++w)
+                if (inm[s] && (pos[s] >> 5) == uint32_t(w)) md[w] |= 1u << (pos[s] & 31);
+            }
 #pragma unroll
             for (int w = 0; w < NS; ++w)
-              if (inm[s] && (pos[s] >> 5) == uint32_t(w)) md[w] |= 1u << (pos[s] & 31);
+              for (int o = 16; o > 0; o >>= 1) md[w] |= __shfl_xor_sync(FULL, md[w], o);
           }
-#pragma unroll
-          for (int w = 0; w < NS; ++w)
-            for (int o = 16; o > 0; o >>= 1) md[w] |= __shfl_xor_sync(FULL, md[w], o);
           // invariant pairs (both in M' or both outside) of the current pose: exact from crow
-          bool inv_l = false, frag_l = false, cne_l = false, famb_l = false;
+          bool inv_l = false, frag_l = false, cne_l = false;
           float fsum = 0.f;
 #pragma unroll
           for (int s = 0; s < NS; ++s) {
             if (lane + 32 * s >= n) continue;
+            // Invariant pairs: both in M', both outside M', and (m, atom_j) — j lies on the axis,
+            // so |m - j| does not change with the angle either. Their exact verdicts (crow) hold
+            // for every candidate unless the exact margin is razor-thin (arow after refresh).
+            const bool isj = pos[s] == s0;
 #pragma unroll
             for (int w = 0; w < NS; ++w) {
               const uint32_t lo = 32u * w;
               const uint32_t valid = lo + 32u <= n ? FULL : (lo >= n ? 0u : ((1u << (n - lo)) - 1u));
-              inv_l |= (crow[s][w] & (inm[s] ? md[w] : (~md[w] & valid))) != 0u;
-              if (inm[s]) frag_l |= (arow[s][w] & md[w]) != 0u;
+              const uint32_t mdj = md[w] | ((s0 >> 5) == uint32_t(w) ? 1u << (s0 & 31) : 0u);
+              inv_l |= (crow[s][w] & (inm[s] ? mdj : isj ? valid : (~md[w] & valid))) != 0u;
+              if (inm[s]) frag_l |= (arow[s][w] & mdj) != 0u;
+              if (isj) frag_l |= (arow[s][w] & md[w]) != 0u;
               cne_l |= crow[s][w] != 0u;
             }
-            if (!inm[s]) {
-              fsum += cs[s];
-              famb_l |= samb[s];
-            }
+            if (!inm[s]) fsum += cs[s];
           }
           const bool inv = __any_sync(FULL, inv_l);
           const bool frag = __any_sync(FULL, frag_l);
           const bool elig0 = !__any_sync(FULL, cne_l);  // k = 0: the current pose passes bump_check
-          const bool famb = __any_sync(FULL, famb_l);
           fsum = warp_sum(fsum);
           // FP64 axis (rotate_fragment, molecule.cpp:150-160), computed when first needed; the
           // DegenerateAxisError check (len < 1e-12) only needs FP64 when the FP32 bond is tiny
@@ -769,8 +983,8 @@ __global__ void __launch_bounds__(NT, 1)
             get_axis();
             for (uint32_t k = 0; k < pr.S; ++k) {
               const Qd q = frag_quat(pr.dtab[k], axis);
-              const double sk = k == 0 ? __ddiv_rn(ordered_sum<NS>(es, n), double(n))
-                                       : exact_candidate_score<NS>(pk, it, P, es, mo, pi, q, lane);
+              const double sk = k == 0 ? __ddiv_rn(ordered_sum_smem<NS>(es, n, SCR1, lane), double(n))
+                                       : exact_candidate_score<NS>(pk, it, P, es, mo, pi, q, lane, SCR1);
               bool clash;
               if (k == 0) clash = !elig0;
               else if (frag) clash = exact_clash<NS>(b, it, P, rad, mo, true, pi, q, pr.clash, false, lane);
@@ -793,6 +1007,52 @@ __global__ void __launch_bounds__(NT, 1)
               ay *= il;
               az *= il;
             }
+            // Cross-pair survivors. Rotating M' about the axis keeps each moved atom m on a circle
+            // (axial coordinate h, radius rho about the FP32 axis through pi). A fixed-side atom
+            // whose distance to that circle, sqrt(dh^2 + drho^2), is at least t + 2 sqrt(tau) + 1e-3
+            // passes bump_check at every candidate angle with margin, so its d^2 - t^2 is >= tau for
+            // every k and cannot change any candidate's status. Bit f of word
+            // SURV[(m - s0 - 1) NS + f / 32] marks the other partners of m on the fixed side
+            // [0, s0) U [e0, n) (pairs with atom_j are invariant, see above).
+            {
+              float hq[NS], rq[NS], tq[NS];
+#pragma unroll
+              for (int t = 0; t < NS; ++t) {
+                const uint32_t q = lane + 32 * t;
+                hq[t] = rq[t] = tq[t] = 0.f;
+                if (q < n) {
+                  const float4 pq = A[q];
+                  const float wx = pq.x - fpi.x, wy = pq.y - fpi.y, wz = pq.z - fpi.z;
+                  const float h = fmaf(wx, ax, fmaf(wy, ay, wz * az));
+                  const float px = fmaf(-h, ax, wx), py = fmaf(-h, ay, wy), pz = fmaf(-h, az, wz);
+                  hq[t] = h;
+                  rq[t] = sqrtf(fmaf(px, px, fmaf(py, py, pz * pz)));
+                  tq[t] = pq.w + st;
+                }
+              }
+              for (uint32_t mq = s0 + 1; mq < e0; ++mq) {
+                const uint32_t sl = mq >> 5, src = mq & 31;
+                float hm = hq[0], rm = rq[0];
+#pragma unroll
+                for (int t = 1; t < NS; ++t)
+                  if (sl == uint32_t(t)) {
+                    hm = hq[t];
+                    rm = rq[t];
+                  }
+                hm = __shfl_sync(FULL, hm, src);
+                rm = __shfl_sync(FULL, rm, src);
+                const float tm = A[mq].w;
+#pragma unroll
+                for (int t = 0; t < NS; ++t) {
+                  const uint32_t q = lane + 32 * t;
+                  const bool fixed = q < n && (q < s0 || q >= e0);
+                  const float dh = hq[t] - hm, dr = rq[t] - rm, T = tq[t] + tm;
+                  const uint32_t word = __ballot_sync(FULL, fixed && fmaf(dh, dh, dr * dr) < T * T);
+                  if (lane == uint32_t(t)) SURV[(mq - s0 - 1) * NS + t] = word;
+                }
+              }
+              __syncwarp();
+            }
             float res_s[2] = {-1e30f, -1e30f};
             uint32_t res_st[2] = {0u, 0u};
             const uint32_t n_cand = pr.S - 1;  // k = 1 .. S-1
@@ -806,9 +1066,11 @@ __global__ void __launch_bounds__(NT, 1)
               const uint32_t grp = lane >> sh, sub = lane & (gs - 1);
               const uint32_t k = pass == 0 ? lane + 1 : 33 + grp;
               const bool active = pass == 0 ? (k <= n_cand) : (grp < rem);
+              // this lane's share of the survivors: bit positions congruent to sub modulo gs
+              const uint32_t mypat = (gs >= 32 ? 1u : FULL / ((1u << gs) - 1u)) << sub;
               float part = 0.f, amin = 1e30f, mmin = 1e30f, emin = 1e30f;
               if (active) {
-                const float2 cq = __ldg(pr.dtab_f + k);
+                const float2 cq = pass == 0 ? cq_p0 : cq_p1;
                 const float qw = cq.x, qx = ax * cq.y, qy = ay * cq.y, qz = az * cq.y;
                 const float xx = qx * qx, yy = qy * qy, zz = qz * qz, xy = qx * qy, xz = qx * qz, yz = qy * qz;
                 const float wx = qw * qx, wy = qw * qy, wz = qw * qz;
@@ -824,20 +1086,15 @@ __global__ void __launch_bounds__(NT, 1)
                   const float gy = fmaf(m10, pm.x, fmaf(m11, pm.y, fmaf(m12, pm.z, tvy)));
                   const float gz = fmaf(m20, pm.x, fmaf(m21, pm.y, fmaf(m22, pm.z, tvz)));
                   if (((mq - s0 - 1) & (gs - 1)) == sub) part += coarse_sample_e(cg, gx, gy, gz, amin, emin) - 1.0f;
-                  // cross pairs with the fixed side [0, s0) U [e0, n) and with atom_j unless bonded
-                  for (uint32_t f = sub; f < s0; f += gs) {
-                    const float4 pf = A[f];
-                    const float dx = gx - pf.x, dy = gy - pf.y, dz = gz - pf.z, tt = pm.w + pf.w;
-                    mmin = fminf(mmin, fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -tt * tt))));
-                  }
-                  for (uint32_t f = e0 + sub; f < n; f += gs) {
-                    const float4 pf = A[f];
-                    const float dx = gx - pf.x, dy = gy - pf.y, dz = gz - pf.z, tt = pm.w + pf.w;
-                    mmin = fminf(mmin, fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -tt * tt))));
-                  }
-                  if (sub == 0 && !((__ldg(b.adjd + it.m.adj_base + mq * it.W + (s0 >> 5)) >> (s0 & 31)) & 1u)) {
-                    const float dx = gx - fpj.x, dy = gy - fpj.y, dz = gz - fpj.z, tt = pm.w + fpj.w;
-                    mmin = fminf(mmin, fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -tt * tt))));
+                  // surviving cross pairs (fixed side and atom_j unless bonded)
+                  const uint32_t* sv = SURV + (mq - s0 - 1) * NS;
+#pragma unroll
+                  for (int t = 0; t < NS; ++t) {
+                    for (uint32_t bits = sv[t] & mypat; bits; bits &= bits - 1) {
+                      const float4 pf = A[32 * t + __ffs(bits) - 1];
+                      const float dx = gx - pf.x, dy = gy - pf.y, dz = gz - pf.z, tt = pm.w + pf.w;
+                      mmin = fminf(mmin, fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -tt * tt))));
+                    }
                   }
                 }
               }
@@ -933,7 +1190,7 @@ __global__ void __launch_bounds__(NT, 1)
                   const uint32_t k = (h == 0 ? 1u : 33u) + src;
                   ++st_sexact;
                   get_axis();
-                  const double sk = exact_candidate_score<NS>(pk, it, P, es, mo, pi, frag_quat(pr.dtab[k], axis), lane);
+                  const double sk = exact_candidate_score<NS>(pk, it, P, es, mo, pi, frag_quat(pr.dtab[k], axis), lane, SCR1);
                   if (!committed || sk > bs || (sk == bs && k < bk)) {
                     committed = true;
                     bk = k;
@@ -996,41 +1253,61 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
-template <int NS, int NT, bool SC>
-static cudaError_t launch_sc(int warps, size_t smem, const DevPocket& pk, const DevParams& pr, const DevBatch& b,
-                             uint32_t slot_floats, int n_sms, cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(dock_fast_kernel<NS, NT, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  dock_fast_kernel<NS, NT, SC><<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, slot_floats);
-  return cudaGetLastError();
-}
+// Shared-memory plan of one persistent kernel: the pocket cells (when they fit next to 8 warp
+// slots) plus one slot per warp, as many warps as fit up to NT / 32.
+struct SmemPlan {
+  bool cells_in_smem;
+  int warps;
+  size_t smem;
+};
 
-template <int NS, int NT>
-static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                             cudaStream_t stream) {
+static SmemPlan plan_smem(const DevPocket& pk, size_t slot_bytes, int max_warps) {
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
   const size_t cell_bytes = size_t(n_cells) * sizeof(uint4);
-  const uint32_t npad_max = (b.max_n + 3) & ~3u;
-  const uint32_t slot_floats = 4 * npad_max;
-  const size_t slot_bytes = size_t(slot_floats) * sizeof(float);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const bool cells_in_smem = cell_bytes + 8 * slot_bytes <= size_t(optin);
-  const size_t avail = size_t(optin) - (cells_in_smem ? cell_bytes : 0);
-  int warps = int(avail / slot_bytes);
-  if (warps > NT / 32) warps = NT / 32;
-  if (warps < 1) return cudaErrorInvalidConfiguration;
-  const size_t smem = (cells_in_smem ? cell_bytes : 0) + slot_bytes * warps;
-  return cells_in_smem ? launch_sc<NS, NT, true>(warps, smem, pk, pr, b, slot_floats, n_sms, stream)
-                       : launch_sc<NS, NT, false>(warps, smem, pk, pr, b, slot_floats, n_sms, stream);
+  SmemPlan p{};
+  p.cells_in_smem = cell_bytes + 8 * slot_bytes <= size_t(optin);
+  const size_t avail = size_t(optin) - (p.cells_in_smem ? cell_bytes : 0);
+  p.warps = int(avail / slot_bytes);
+  if (p.warps > max_warps) p.warps = max_warps;
+  p.smem = (p.cells_in_smem ? cell_bytes : 0) + slot_bytes * size_t(p.warps > 0 ? p.warps : 0);
+  return p;
+}
+
+template <class K>
+static cudaError_t launch_persistent(K kernel, const SmemPlan& p, int n_sms, cudaStream_t stream, const DevPocket& pk,
+                                     const DevParams& pr, const DevBatch& b, uint32_t slot_floats) {
+  if (p.warps < 1) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem));
+  if (e != cudaSuccess) return e;
+  kernel<<<n_sms, 32 * p.warps, p.smem, stream>>>(pk, pr, b, slot_floats);
+  return cudaGetLastError();
+}
+
+// K1a (coarse alignment, NTA threads) then K1b (exact refinement + dihedral sweep, NTB threads).
+template <int NS, int NTA, int NTB>
+static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
+                             cudaStream_t stream) {
+  const uint32_t npad_max = (b.max_n + 3) & ~3u;
+  const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
+  const uint32_t slot_b = (4 + (NS > 2 ? NS : 2)) * npad_max;  // A + SURV/SCR (max(NS, 2) words per atom)
+  const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32);
+  cudaError_t e = pa.cells_in_smem
+                      ? launch_persistent(align_coarse_kernel<NS, NTA, true>, pa, n_sms, stream, pk, pr, b, slot_a)
+                      : launch_persistent(align_coarse_kernel<NS, NTA, false>, pa, n_sms, stream, pk, pr, b, slot_a);
+  if (e != cudaSuccess) return e;
+  const SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32);
+  return pb.cells_in_smem ? launch_persistent(dock_fast_kernel<NS, NTB, true>, pb, n_sms, stream, pk, pr, b, slot_b)
+                          : launch_persistent(dock_fast_kernel<NS, NTB, false>, pb, n_sms, stream, pk, pr, b, slot_b);
 }
 
 cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                         cudaStream_t stream) {
-  if (b.max_n <= 32) return launch_ns<1, GD_FAST_THREADS>(pk, pr, b, n_sms, stream);
-  if (b.max_n <= 64) return launch_ns<2, GD_FAST_THREADS>(pk, pr, b, n_sms, stream);
-  if (b.max_n <= 128) return launch_ns<4, GD_FAST_THREADS_NS4>(pk, pr, b, n_sms, stream);
+  if (b.max_n <= 32) return launch_ns<1, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream);
+  if (b.max_n <= 64) return launch_ns<2, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream);
+  if (b.max_n <= 128) return launch_ns<4, GD_ALIGN_THREADS, GD_FAST_THREADS_NS4>(pk, pr, b, n_sms, stream);
   return cudaErrorNotSupported;  // launch_dock routes > 128 atoms to the exact kernel
 }
 

@@ -12,6 +12,7 @@ namespace gdk {
 
 constexpr int kMaxAtoms = 256;      // GD_MAX_ATOMS
 constexpr int kMaxWords = kMaxAtoms / 32;
+constexpr int kAlignCand = 32;      // alignment candidates handed from K1a to K1b per restart
 
 // Per-ligand metadata (32 B, one coalesced load per warp).
 struct LigMeta {
@@ -78,6 +79,8 @@ struct DevBatch {
   const ushort4* rdfs;     // per rotamer: (s = DFS pos of j, e = end of moving range, DFS pos of i, 0)
   const uint32_t* adjd;    // bonded bitmask rows in DFS space: adjd[adj_base + pos*W + w]
   // per-restart scratch / trace
+  uint16_t* rs_cand;       // K1a -> K1b: alignment candidates of restart `item`, [item*kAlignCand ..)
+  int32_t* rs_ncand;       // candidate count, or -1: full FP64 alignment (overflow / plateau)
   double* rs_score;
   double* rs_align_score;
   uint32_t* rs_align_index;
@@ -90,7 +93,7 @@ struct DevBatch {
   double* final_xyz;
   double* final_dih;
   // control
-  unsigned int* work_counter;
+  unsigned int* work_counter;  // [0] K1 / K1b items, [1] K1a items
   int* error;              // [0] = status, [1] = ligand index
   unsigned long long* stats;  // gd_stats counters (6 x u64)
 };

@@ -259,7 +259,7 @@ __global__ void finalize_kernel(DevParams pr, DevBatch b) {
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                         cudaStream_t stream, int* launches) {
   *launches = 0;
-  cudaError_t e = cudaMemsetAsync(b.work_counter, 0, sizeof(unsigned int), stream);
+  cudaError_t e = cudaMemsetAsync(b.work_counter, 0, 2 * sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
   if (b.n_lig == 0) return cudaSuccess;
   const int mode = pr.mode & 0xff;
@@ -275,9 +275,9 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
     dock_exact_kernel<<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, stride);
     ++*launches;
   } else {
-    e = launch_fast(pk, pr, b, n_sms, stream);
+    e = launch_fast(pk, pr, b, n_sms, stream);  // K1a + K1b
     if (e != cudaSuccess) return e;
-    ++*launches;
+    *launches += 2;
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;

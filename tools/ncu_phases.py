@@ -13,24 +13,29 @@ src = open(__file__.replace("tools/ncu_phases.py", "paper_1901_06229_b200/csrc/g
 
 
 def find(pat):
-    for i, l in enumerate(src):
-        if pat in l:
+    lines = pat.split("\n")
+    for i in range(len(src)):
+        if all(lines[k].strip() in src[i + k] for k in range(len(lines)) if i + k < len(src)):
             return i + 1
     raise KeyError(pat)
 
 
 marks = [("setup/start-pose", find("dock_fast_kernel(DevPocket pk")),
-         ("align-coarse", find("coarse alignment sweep (all G rotations)")),
-         ("align-ambig-pass", find("second pass over face-ambiguous")),
-         ("align-exact", find("exact FP64 re-scoring of the candidates")),
+         ("align-exact", find("exact FP64 re-scoring (docking.cpp:71-91)")),
          ("sweep-setup+refresh", find("dihedral sweep (docking.cpp:155-167")),
          ("step-head", find("for (uint32_t rep = 0; rep < pr.reps; ++rep)")),
          ("step-slowpath", find("slow path: every candidate exactly")),
-         ("step-coarse-cand", find("coarse evaluation of every candidate k = 1")),
+         ("step-axis", find("coarse evaluation of every candidate k = 1")),
+         ("step-survivors", find("Cross-pair survivors.")),
+         ("step-cand-setup", find("float res_s[2] = {-1e30f, -1e30f};")),
+         ("step-cand-loop", find("for (uint32_t mq = s0 + 1; mq < e0; ++mq) {\n                  const float4 pm")),
+         ("step-cand-reduce", find("for (uint32_t o = 1; o < gs; o <<= 1) {  // group reduction")),
          ("step-decisions", find("exact decisions (reference semantics")),
          ("step-commit", find("commit = rotate_fragment(current, r, k*delta)")),
          ("restart-tail", find("restart result"))]
 kstart = marks[0][1]
+# prologue lines (lane, smem bases, grid constants) are rematerialised inside loops: transparent
+kloop = next(i + 1 for i in range(kstart, len(src)) if src[i].strip().startswith("for (;;) {"))
 # pass 1: collect (address, instr, samples, (file, line)) in page order
 hdr, fname, cur = None, None, None
 ins_rows = []
@@ -54,9 +59,9 @@ for r in rows:
             continue
         ins_rows.append((int(r[2], 16), ins, smp, cur))
 ins_rows.sort()
-phase, agg = "setup/start-pose", {}
+phase, agg = "k1b-prologue", {}
 for addr, ins, smp, (f, l) in ins_rows:
-    if f == "gd_fast.cu" and l >= kstart:
+    if f == "gd_fast.cu" and l > kloop:
         phase = [m for m, ln in marks if ln <= l][-1]
     a = agg.setdefault(phase, [0.0, 0.0])
     a[0] += ins

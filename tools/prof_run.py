@@ -15,10 +15,11 @@ ap.add_argument("--runs", type=int, default=2)
 ap.add_argument("--exact", action="store_true")
 ap.add_argument("--dims", type=int, default=24)
 ap.add_argument("--spacing", type=float, default=0.75)
+ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 ctx = gd.Context(0, mode=gd.MODE_EXACT if a.exact else gd.MODE_FAST)
 ctx.set_pocket(gd.make_pocket(gd.PocketSpec(dims=(a.dims,) * 3, spacing=a.spacing)))
-ctx.set_params(gd.DockParams(clash_factor=a.clash))
+ctx.set_params(gd.DockParams(clash_factor=a.clash, num_repetitions=a.reps))
 b = ctx.stage(gd.make_library(gd.LibrarySpec(a.ligands, a.atoms, a.rotamers, 0)))
 import time
 for i in range(a.runs):
