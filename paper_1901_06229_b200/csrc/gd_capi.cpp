@@ -367,7 +367,7 @@ DevPocket dev_pocket(const gd_ctx* ctx) {
   pk.inv_spacing_f = float(1.0 / ctx->spacing);
   pk.q_eps = ctx->q_eps;
   pk.max_step = ctx->max_step;
-  pk.coarse_scale = float(32768.0 / 32767.0);
+  pk.coarse_scale = 1.0f;
   return pk;
 }
 
@@ -500,24 +500,32 @@ int gd_set_pocket(gd_ctx* ctx, const uint32_t dims[3], const double origin[3], d
   GD_CUDA(ctx, cudaMalloc(&ctx->d_field, nv * sizeof(double)));
   GD_CUDA(ctx, cudaMemcpy(ctx->d_field, field, nv * sizeof(double), cudaMemcpyHostToDevice));
 
-  // Coarse-path cells: for every grid cell (ix,iy,iz) < dims-1, its 8 corner values as 15-bit
-  // fixed point u = round(v * 32767) with bit 15 set (so a byte permute turns a half-word into
-  // the float 1 + u/32768). Corner order: bit0 = +x, bit1 = +y, bit2 = +z.
+  // Coarse-path cells: for every grid cell (ix,iy,iz) < dims-1, its four x-edges
+  // (y, z in {0,1}) as a base value c = v(x) and a difference d = v(x+1) - v(x), one 32-bit word
+  // each: low half 0x8000 | uc with uc = round(32768 c) (a byte permute makes it the float
+  // C = 1 + uc/32768), high half ud = round(16384 (d + 1)) (the float D = 2 + ud/16384 = 3 + d').
+  // Then fma(fx, D, C) = (c' + fx d') + (1 + 3 fx): every x-lerp is one FFMA carrying the same
+  // bias, which cancels in the y- and z-lerps and is subtracted once. Word order: (y,z) = (0,0),
+  // (1,0), (0,1), (1,1). One extra dummy cell (c' = d' = 0) at index cx*cy*cz evaluates to exactly
+  // 0 for any fractions: samples outside the grid read it.
   const uint32_t cx = dims[0] - 1, cy = dims[1] - 1, cz = dims[2] - 1;
-  std::vector<uint4> cells(size_t(cx) * cy * cz);
+  std::vector<uint4> cells(size_t(cx) * cy * cz + 1);
   double max_step = 0.0;  // largest |v(i+1) - v(i)| along any axis: Lipschitz bound per cell
+  double q_err = 0.0;     // largest |c' - c| + |d' - d| over all x-edges: quantisation bound
   auto at = [&](uint32_t x, uint32_t y, uint32_t z) { return field[(size_t(z) * dims[1] + y) * dims[0] + x]; };
-  auto enc = [](double v) -> uint32_t {
-    double c = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
-    return 0x8000u | uint32_t(std::lround(c * 32767.0));
+  auto clamp01 = [](double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); };
+  auto edge = [&](uint32_t x, uint32_t y, uint32_t z) -> uint32_t {
+    const double c = clamp01(at(x, y, z)), d = clamp01(at(x + 1, y, z)) - c;
+    const long uc = std::min(32767L, std::lround(c * 32768.0));
+    const long ud = std::min(32767L, std::max(0L, std::lround((d + 1.0) * 16384.0)));
+    q_err = std::max(q_err, std::fabs(double(uc) / 32768.0 - c) + std::fabs((double(ud) / 16384.0 - 1.0) - d));
+    return (0x8000u | uint32_t(uc)) | (uint32_t(ud) << 16);
   };
   for (uint32_t z = 0; z < cz; ++z)
     for (uint32_t y = 0; y < cy; ++y)
       for (uint32_t x = 0; x < cx; ++x) {
-        uint32_t h[8];
-        for (int c = 0; c < 8; ++c) h[c] = enc(at(x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1)));
-        cells[(size_t(z) * cy + y) * cx + x] = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16),
-                                                          h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+        cells[(size_t(z) * cy + y) * cx + x] =
+            make_uint4(edge(x, y, z), edge(x, y + 1, z), edge(x, y, z + 1), edge(x, y + 1, z + 1));
         for (int c = 0; c < 8; ++c) {
           const double v0 = at(x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1));
           if (!(c & 1)) max_step = std::max(max_step, std::fabs(at(x + 1, y + ((c >> 1) & 1), z + ((c >> 2) & 1)) - v0));
@@ -525,14 +533,18 @@ int gd_set_pocket(gd_ctx* ctx, const uint32_t dims[3], const double origin[3], d
           if (!(c & 4)) max_step = std::max(max_step, std::fabs(at(x + (c & 1), y + ((c >> 1) & 1), z + 1) - v0));
         }
       }
+  const uint32_t dummy_half_c = 0x8000u, dummy_half_d = 16384u;  // c' = 0, d' = 0
+  const uint32_t dw = dummy_half_c | (dummy_half_d << 16);
+  cells.back() = make_uint4(dw, dw, dw, dw);
   bool in_range = true;
   for (size_t i = 0; i < nv; ++i) in_range &= (field[i] >= 0.0 && field[i] <= 1.0);
   GD_CUDA(ctx, cudaMalloc(&ctx->d_cells, cells.size() * sizeof(uint4)));
   GD_CUDA(ctx, cudaMemcpy(ctx->d_cells, cells.data(), cells.size() * sizeof(uint4), cudaMemcpyHostToDevice));
-  // Coarse error model: quantisation 0.5/32767 per corner value; the kernel adds
-  // 3 * max_step * (its FP32 position bound). A field outside [0,1] breaks the quantiser, so the
-  // fast path is disabled for it (q_eps = inf -> exact kernel).
-  ctx->q_eps = in_range ? float(0.5 / 32767.0) : INFINITY;
+  // Coarse error model: quantisation q_err per sample (the y- and z-lerps are
+  // convex combinations of x-edges); the kernel adds 3 * max_step * (its FP32 position bound). A
+  // field outside [0,1] breaks the quantiser, so the fast path is disabled for it (q_eps = inf ->
+  // exact kernel).
+  ctx->q_eps = in_range ? float(q_err * (1.0 + 1e-6)) : INFINITY;
   ctx->max_step = float(max_step);
   for (int i = 0; i < 3; ++i) {
     ctx->dims[i] = dims[i];

@@ -39,6 +39,10 @@ constexpr int kAlignUnroll = GD_ALIGN_UNROLL;
 #define GD_ALPHA_CHUNK 4
 #endif
 constexpr int kAlphaChunk = GD_ALPHA_CHUNK;
+#ifndef GD_QT_GROUPS
+#define GD_QT_GROUPS 2
+#endif
+constexpr int kQtGroups = GD_QT_GROUPS;  // quarter-turn groups per pass over the atoms
 // Optional device-side phase timers (build with -DGD_PHASE_TIMERS): per-warp clock64 deltas summed
 // into gd_stats-adjacent counters 8..15 (setup, align coarse, align refine, refresh, step head,
 // step coarse candidates, step decisions+commit, tail).
@@ -58,47 +62,44 @@ constexpr int kAlphaChunk = GD_ALPHA_CHUNK;
 constexpr uint32_t ST_CLASH = 1, ST_OK = 2, ST_XAMB = 4, ST_SAMB = 8, ST_ALLOUT = 16;
 
 struct CoarseGrid {
-  const uint4* cells;  // shared (or global) 8-corner cells
+  const uint4* cells;  // shared (or global) cells: four x-edges each, plus the dummy cell
   float hx, hy, hz;    // half extents (dims-1)/2 in grid units
   uint32_t cx, cxy;    // cells per row / per plane
   uint32_t koff;       // 0x4B000000 * (1 + cx + cxy): removes the 2^23 exponent bits of the three floors
+  uint32_t dummy;      // index of the dummy cell (every fraction evaluates to exactly 0)
 };
 
-// Decode of one 8-corner cell and the trilinear interpolation in the [1, 2) domain.
+// One cell: the four x-edges (C = 1 + c', D = 3 + d' by byte permutes) give fma(fx, D, C) =
+// (c' + fx d') + (1 + 3 fx); the common bias survives the y- and z-lerps unchanged and is removed
+// at the end. Returns the trilinear value of the quantised field.
+// Byte permutes against one constant K = 0x3F400000: C = bits 0x3F | half0 << 8 (selector 0x7104,
+// half0 carries bit 15, so C = 1 + uc/32768), D = bits 0x40 | half1 << 8 (selector 0x6324, D = 2 +
+// ud/16384). One shared constant lets every PRMT take an immediate selector.
+__device__ __forceinline__ float dec_c(uint32_t w) { return __uint_as_float(__byte_perm(w, 0x3F400000u, 0x7104)); }
+__device__ __forceinline__ float dec_d(uint32_t w) { return __uint_as_float(__byte_perm(w, 0x3F400000u, 0x6324)); }
+
 __device__ __forceinline__ float cell_lerp(const uint4 w, float fx, float fy, float fz) {
-  // byte permute: half-word 0x8000|u -> float bits 0x3F800000 | u<<8 = 1 + u/32768
-  const float c000 = __uint_as_float(__byte_perm(w.x, 0x3F000000u, 0x7104));
-  const float c100 = __uint_as_float(__byte_perm(w.x, 0x3F000000u, 0x7324));
-  const float c010 = __uint_as_float(__byte_perm(w.y, 0x3F000000u, 0x7104));
-  const float c110 = __uint_as_float(__byte_perm(w.y, 0x3F000000u, 0x7324));
-  const float c001 = __uint_as_float(__byte_perm(w.z, 0x3F000000u, 0x7104));
-  const float c101 = __uint_as_float(__byte_perm(w.z, 0x3F000000u, 0x7324));
-  const float c011 = __uint_as_float(__byte_perm(w.w, 0x3F000000u, 0x7104));
-  const float c111 = __uint_as_float(__byte_perm(w.w, 0x3F000000u, 0x7324));
-  const float c00 = fmaf(fx, c100 - c000, c000);
-  const float c10 = fmaf(fx, c110 - c010, c010);
-  const float c01 = fmaf(fx, c101 - c001, c001);
-  const float c11 = fmaf(fx, c111 - c011, c011);
-  const float c0 = fmaf(fy, c10 - c00, c00);
-  const float c1 = fmaf(fy, c11 - c01, c01);
-  return fmaf(fz, c1 - c0, c0);
+  const float x00 = fmaf(fx, dec_d(w.x), dec_c(w.x));
+  const float x10 = fmaf(fx, dec_d(w.y), dec_c(w.y));
+  const float x01 = fmaf(fx, dec_d(w.z), dec_c(w.z));
+  const float x11 = fmaf(fx, dec_d(w.w), dec_c(w.w));
+  const float y0 = fmaf(fy, x10 - x00, x00);
+  const float y1 = fmaf(fy, x11 - x01, x01);
+  return fmaf(fz, y1 - y0, y0) - fmaf(fx, 3.0f, 1.0f);
 }
 
-// One coarse sample at grid coordinates g. Returns 1 + v' (v' = trilinear of the
-// 15-bit codes u/32768) when strictly inside the grid, else exactly 1.0. amin tracks the smallest
-// L-inf distance of any sample to the grid boundary: a sample within the position bound of a face
-// may be classified differently from the FP64 reference, so its candidate is re-scored exactly.
+// One coarse sample at grid coordinates g: the quantised trilinear value when
+// strictly inside the grid, else exactly 0 (the dummy cell). amin tracks the smallest L-inf
+// distance of any sample to the grid boundary: a sample within the position bound of a face may be
+// classified differently from the FP64 reference, so its candidate is re-scored exactly.
 __device__ __forceinline__ float coarse_sample(const CoarseGrid& cg, float gx, float gy, float gz,
                                                float& amin) {
   const float e = fmaxf(fabsf(gx - cg.hx) - cg.hx, fmaxf(fabsf(gy - cg.hy) - cg.hy, fabsf(gz - cg.hz) - cg.hz));
   amin = fminf(amin, fabsf(e));
-  const bool inside = e < 0.0f;
   const float rx = __fadd_rz(gx, kMagic), ry = __fadd_rz(gy, kMagic), rz = __fadd_rz(gz, kMagic);
   const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic), fz = gz - (rz - kMagic);
   const uint32_t cell = __float_as_uint(rx) + __float_as_uint(ry) * cg.cx + __float_as_uint(rz) * cg.cxy - cg.koff;
-  const uint4 w = cg.cells[inside ? cell : 0u];
-  const float v = cell_lerp(w, fx, fy, fz);
-  return inside ? v : 1.0f;
+  return cell_lerp(cg.cells[e < 0.0f ? cell : cg.dummy], fx, fy, fz);
 }
 
 // coarse_sample that also tracks the smallest signed box distance (emin > ptol: clearly outside).
@@ -110,18 +111,15 @@ __device__ __forceinline__ float coarse_sample_e(const CoarseGrid& cg, float gx,
 }
 
 // coarse_sample for the separable alignment: the z coordinate's box term ez, fraction fz and cell
-// plane offset zoff (already carrying -koff) are shared by the 16 alpha rotations of a frame.
+// plane offset zoff (already carrying -koff) are shared by the alpha rotations of a frame.
 __device__ __forceinline__ float coarse_sample_z(const CoarseGrid& cg, float gx, float gy, float ez, float fz,
                                                  uint32_t zoff, float& amin) {
   const float e = fmaxf(fmaxf(fabsf(gx - cg.hx) - cg.hx, fabsf(gy - cg.hy) - cg.hy), ez);
   amin = fminf(amin, fabsf(e));
-  const bool inside = e < 0.0f;
   const float rx = __fadd_rz(gx, kMagic), ry = __fadd_rz(gy, kMagic);
   const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic);
   const uint32_t cell = __float_as_uint(rx) + __float_as_uint(ry) * cg.cx + zoff;
-  const uint4 w = cg.cells[inside ? cell : 0u];
-  const float v = cell_lerp(w, fx, fy, fz);
-  return inside ? v : 1.0f;
+  return cell_lerp(cg.cells[e < 0.0f ? cell : cg.dummy], fx, fy, fz);
 }
 
 // Interval form of coarse_sample for rotations with a sample near a face: a sample within ptol of
@@ -134,7 +132,7 @@ __device__ __forceinline__ void coarse_sample_iv(const CoarseGrid& cg, float gx,
   float am = 0.f;
   const float v = coarse_sample(cg, fminf(fmaxf(gx, 0.f), 2.f * cg.hx - 1e-3f),
                                 fminf(fmaxf(gy, 0.f), 2.f * cg.hy - 1e-3f),
-                                fminf(fmaxf(gz, 0.f), 2.f * cg.hz - 1e-3f), am) - 1.0f;
+                                fminf(fmaxf(gz, 0.f), 2.f * cg.hz - 1e-3f), am);
   hi += v;
   if (e < -ptol) lo += v;
 }
@@ -333,9 +331,9 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
   uint4* sc = reinterpret_cast<uint4*>(smem_raw);
   const uint4* cells = SC ? sc : pk.cells;
-  float* slots = SC ? reinterpret_cast<float*>(sc + n_cells) : reinterpret_cast<float*>(smem_raw);
+  float* slots = SC ? reinterpret_cast<float*>(sc + n_cells + 1) : reinterpret_cast<float*>(smem_raw);
   if (SC) {
-    for (uint32_t i = threadIdx.x; i < n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
+    for (uint32_t i = threadIdx.x; i <= n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
     __syncthreads();
   }
   float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
@@ -345,7 +343,8 @@ __global__ void __launch_bounds__(NT, 1)
                       0.5f * float(pk.cell_dims[2]),
                       pk.cell_dims[0],
                       pk.cell_dims[0] * pk.cell_dims[1],
-                      0x4B000000u * (1u + pk.cell_dims[0] + pk.cell_dims[0] * pk.cell_dims[1])};
+                      0x4B000000u * (1u + pk.cell_dims[0] + pk.cell_dims[0] * pk.cell_dims[1]),
+                      n_cells};
   const uint32_t N = pr.n_restarts;
   const uint64_t total = uint64_t(b.n_lig) * N;
   for (;;) {
@@ -418,7 +417,9 @@ __global__ void __launch_bounds__(NT, 1)
     const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
     const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
     const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
-    const float eps = eps_s + 4e-6f;                              // coarse score error bound
+    // coarse score error bound: per-sample FP32 rounding of the biased lerps (<= 1.3e-6), the
+    // accumulation of n values in [0, 1] (<= n 2^-24 after the 1/n), the final scaling
+    const float eps = eps_s + 1.3e-6f + 6e-8f * float(n) + 2e-7f;
     const float inv_n_scale = pk.coarse_scale / float(n);
 
     // ------------------------------------------------ coarse alignment sweep (all G rotations)
@@ -469,7 +470,76 @@ __global__ void __launch_bounds__(NT, 1)
     auto amb_to_g = [&](uint32_t bit) -> uint32_t {
       return separable ? (bit & 15u) * n_frames + lane + 32u * (bit >> 4) : lane + 32u * bit;
     };
-    if (separable) {
+    if (SC && separable && pr.steps[0] % (4 * kQtGroups) == 0) {
+      // Quarter-turn symmetry: alpha_{c + q na/4} = alpha_c + q pi/2, so one 2D rotation
+      // (rx, ry) = Rz(alpha_c) (wx, wy) gives the four samples t + (rx, ry), t + (-ry, rx),
+      // t - (rx, ry), t + (ry, -rx): two FADDs per sample for x, y. kQtGroups consecutive c share
+      // one pass over the atoms (the frame transform and the z terms are per atom).
+      const uint32_t nq = pr.steps[0] / 4;
+      // byte offset of a cell from the three RZ-floor bit patterns: 16 bx + 16 cx by + zoff16
+      const uint32_t cx16 = cg.cx * 16u, cxy16 = cg.cxy * 16u;
+      const uint32_t base16 = uint32_t(__cvta_generic_to_shared(cg.cells)) - cg.koff * 16u;
+      const uint32_t dummy16 = uint32_t(__cvta_generic_to_shared(cg.cells + cg.dummy));
+      for (uint32_t f = lane, m = 0; f < n_frames; f += 32, ++m) {
+        const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < nq; c0 += kQtGroups) {
+          float acc[4 * kQtGroups], amn[4 * kQtGroups];
+          float2 cs[kQtGroups];
+#pragma unroll
+          for (int i = 0; i < 4 * kQtGroups; ++i) {
+            acc[i] = 0.f;
+            amn[i] = 1e30f;
+          }
+#pragma unroll
+          for (int gi = 0; gi < kQtGroups; ++gi) cs[gi] = pr.acs[(c0 + gi) & 15];
+#pragma unroll 1
+          for (uint32_t a = 0; a < npad; ++a) {
+            const float4 v = A[a];
+            const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
+            const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
+            const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
+            const float ez = fabsf(gz - cg.hz) - cg.hz;
+            const float rz = __fadd_rz(gz, kMagic);
+            const float fz = gz - (rz - kMagic);
+            const uint32_t zoff16 = __float_as_uint(rz) * cxy16 + base16;
+#pragma unroll
+            for (int gi = 0; gi < kQtGroups; ++gi) {
+              const float rx = fmaf(cs[gi].x, wx, -cs[gi].y * wy), ry = fmaf(cs[gi].y, wx, cs[gi].x * wy);
+              const float px[4] = {tx + rx, tx - ry, tx - rx, tx + ry};
+              const float py[4] = {ty + ry, ty + rx, ty - ry, ty - rx};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float gx = px[q], gy = py[q];
+                const float e = fmaxf(fmaxf(fabsf(gx - cg.hx) - cg.hx, fabsf(gy - cg.hy) - cg.hy), ez);
+                amn[4 * gi + q] = fminf(amn[4 * gi + q], fabsf(e));
+                const float rxf = __fadd_rz(gx, kMagic), ryf = __fadd_rz(gy, kMagic);
+                const float fx = gx - (rxf - kMagic), fy = gy - (ryf - kMagic);
+                const uint32_t addr = __float_as_uint(ryf) * cx16 + (__float_as_uint(rxf) * 16u + zoff16);
+                uint4 w;
+                asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                             : "r"(e < 0.0f ? addr : dummy16));
+                acc[4 * gi + q] += cell_lerp(w, fx, fy, fz);
+              }
+            }
+          }
+#pragma unroll
+          for (int gi = 0; gi < kQtGroups; ++gi)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t ia = c0 + gi + q * nq;
+              const float sc = acc[4 * gi + q] * inv_n_scale;
+              if (amn[4 * gi + q] <= ptol) {
+                amb_mask |= 1ull << (16 * m + ia);
+              } else {
+                insert(sc, ia * n_frames + f);
+                lkey = fmaxf(lkey, sc);
+              }
+            }
+        }
+      }
+    } else if (separable) {
       const uint32_t na = pr.steps[0];
       for (uint32_t f = lane, m = 0; f < n_frames; f += 32, ++m) {
         const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
@@ -506,7 +576,7 @@ __global__ void __launch_bounds__(NT, 1)
           for (int i = 0; i < kAlphaChunk; ++i) {
             const uint32_t ia = i0 + i;
             if (ia >= na) break;
-            const float sc = (acc[i] - float(npad)) * inv_n_scale;
+            const float sc = acc[i] * inv_n_scale;
             if (amn[i] <= ptol) {
               amb_mask |= 1ull << (16 * m + ia);
             } else {
@@ -536,7 +606,7 @@ __global__ void __launch_bounds__(NT, 1)
                                 fmaf(r1.x, v3.x, fmaf(r1.y, v3.y, fmaf(r1.z, v3.z, ty))),
                                 fmaf(r2.x, v3.x, fmaf(r2.y, v3.y, fmaf(r2.z, v3.z, tz))), amin);
         }
-        const float sc = ((acc0 - float(npad >> 1)) + (acc1 - float(npad >> 1))) * inv_n_scale;
+        const float sc = (acc0 + acc1) * inv_n_scale;
         if (amin <= ptol) {
           amb_mask |= (j < 64 ? 1ull << j : 0ull);
           if (j >= 64) lkey = 1e30f;  // cannot track: forces the exact fallback below
@@ -596,9 +666,9 @@ __global__ void __launch_bounds__(NT, 1)
   // reads them; a compile-time flag so the gather is an LDS.128, not a generic load)
   uint4* sc = reinterpret_cast<uint4*>(smem_raw);
   const uint4* cells = SC ? sc : pk.cells;
-  float* slots = SC ? reinterpret_cast<float*>(sc + n_cells) : reinterpret_cast<float*>(smem_raw);
+  float* slots = SC ? reinterpret_cast<float*>(sc + n_cells + 1) : reinterpret_cast<float*>(smem_raw);
   if (SC) {
-    for (uint32_t i = threadIdx.x; i < n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
+    for (uint32_t i = threadIdx.x; i <= n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
     __syncthreads();
   }
   float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
@@ -615,7 +685,8 @@ __global__ void __launch_bounds__(NT, 1)
                       0.5f * float(pk.cell_dims[2]),
                       pk.cell_dims[0],
                       pk.cell_dims[0] * pk.cell_dims[1],
-                      0x4B000000u * (1u + pk.cell_dims[0] + pk.cell_dims[0] * pk.cell_dims[1])};
+                      0x4B000000u * (1u + pk.cell_dims[0] + pk.cell_dims[0] * pk.cell_dims[1]),
+                      n_cells};
   const uint32_t N = pr.n_restarts;
   const uint64_t total = uint64_t(b.n_lig) * N;
   const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
@@ -807,7 +878,7 @@ __global__ void __launch_bounds__(NT, 1)
             A[pos[s]] = make_float4(gx, gy, gz, rho[s]);
             es[s] = sample_exact_ni(pk, own(P, s));
             float am = 1e30f;
-            cs[s] = coarse_sample(cg, gx, gy, gz, am) - 1.0f;
+            cs[s] = coarse_sample(cg, gx, gy, gz, am);
             samb[s] = am <= ptol;
           }
         }
@@ -1067,7 +1138,11 @@ __global__ void __launch_bounds__(NT, 1)
               const uint32_t k = pass == 0 ? lane + 1 : 33 + grp;
               const bool active = pass == 0 ? (k <= n_cand) : (grp < rem);
               // this lane's share of the survivors: bit positions congruent to sub modulo gs
-              const uint32_t mypat = (gs >= 32 ? 1u : FULL / ((1u << gs) - 1u)) << sub;
+              uint32_t mypat = 1u;
+#pragma unroll
+              for (uint32_t w = 1; w < 32; w <<= 1)
+                if (w >= gs) mypat |= mypat << w;
+              mypat <<= sub;
               float part = 0.f, amin = 1e30f, mmin = 1e30f, emin = 1e30f;
               if (active) {
                 const float2 cq = pass == 0 ? cq_p0 : cq_p1;
@@ -1085,7 +1160,7 @@ __global__ void __launch_bounds__(NT, 1)
                   const float gx = fmaf(m00, pm.x, fmaf(m01, pm.y, fmaf(m02, pm.z, tvx)));
                   const float gy = fmaf(m10, pm.x, fmaf(m11, pm.y, fmaf(m12, pm.z, tvy)));
                   const float gz = fmaf(m20, pm.x, fmaf(m21, pm.y, fmaf(m22, pm.z, tvz)));
-                  if (((mq - s0 - 1) & (gs - 1)) == sub) part += coarse_sample_e(cg, gx, gy, gz, amin, emin) - 1.0f;
+                  if (((mq - s0 - 1) & (gs - 1)) == sub) part += coarse_sample_e(cg, gx, gy, gz, amin, emin);
                   // surviving cross pairs (fixed side and atom_j unless bonded)
                   const uint32_t* sv = SURV + (mq - s0 - 1) * NS;
 #pragma unroll
@@ -1151,7 +1226,8 @@ __global__ void __launch_bounds__(NT, 1)
               // values), so two candidates' exact scores differ from their coarse difference by at
               // most the moved atoms' error: 2 * eps_rel with eps_rel = |M'| eps_sample / n.
               const uint32_t nm = e0 - s0 - 1;
-              const float eps_rel = float(nm) * (eps_s + 3e-7f) / float(n) + 2e-7f;
+              const float eps_rel =
+                  (float(nm) * (eps_s + 1.3e-6f) + 6e-8f * (float(nm) * float(nm) + float(n))) / float(n) + 2e-7f;
               // k = 0 in the same coarse terms: fixed part + the cached coarse values of M'
               float p0 = 0.f;
               bool samb0 = false;
@@ -1263,7 +1339,7 @@ struct SmemPlan {
 
 static SmemPlan plan_smem(const DevPocket& pk, size_t slot_bytes, int max_warps) {
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
-  const size_t cell_bytes = size_t(n_cells) * sizeof(uint4);
+  const size_t cell_bytes = size_t(n_cells + 1) * sizeof(uint4);  // + the dummy cell
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
