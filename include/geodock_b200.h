@@ -135,8 +135,10 @@ int gd_set_pocket(gd_ctx* ctx, const uint32_t dims[3], const double origin[3], d
 int gd_set_params(gd_ctx* ctx, const gd_params* params);
 int gd_set_mode(gd_ctx* ctx, int mode_and_flags);
 
-/* dock_ligand / run_screening for a whole batch: validate + pack on the host, H2D, kernels, D2H.
- * Synchronous. Results are written in library order. */
+/* dock_ligand / run_screening for a whole batch: validate + pack on the host, H2D, kernels, D2H,
+ * pipelined over chunks of the library (host packing of chunk c+1 overlaps the GPU work of chunk
+ * c; pinned staging and device arenas are kept by the context between calls). Synchronous.
+ * Results are written in library order. */
 int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out);
 
 /* Split form used by the benchmark: stage (validate + pack + H2D, resident), run (kernels only,
@@ -149,6 +151,9 @@ void gd_batch_free(gd_batch* batch);
 int gd_sync(gd_ctx* ctx);
 void* gd_stream(gd_ctx* ctx);           /* cudaStream_t of the context */
 int gd_last_stats(gd_ctx* ctx, gd_stats* out);
+/* Device time (ms) of the last gd_run's kernels: ms[0] K1a coarse alignment, ms[1] K1b exact
+ * refinement + dihedral sweep, ms[2] K2 finalize (CUDA events on the context stream). */
+int gd_last_kernel_ms(gd_ctx* ctx, float* ms, uint32_t n);
 
 /* Closed-form scoring-call count, count_score_calls (docking.cpp:44-50). */
 uint64_t gd_count_score_calls(const gd_params* params, uint64_t n_rotamers);

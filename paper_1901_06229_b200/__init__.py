@@ -138,6 +138,7 @@ def _load():
             "gd_sync": (C.c_int, [vp]),
             "gd_stream": (vp, [vp]),
             "gd_last_stats": (C.c_int, [vp, C.POINTER(_Stats)]),
+            "gd_last_kernel_ms": (C.c_int, [vp, C.POINTER(C.c_float), C.c_uint32]),
             "gd_count_score_calls": (C.c_uint64, [C.POINTER(_Params), C.c_uint64]),
             "gd_validate_ligand": (C.c_int, [C.POINTER(_Library), C.c_uint32, C.c_char_p, C.c_uint32]),
             "gd_moving_set": (C.c_int, [C.POINTER(_Library), C.c_uint32, C.c_uint32, _u32p, _u32p]),
@@ -526,6 +527,12 @@ class Context:
         s = _Stats()
         self._check(self._lib.gd_last_stats(self._h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in s._fields_ if k != "reserved"}
+
+    def kernel_ms(self) -> dict:
+        """Device time of the last gd_run's kernels (CUDA events on the context stream)."""
+        ms = (C.c_float * 3)()
+        self._check(self._lib.gd_last_kernel_ms(self._h, ms, 3))
+        return {"k1a_align": ms[0], "k1b_sweep": ms[1], "k2_finalize": ms[2]}
 
     def sync(self):
         self._check(self._lib.gd_sync(self._h))

@@ -60,6 +60,28 @@ struct gd_ctx {
   unsigned long long* d_stats = nullptr;
   int* d_error = nullptr;
   unsigned int* d_counter = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // gd_run: K1a | K1b | K2 boundaries
+
+  // executor staging slots (gd_dock_batch): grow-only pinned host buffers + device arena + stream
+  struct Slot {
+    void* h_in = nullptr;
+    size_t h_in_cap = 0;
+    void* h_out = nullptr;
+    size_t h_out_cap = 0;
+    void* d_arena = nullptr;
+    size_t d_cap = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+  } slot[2];
+};
+
+struct Layout {
+  uint32_t L = 0, A = 0, Rt = 0, max_n = 1;
+  size_t n_items = 0;
+  std::vector<uint32_t> mask_base, adj_base;
+  size_t o_meta, o_atoms, o_start, o_rots, o_dih0, o_masks, o_adj, o_dfs, o_rdfs, o_adjd, host_bytes;
+  size_t o_cand, o_ncand, o_rs_score, o_rs_ascore, o_rs_aidx, o_rs_stepk, o_rs_xyz, o_rs_dih;
+  size_t o_best, o_brs, o_fxyz, o_fdih, o_ctr, total;
 };
 
 struct gd_batch {
@@ -73,6 +95,7 @@ struct gd_batch {
   std::vector<uint32_t> atom_off, rot_off;
   uint32_t n_restarts = 0, reps = 0, S = 0;
   gd_params params{};
+  Layout layout;
 };
 
 namespace {
@@ -430,6 +453,11 @@ int gd_create(int device, gd_ctx** out) {
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_stats, sizeof(unsigned long long) * 16);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_error, sizeof(int) * 2);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_counter, sizeof(unsigned int) * 4);
+  for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaStreamCreateWithFlags(&ctx->slot[i].stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->slot[i].done, cudaEventDisableTiming);
+  }
   if (e != cudaSuccess) {
     static thread_local std::string msg;
     msg = std::string("gd_create: ") + cudaGetErrorString(e);
@@ -454,6 +482,15 @@ void gd_destroy(gd_ctx* ctx) {
   cudaFree(ctx->d_stats);
   cudaFree(ctx->d_error);
   cudaFree(ctx->d_counter);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& sl : ctx->slot) {
+    if (sl.h_in) cudaFreeHost(sl.h_in);
+    if (sl.h_out) cudaFreeHost(sl.h_out);
+    cudaFree(sl.d_arena);
+    if (sl.done) cudaEventDestroy(sl.done);
+    if (sl.stream) cudaStreamDestroy(sl.stream);
+  }
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -580,118 +617,118 @@ int gd_moving_set(const gd_library* lib, uint32_t l, uint32_t r, uint32_t* out, 
   return GD_OK;
 }
 
-int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
-  if (!ctx || !lib || !out) return GD_ERR_ARGUMENT;
-  *out = nullptr;
-  if (!ctx->have_pocket) return set_err(ctx, GD_ERR_NO_POCKET, "no pocket set");
-  if (!ctx->have_params) return set_err(ctx, GD_ERR_CUDA, "parameters not uploaded");
-  cudaSetDevice(ctx->device);
-  const uint32_t L = lib->n_ligands;
-  if (L > 0 && (!lib->atom_off || !lib->bond_off || !lib->rot_off || !lib->name_off || !lib->names)) {
-    return set_err(ctx, GD_ERR_ARGUMENT, "null library array");
-  }
-  const gd_params& P = ctx->params;
-  const uint32_t N = P.n_restarts, reps = P.num_repetitions, S = P.dihedral_steps;
+}  // extern "C"
 
-  // ---- validation (dock_ligand throws before any work, docking.cpp:239-240; run_screening
-  // validates per task, pipeline.cpp:233 — the first invalid ligand in library order is reported).
-  std::vector<uint32_t> bad(L, 0);
-  parallel_for(L, 256, [&](size_t l) {
-    const LigView v = view_of(lib, uint32_t(l));
-    bad[l] = (!validate(v).empty() || v.n > GD_MAX_ATOMS) ? 1u : 0u;
-  });
-  uint32_t any_rot = 0, max_n = 1;
-  for (uint32_t l = 0; l < L; ++l) {
-    if (bad[l]) {
-      const LigView v = view_of(lib, l);
-      const auto viol = validate(v);
-      if (!viol.empty()) return set_err(ctx, GD_ERR_INVALID_LIGAND, validation_message(v.name, viol));
-      return set_err(ctx, GD_ERR_UNSUPPORTED,
-                     "ligand '" + std::string(v.name) + "' has " + std::to_string(v.n) +
-                         " atoms; this build supports up to " + std::to_string(GD_MAX_ATOMS));
-    }
-    const LigView v = view_of(lib, l);
-    any_rot |= v.nr;
-    max_n = std::max(max_n, v.n);
-  }
-  // bump_check's clash-factor contract fires on the first dihedral candidate (scoring.cpp:48-50).
-  if (any_rot && reps && S && (!(P.clash_factor > 0.0) || P.clash_factor > 1.0)) {
-    return set_err(ctx, GD_ERR_CONTRACT, "clash_factor must lie in (0, 1]");
-  }
+namespace {
 
-  auto* b = new gd_batch();
-  b->ctx = ctx;
-  b->params = P;
-  b->n_restarts = N;
-  b->reps = reps;
-  b->S = S;
-  b->atom_off.assign(lib->atom_off, lib->atom_off + L + 1);
-  b->rot_off.assign(lib->rot_off, lib->rot_off + L + 1);
-  const uint32_t A = L ? lib->atom_off[L] : 0;
-  const uint32_t Rt = L ? lib->rot_off[L] : 0;
+// ------------------------------------------------------------------ batch layout / packing
+// One packed batch lives in one device arena: [0, host_bytes) is packed on the host and uploaded,
+// the rest is per-restart scratch and per-ligand results.
 
-  // ---- host-side packing sizes
-  std::vector<uint32_t> mask_base(L + 1, 0), adj_base(L + 1, 0);
+Layout plan_layout(const gd_library* lib, const gd_params& P) {
+  Layout y;
+  const uint32_t L = lib->n_ligands, N = P.n_restarts, reps = P.num_repetitions;
+  y.L = L;
+  y.A = L ? lib->atom_off[L] - lib->atom_off[0] : 0;
+  y.Rt = L ? lib->rot_off[L] - lib->rot_off[0] : 0;
+  y.mask_base.assign(L + 1, 0);
+  y.adj_base.assign(L + 1, 0);
   for (uint32_t l = 0; l < L; ++l) {
     const uint32_t n = lib->atom_off[l + 1] - lib->atom_off[l];
     const uint32_t W = (n + 31) / 32;
-    mask_base[l + 1] = mask_base[l] + (lib->rot_off[l + 1] - lib->rot_off[l]) * W;
-    adj_base[l + 1] = adj_base[l] + n * W;
+    y.max_n = std::max(y.max_n, n);
+    y.mask_base[l + 1] = y.mask_base[l] + (lib->rot_off[l + 1] - lib->rot_off[l]) * W;
+    y.adj_base[l + 1] = y.adj_base[l] + n * W;
   }
-  const size_t n_items = size_t(L) * N;
+  y.n_items = size_t(L) * N;
   Arena ar;
-  const size_t o_meta = ar.take<LigMeta>(L);
-  const size_t o_atoms = ar.take<double4>(A);
-  const size_t o_start = ar.take<double4>(2 * n_items);
-  const size_t o_rots = ar.take<uint2>(Rt);
-  const size_t o_dih0 = ar.take<double>(Rt);
-  const size_t o_masks = ar.take<uint32_t>(mask_base[L]);
-  const size_t o_adj = ar.take<uint32_t>(adj_base[L]);
-  const size_t o_dfs = ar.take<uint16_t>(A);
-  const size_t o_rdfs = ar.take<ushort4>(Rt);
-  const size_t o_adjd = ar.take<uint32_t>(adj_base[L]);
-  const size_t host_bytes = ar.off;  // everything above is uploaded
-  const size_t o_rs_cand = ar.take<uint16_t>(n_items * gdk::kAlignCand);
-  const size_t o_rs_ncand = ar.take<int32_t>(n_items);
-  const size_t o_rs_score = ar.take<double>(n_items);
-  const size_t o_rs_ascore = ar.take<double>(n_items);
-  const size_t o_rs_aidx = ar.take<uint32_t>(n_items);
-  const size_t o_rs_stepk = ar.take<int32_t>(size_t(Rt) * N * reps);
-  const size_t o_rs_xyz = ar.take<double>(size_t(A) * N * 3);
-  const size_t o_rs_dih = ar.take<double>(size_t(Rt) * N);
-  const size_t o_best = ar.take<double>(L);
-  const size_t o_brs = ar.take<uint32_t>(L);
-  const size_t o_fxyz = ar.take<double>(size_t(A) * 3);
-  const size_t o_fdih = ar.take<double>(Rt);
-  b->arena_bytes = ar.off + 256;
+  y.o_meta = ar.take<LigMeta>(L);
+  y.o_atoms = ar.take<double4>(y.A);
+  y.o_start = ar.take<double4>(2 * y.n_items);
+  y.o_rots = ar.take<uint2>(y.Rt);
+  y.o_dih0 = ar.take<double>(y.Rt);
+  y.o_masks = ar.take<uint32_t>(y.mask_base[L]);
+  y.o_adj = ar.take<uint32_t>(y.adj_base[L]);
+  y.o_dfs = ar.take<uint16_t>(y.A);
+  y.o_rdfs = ar.take<ushort4>(y.Rt);
+  y.o_adjd = ar.take<uint32_t>(y.adj_base[L]);
+  y.host_bytes = ar.off;
+  y.o_cand = ar.take<uint16_t>(y.n_items * gdk::kAlignCand);
+  y.o_ncand = ar.take<int32_t>(y.n_items);
+  y.o_rs_score = ar.take<double>(y.n_items);
+  y.o_rs_ascore = ar.take<double>(y.n_items);
+  y.o_rs_aidx = ar.take<uint32_t>(y.n_items);
+  y.o_rs_stepk = ar.take<int32_t>(size_t(y.Rt) * N * reps);
+  y.o_rs_xyz = ar.take<double>(size_t(y.A) * N * 3);
+  y.o_rs_dih = ar.take<double>(size_t(y.Rt) * N);
+  y.o_best = ar.take<double>(L);
+  y.o_brs = ar.take<uint32_t>(L);
+  y.o_fxyz = ar.take<double>(size_t(y.A) * 3);
+  y.o_fdih = ar.take<double>(y.Rt);
+  y.o_ctr = ar.take<unsigned int>(4);
+  y.total = ar.off + 256;
+  return y;
+}
 
-  std::vector<unsigned char> host(host_bytes + 256);
-  unsigned char* H = host.data();
-  auto* meta = reinterpret_cast<LigMeta*>(H + o_meta);
-  auto* atoms = reinterpret_cast<double4*>(H + o_atoms);
-  auto* start = reinterpret_cast<double4*>(H + o_start);
-  auto* rots = reinterpret_cast<uint2*>(H + o_rots);
-  auto* dih0 = reinterpret_cast<double*>(H + o_dih0);
-  auto* masks = reinterpret_cast<uint32_t*>(H + o_masks);
-  auto* adjm = reinterpret_cast<uint32_t*>(H + o_adj);
-  auto* dfs = reinterpret_cast<uint16_t*>(H + o_dfs);
-  auto* rdfs = reinterpret_cast<ushort4*>(H + o_rdfs);
-  auto* adjd = reinterpret_cast<uint32_t*>(H + o_adjd);
+// Validation of ligands [l0, l1) in library order (dock_ligand throws before any work,
+// docking.cpp:239-240; run_screening reports the first failing task, pipeline.cpp:233).
+int validate_range(gd_ctx* ctx, const gd_library* lib, uint32_t l0, uint32_t l1) {
+  std::vector<uint8_t> bad(l1 - l0, 0);
+  parallel_for(l1 - l0, 256, [&](size_t i) {
+    const LigView v = view_of(lib, uint32_t(l0 + i));
+    bad[i] = (!validate(v).empty() || v.n > GD_MAX_ATOMS) ? 1u : 0u;
+  });
+  for (uint32_t l = l0; l < l1; ++l) {
+    if (!bad[l - l0]) continue;
+    const LigView v = view_of(lib, l);
+    const auto viol = validate(v);
+    if (!viol.empty()) return set_err(ctx, GD_ERR_INVALID_LIGAND, validation_message(v.name, viol));
+    return set_err(ctx, GD_ERR_UNSUPPORTED, "ligand '" + std::string(v.name) + "' has " + std::to_string(v.n) +
+                                                " atoms; this build supports up to " + std::to_string(GD_MAX_ATOMS));
+  }
+  return GD_OK;
+}
+
+// bump_check's clash-factor contract fires on the first dihedral candidate (scoring.cpp:48-50).
+int check_contract(gd_ctx* ctx, const gd_library* lib) {
+  const gd_params& P = ctx->params;
+  const uint32_t L = lib->n_ligands;
+  const bool any_rot = L && lib->rot_off[L] != lib->rot_off[0];
+  if (any_rot && P.num_repetitions && P.dihedral_steps && (!(P.clash_factor > 0.0) || P.clash_factor > 1.0)) {
+    return set_err(ctx, GD_ERR_CONTRACT, "clash_factor must lie in (0, 1]");
+  }
+  return GD_OK;
+}
+
+// Host SoA packing of a (rebased, atom_off[0] == 0) library into H[0, host_bytes).
+void pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, unsigned char* H) {
+  const gd_params& P = ctx->params;
+  const uint32_t L = y.L, N = P.n_restarts;
+  auto* meta = reinterpret_cast<LigMeta*>(H + y.o_meta);
+  auto* atoms = reinterpret_cast<double4*>(H + y.o_atoms);
+  auto* start = reinterpret_cast<double4*>(H + y.o_start);
+  auto* rots = reinterpret_cast<uint2*>(H + y.o_rots);
+  auto* dih0 = reinterpret_cast<double*>(H + y.o_dih0);
+  auto* masks = reinterpret_cast<uint32_t*>(H + y.o_masks);
+  auto* adjm = reinterpret_cast<uint32_t*>(H + y.o_adj);
+  auto* dfs = reinterpret_cast<uint16_t*>(H + y.o_dfs);
+  auto* rdfs = reinterpret_cast<ushort4*>(H + y.o_rdfs);
+  auto* adjd = reinterpret_cast<uint32_t*>(H + y.o_adjd);
   const double lo[3] = {ctx->origin[0], ctx->origin[1], ctx->origin[2]};
   // Pocket::bounds_hi (scoring.hpp:32-36)
   const double hi[3] = {ctx->origin[0] + ctx->spacing * static_cast<double>(ctx->dims[0] - 1),
                         ctx->origin[1] + ctx->spacing * static_cast<double>(ctx->dims[1] - 1),
                         ctx->origin[2] + ctx->spacing * static_cast<double>(ctx->dims[2] - 1)};
-
+  const uint32_t a0 = L ? lib->atom_off[0] : 0, r0 = L ? lib->rot_off[0] : 0;
   parallel_for(L, 64, [&](size_t li) {
     const uint32_t l = uint32_t(li);
     const LigView v = view_of(lib, l);
     const uint32_t n = v.n, W = (n + 31) / 32;
     LigMeta m{};
-    m.atom_base = lib->atom_off[l];
-    m.rot_base = lib->rot_off[l];
-    m.mask_base = mask_base[l];
-    m.adj_base = adj_base[l];
+    m.atom_base = lib->atom_off[l] - a0;
+    m.rot_base = lib->rot_off[l] - r0;
+    m.mask_base = y.mask_base[l];
+    m.adj_base = y.adj_base[l];
     m.n = uint16_t(n);
     m.nr = uint16_t(v.nr);
     meta[l] = m;
@@ -713,7 +750,7 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
     for (uint32_t r = 0; r < v.nr; ++r) {
       const uint32_t i = v.rots[2 * r], j = v.rots[2 * r + 1];
       rots[m.rot_base + r] = make_uint2(i, j);
-      dih0[m.rot_base + r] = lib->dihedrals ? lib->dihedrals[m.rot_base + r] : 0.0;
+      dih0[m.rot_base + r] = lib->dihedrals ? lib->dihedrals[lib->rot_off[l] + r] : 0.0;
       reachable(adj, n, j, i, j, seen, stack);
       uint32_t* mk = masks + m.mask_base + r * W;
       std::fill(mk, mk + W, 0u);
@@ -795,82 +832,64 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
     }
   });
 
-  cudaError_t e = cudaMalloc(&b->arena, b->arena_bytes);
-  if (e != cudaSuccess) {
-    delete b;
-    return cuda_err(ctx, e, "cudaMalloc(batch)");
-  }
-  auto* D = static_cast<unsigned char*>(b->arena);
-  e = cudaMemcpyAsync(D, H, host_bytes, cudaMemcpyHostToDevice, ctx->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  if (e != cudaSuccess) {
-    cudaFree(b->arena);
-    delete b;
-    return cuda_err(ctx, e, "upload batch");
-  }
-  ctx->last.h2d_bytes = host_bytes;
-  DevBatch& d = b->dev;
-  d.n_lig = L;
-  d.n_atoms = A;
-  d.n_rots = Rt;
-  d.max_n = max_n;
-  d.meta = reinterpret_cast<const LigMeta*>(D + o_meta);
-  d.atoms = reinterpret_cast<const double4*>(D + o_atoms);
-  d.start = reinterpret_cast<const double4*>(D + o_start);
-  d.rots = reinterpret_cast<const uint2*>(D + o_rots);
-  d.dih0 = reinterpret_cast<const double*>(D + o_dih0);
-  d.masks = reinterpret_cast<const uint32_t*>(D + o_masks);
-  d.adj = reinterpret_cast<const uint32_t*>(D + o_adj);
-  d.dfs_pos = reinterpret_cast<const uint16_t*>(D + o_dfs);
-  d.rdfs = reinterpret_cast<const ushort4*>(D + o_rdfs);
-  d.adjd = reinterpret_cast<const uint32_t*>(D + o_adjd);
-  d.rs_cand = reinterpret_cast<uint16_t*>(D + o_rs_cand);
-  d.rs_ncand = reinterpret_cast<int32_t*>(D + o_rs_ncand);
-  d.rs_score = reinterpret_cast<double*>(D + o_rs_score);
-  d.rs_align_score = reinterpret_cast<double*>(D + o_rs_ascore);
-  d.rs_align_index = reinterpret_cast<uint32_t*>(D + o_rs_aidx);
-  d.rs_step_k = reinterpret_cast<int32_t*>(D + o_rs_stepk);
-  d.rs_xyz = reinterpret_cast<double*>(D + o_rs_xyz);
-  d.rs_dih = reinterpret_cast<double*>(D + o_rs_dih);
-  d.best_score = reinterpret_cast<double*>(D + o_best);
-  d.best_restart = reinterpret_cast<uint32_t*>(D + o_brs);
-  d.final_xyz = reinterpret_cast<double*>(D + o_fxyz);
-  d.final_dih = reinterpret_cast<double*>(D + o_fdih);
-  d.work_counter = ctx->d_counter;
+}
+
+// Device view of a packed batch in arena D (ctx-level stats / error flag, per-batch counters).
+DevBatch bind_batch(const gd_ctx* ctx, const Layout& y, unsigned char* D) {
+  DevBatch d{};
+  d.n_lig = y.L;
+  d.n_atoms = y.A;
+  d.n_rots = y.Rt;
+  d.max_n = y.max_n;
+  d.meta = reinterpret_cast<const LigMeta*>(D + y.o_meta);
+  d.atoms = reinterpret_cast<const double4*>(D + y.o_atoms);
+  d.start = reinterpret_cast<const double4*>(D + y.o_start);
+  d.rots = reinterpret_cast<const uint2*>(D + y.o_rots);
+  d.dih0 = reinterpret_cast<const double*>(D + y.o_dih0);
+  d.masks = reinterpret_cast<const uint32_t*>(D + y.o_masks);
+  d.adj = reinterpret_cast<const uint32_t*>(D + y.o_adj);
+  d.dfs_pos = reinterpret_cast<const uint16_t*>(D + y.o_dfs);
+  d.rdfs = reinterpret_cast<const ushort4*>(D + y.o_rdfs);
+  d.adjd = reinterpret_cast<const uint32_t*>(D + y.o_adjd);
+  d.rs_cand = reinterpret_cast<uint16_t*>(D + y.o_cand);
+  d.rs_ncand = reinterpret_cast<int32_t*>(D + y.o_ncand);
+  d.rs_score = reinterpret_cast<double*>(D + y.o_rs_score);
+  d.rs_align_score = reinterpret_cast<double*>(D + y.o_rs_ascore);
+  d.rs_align_index = reinterpret_cast<uint32_t*>(D + y.o_rs_aidx);
+  d.rs_step_k = reinterpret_cast<int32_t*>(D + y.o_rs_stepk);
+  d.rs_xyz = reinterpret_cast<double*>(D + y.o_rs_xyz);
+  d.rs_dih = reinterpret_cast<double*>(D + y.o_rs_dih);
+  d.best_score = reinterpret_cast<double*>(D + y.o_best);
+  d.best_restart = reinterpret_cast<uint32_t*>(D + y.o_brs);
+  d.final_xyz = reinterpret_cast<double*>(D + y.o_fxyz);
+  d.final_dih = reinterpret_cast<double*>(D + y.o_fdih);
+  d.work_counter = reinterpret_cast<unsigned int*>(D + y.o_ctr);
   d.error = ctx->d_error;
   d.stats = ctx->d_stats;
-  *out = b;
+  return d;
+}
+
+int reset_device_status(gd_ctx* ctx, cudaStream_t s) {
+  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_error, 0, 2 * sizeof(int), s));
+  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, 16 * sizeof(unsigned long long), s));
   return GD_OK;
 }
 
-int gd_run(gd_batch* b) {
-  if (!b) return GD_ERR_ARGUMENT;
-  gd_ctx* ctx = b->ctx;
-  cudaSetDevice(ctx->device);
-  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_error, 0, 2 * sizeof(int), ctx->stream));
-  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, 16 * sizeof(unsigned long long), ctx->stream));
+int launch_batch(gd_ctx* ctx, const DevBatch& d, cudaStream_t s, cudaEvent_t* ev) {
   int launches = 0;
   DevParams pr = dev_params(ctx);
   if (!(ctx->q_eps < 1.0f)) pr.mode = (pr.mode & ~0xff) | GD_MODE_EXACT;
-  const cudaError_t e = gdk::launch_dock(dev_pocket(ctx), pr, b->dev, ctx->n_sms, ctx->stream, &launches);
+  const cudaError_t e = gdk::launch_dock(dev_pocket(ctx), pr, d, ctx->n_sms, s, &launches, ev);
   ctx->last.launches = uint32_t(launches);
   if (e != cudaSuccess) return cuda_err(ctx, e, "launch_dock");
   return GD_OK;
 }
 
-int gd_sync(gd_ctx* ctx) {
-  if (!ctx) return GD_ERR_ARGUMENT;
-  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  return GD_OK;
-}
-
-static int check_device_error(gd_batch* b) {
-  gd_ctx* ctx = b->ctx;
+int read_device_status(gd_ctx* ctx) {
   int err[2] = {0, 0};
   unsigned long long st[8];
-  GD_CUDA(ctx, cudaMemcpyAsync(err, ctx->d_error, sizeof err, cudaMemcpyDeviceToHost, ctx->stream));
-  GD_CUDA(ctx, cudaMemcpyAsync(st, ctx->d_stats, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
-  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  GD_CUDA(ctx, cudaMemcpy(err, ctx->d_error, sizeof err, cudaMemcpyDeviceToHost));
+  GD_CUDA(ctx, cudaMemcpy(st, ctx->d_stats, sizeof st, cudaMemcpyDeviceToHost));
   ctx->last.restarts = st[0];
   ctx->last.align_exact_evals = st[1];
   ctx->last.align_fallbacks = st[2];
@@ -885,56 +904,186 @@ static int check_device_error(gd_batch* b) {
   return GD_OK;
 }
 
-int gd_fetch(gd_batch* b, gd_results* out) {
-  if (!b || !out || !out->best_score || !out->best_restart) return GD_ERR_ARGUMENT;
-  gd_ctx* ctx = b->ctx;
-  cudaSetDevice(ctx->device);
-  int rc = check_device_error(b);
-  if (rc != GD_OK) return rc;
-  const DevBatch& d = b->dev;
-  const uint32_t L = d.n_lig, N = b->n_restarts;
-  const cudaStream_t s = ctx->stream;
-  GD_CUDA(ctx, cudaMemcpyAsync(out->best_score, d.best_score, L * sizeof(double), cudaMemcpyDeviceToHost, s));
-  GD_CUDA(ctx, cudaMemcpyAsync(out->best_restart, d.best_restart, L * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  if (out->final_xyz)
-    GD_CUDA(ctx, cudaMemcpyAsync(out->final_xyz, d.final_xyz, size_t(d.n_atoms) * 3 * sizeof(double),
-                                 cudaMemcpyDeviceToHost, s));
-  if (out->final_dihedrals)
-    GD_CUDA(ctx, cudaMemcpyAsync(out->final_dihedrals, d.final_dih, size_t(d.n_rots) * sizeof(double),
-                                 cudaMemcpyDeviceToHost, s));
-  if (out->align_index)
-    GD_CUDA(ctx, cudaMemcpyAsync(out->align_index, d.rs_align_index, size_t(L) * N * sizeof(uint32_t),
-                                 cudaMemcpyDeviceToHost, s));
-  if (out->align_score)
-    GD_CUDA(ctx, cudaMemcpyAsync(out->align_score, d.rs_align_score, size_t(L) * N * sizeof(double),
-                                 cudaMemcpyDeviceToHost, s));
-  if (out->restart_score)
-    GD_CUDA(ctx, cudaMemcpyAsync(out->restart_score, d.rs_score, size_t(L) * N * sizeof(double),
-                                 cudaMemcpyDeviceToHost, s));
-  if (out->step_k)
-    GD_CUDA(ctx, cudaMemcpyAsync(out->step_k, d.rs_step_k, size_t(d.n_rots) * N * b->reps * sizeof(int32_t),
-                                 cudaMemcpyDeviceToHost, s));
-  GD_CUDA(ctx, cudaStreamSynchronize(s));
-  ctx->last.d2h_bytes = L * (sizeof(double) + sizeof(uint32_t)) +
-                        (out->final_xyz ? size_t(d.n_atoms) * 3 * sizeof(double) : 0) +
-                        (out->final_dihedrals ? size_t(d.n_rots) * sizeof(double) : 0) +
-                        (out->align_index ? size_t(L) * N * sizeof(uint32_t) : 0) +
-                        (out->align_score ? size_t(L) * N * sizeof(double) : 0) +
-                        (out->restart_score ? size_t(L) * N * sizeof(double) : 0) +
-                        (out->step_k ? size_t(d.n_rots) * N * b->reps * sizeof(int32_t) : 0);
-  // score_calls / nominal phase times are the closed form (docking.cpp:44-50, 226-229): the
-  // reference's recorded counters equal it by construction (docking_test.cpp:304-320).
-  const uint64_t G = uint64_t(b->params.rotation_steps[0]) * b->params.rotation_steps[1] * b->params.rotation_steps[2];
-  for (uint32_t l = 0; l < L; ++l) {
-    const uint64_t R = b->rot_off[l + 1] - b->rot_off[l];
-    const uint64_t align_calls = uint64_t(N) * G;
-    const uint64_t opt_calls = uint64_t(N) * b->reps * R * b->S;
+// score_calls / nominal phase times are the closed form (docking.cpp:44-50, 226-229): the
+// reference's recorded counters equal it by construction (docking_test.cpp:304-320).
+void closed_form_counts(const gd_params& P, const gd_library* lib, uint32_t l0, uint32_t l1, gd_results* out) {
+  const uint64_t G = uint64_t(P.rotation_steps[0]) * P.rotation_steps[1] * P.rotation_steps[2];
+  for (uint32_t l = l0; l < l1; ++l) {
+    const uint64_t R = lib->rot_off[l + 1] - lib->rot_off[l];
+    const uint64_t align_calls = uint64_t(P.n_restarts) * G;
+    const uint64_t opt_calls = uint64_t(P.n_restarts) * P.num_repetitions * R * P.dihedral_steps;
     if (out->score_calls) out->score_calls[l] = align_calls + opt_calls;
     if (out->phase_times) {
       out->phase_times[2 * l] = static_cast<double>(align_calls) * 1e-7;  // kNominalSecondsPerScoreCall
       out->phase_times[2 * l + 1] = static_cast<double>(opt_calls) * 1e-7;
     }
   }
+}
+
+// Result regions of a batch: (device offset, bytes, destination in out at ligand/atom/rotamer
+// offsets of the chunk). Trace arrays only when requested.
+struct OutCopy {
+  size_t dev_off, bytes;
+  void* dst;
+};
+
+std::vector<OutCopy> result_copies(const Layout& y, const gd_params& P, const gd_library* full, uint32_t l0,
+                                   gd_results* out) {
+  std::vector<OutCopy> v;
+  const size_t a0 = full->atom_off[l0], r0 = full->rot_off[l0], N = P.n_restarts;
+  v.push_back({y.o_best, y.L * sizeof(double), out->best_score + l0});
+  v.push_back({y.o_brs, y.L * sizeof(uint32_t), out->best_restart + l0});
+  if (out->final_xyz) v.push_back({y.o_fxyz, size_t(y.A) * 3 * sizeof(double), out->final_xyz + 3 * a0});
+  if (out->final_dihedrals) v.push_back({y.o_fdih, size_t(y.Rt) * sizeof(double), out->final_dihedrals + r0});
+  if (out->align_index) v.push_back({y.o_rs_aidx, y.n_items * sizeof(uint32_t), out->align_index + size_t(l0) * N});
+  if (out->align_score) v.push_back({y.o_rs_ascore, y.n_items * sizeof(double), out->align_score + size_t(l0) * N});
+  if (out->restart_score) v.push_back({y.o_rs_score, y.n_items * sizeof(double), out->restart_score + size_t(l0) * N});
+  if (out->step_k)
+    v.push_back({y.o_rs_stepk, size_t(y.Rt) * N * P.num_repetitions * sizeof(int32_t),
+                 out->step_k + r0 * N * P.num_repetitions});
+  return v;
+}
+
+// A library view of ligands [l0, l1) with offsets rebased to 0.
+struct SubLib {
+  gd_library v{};
+  std::vector<uint32_t> ao, bo, ro, no;
+};
+
+void sub_library(const gd_library* lib, uint32_t l0, uint32_t l1, SubLib& s) {
+  const uint32_t L = l1 - l0;
+  auto rebase = [&](const uint32_t* off, std::vector<uint32_t>& o) {
+    o.resize(L + 1);
+    for (uint32_t i = 0; i <= L; ++i) o[i] = off[l0 + i] - off[l0];
+  };
+  rebase(lib->atom_off, s.ao);
+  rebase(lib->bond_off, s.bo);
+  rebase(lib->rot_off, s.ro);
+  rebase(lib->name_off, s.no);
+  s.v.n_ligands = L;
+  s.v.atom_off = s.ao.data();
+  s.v.xyz = lib->xyz + 3 * size_t(lib->atom_off[l0]);
+  s.v.radius = lib->radius + lib->atom_off[l0];
+  s.v.bond_off = s.bo.data();
+  s.v.bonds = lib->bonds + 2 * size_t(lib->bond_off[l0]);
+  s.v.rot_off = s.ro.data();
+  s.v.rots = lib->rots + 2 * size_t(lib->rot_off[l0]);
+  s.v.dihedrals = lib->dihedrals ? lib->dihedrals + lib->rot_off[l0] : nullptr;
+  s.v.name_off = s.no.data();
+  s.v.names = lib->names + lib->name_off[l0];
+}
+
+// Grow-only pinned / device buffers owned by the context (the executor's staging slots).
+int ensure_pinned(gd_ctx* ctx, void*& p, size_t& cap, size_t need) {
+  if (cap >= need) return GD_OK;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  cap = 0;
+  GD_CUDA(ctx, cudaMallocHost(&p, need));
+  cap = need;
+  return GD_OK;
+}
+
+int ensure_device(gd_ctx* ctx, void*& p, size_t& cap, size_t need) {
+  if (cap >= need) return GD_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  GD_CUDA(ctx, cudaMalloc(&p, need));
+  cap = need;
+  return GD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
+  if (!ctx || !lib || !out) return GD_ERR_ARGUMENT;
+  *out = nullptr;
+  if (!ctx->have_pocket) return set_err(ctx, GD_ERR_NO_POCKET, "no pocket set");
+  if (!ctx->have_params) return set_err(ctx, GD_ERR_CUDA, "parameters not uploaded");
+  cudaSetDevice(ctx->device);
+  const uint32_t L = lib->n_ligands;
+  if (L > 0 && (!lib->atom_off || !lib->bond_off || !lib->rot_off || !lib->name_off || !lib->names)) {
+    return set_err(ctx, GD_ERR_ARGUMENT, "null library array");
+  }
+  int rc = validate_range(ctx, lib, 0, L);
+  if (rc == GD_OK) rc = check_contract(ctx, lib);
+  if (rc != GD_OK) return rc;
+  SubLib sl;
+  sub_library(lib, 0, L, sl);
+  auto* b = new gd_batch();
+  b->ctx = ctx;
+  b->params = ctx->params;
+  b->n_restarts = ctx->params.n_restarts;
+  b->reps = ctx->params.num_repetitions;
+  b->S = ctx->params.dihedral_steps;
+  b->atom_off.assign(lib->atom_off, lib->atom_off + L + 1);
+  b->rot_off.assign(lib->rot_off, lib->rot_off + L + 1);
+  b->layout = plan_layout(&sl.v, ctx->params);
+  const Layout& y = b->layout;
+  b->arena_bytes = y.total;
+  std::vector<unsigned char> host(y.host_bytes + 256);
+  pack_library(ctx, &sl.v, y, host.data());
+  cudaError_t e = cudaMalloc(&b->arena, b->arena_bytes);
+  if (e != cudaSuccess) {
+    delete b;
+    return cuda_err(ctx, e, "cudaMalloc(batch)");
+  }
+  e = cudaMemcpyAsync(b->arena, host.data(), y.host_bytes, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    cudaFree(b->arena);
+    delete b;
+    return cuda_err(ctx, e, "upload batch");
+  }
+  ctx->last.h2d_bytes = y.host_bytes;
+  b->dev = bind_batch(ctx, y, static_cast<unsigned char*>(b->arena));
+  *out = b;
+  return GD_OK;
+}
+
+int gd_run(gd_batch* b) {
+  if (!b) return GD_ERR_ARGUMENT;
+  gd_ctx* ctx = b->ctx;
+  cudaSetDevice(ctx->device);
+  int rc = reset_device_status(ctx, ctx->stream);
+  if (rc != GD_OK) return rc;
+  return launch_batch(ctx, b->dev, ctx->stream, ctx->ev);
+}
+
+int gd_last_kernel_ms(gd_ctx* ctx, float* ms, uint32_t n) {
+  if (!ctx || !ms) return GD_ERR_ARGUMENT;
+  GD_CUDA(ctx, cudaEventSynchronize(ctx->ev[3]));
+  for (uint32_t i = 0; i < n && i < 3; ++i) GD_CUDA(ctx, cudaEventElapsedTime(ms + i, ctx->ev[i], ctx->ev[i + 1]));
+  return GD_OK;
+}
+
+int gd_sync(gd_ctx* ctx) {
+  if (!ctx) return GD_ERR_ARGUMENT;
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GD_OK;
+}
+
+int gd_fetch(gd_batch* b, gd_results* out) {
+  if (!b || !out || !out->best_score || !out->best_restart) return GD_ERR_ARGUMENT;
+  gd_ctx* ctx = b->ctx;
+  cudaSetDevice(ctx->device);
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  int rc = read_device_status(ctx);
+  if (rc != GD_OK) return rc;
+  const Layout& y = b->layout;
+  gd_library shim{};
+  shim.atom_off = b->atom_off.data();
+  shim.rot_off = b->rot_off.data();
+  size_t d2h = 0;
+  for (const OutCopy& c : result_copies(y, b->params, &shim, 0, out)) {
+    GD_CUDA(ctx, cudaMemcpy(c.dst, static_cast<unsigned char*>(b->arena) + c.dev_off, c.bytes, cudaMemcpyDeviceToHost));
+    d2h += c.bytes;
+  }
+  ctx->last.d2h_bytes = d2h;
+  closed_form_counts(b->params, &shim, 0, y.L, out);
   return GD_OK;
 }
 
@@ -994,14 +1143,100 @@ int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
   return GD_OK;
 }
 
+// The executor (run_screening, pipeline.cpp:187-290, re-designed for one GPU): the library is
+// cut into chunks; two staging slots (pinned host input/output + device arena, one stream each)
+// alternate, so the host packs chunk c+1 while the GPU runs chunk c, the H2D of c+1 overlaps the
+// kernels of c, and the next chunk's persistent kernels fill the SMs the previous chunk's tail
+// frees. Results are written in library order; an invalid ligand is reported before any of its
+// chunk's work (earlier chunks' results are discarded with the error, as the reference's rethrow
+// after join discards them, pipeline.cpp:262-272).
 int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
-  if (!ctx || !lib || !out) return GD_ERR_ARGUMENT;
-  gd_batch* b = nullptr;
-  int rc = gd_stage(ctx, lib, &b);
+  if (!ctx || !lib || !out || !out->best_score || !out->best_restart) return GD_ERR_ARGUMENT;
+  if (!ctx->have_pocket) return set_err(ctx, GD_ERR_NO_POCKET, "no pocket set");
+  if (!ctx->have_params) return set_err(ctx, GD_ERR_CUDA, "parameters not uploaded");
+  cudaSetDevice(ctx->device);
+  const uint32_t L = lib->n_ligands;
+  if (L > 0 && (!lib->atom_off || !lib->bond_off || !lib->rot_off || !lib->name_off || !lib->names)) {
+    return set_err(ctx, GD_ERR_ARGUMENT, "null library array");
+  }
+  int rc = check_contract(ctx, lib);
   if (rc != GD_OK) return rc;
-  rc = gd_run(b);
-  if (rc == GD_OK) rc = gd_fetch(b, out);
-  gd_batch_free(b);
+  const gd_params P = ctx->params;
+  // chunk size: ~8 chunks for large libraries, at least 256 ligands, at most kMaxChunk
+  constexpr uint32_t kMaxChunk = 4096;
+  const uint32_t chunk = std::min<uint32_t>(kMaxChunk, std::max<uint32_t>(256, (L + 7) / 8));
+  const uint32_t n_chunks = L ? (L + chunk - 1) / chunk : 0;
+  rc = reset_device_status(ctx, ctx->stream);
+  if (rc != GD_OK) return rc;
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  struct Pending {
+    bool busy = false;
+    uint32_t l0 = 0, l1 = 0;
+    Layout y;
+    std::vector<OutCopy> copies;
+  } pend[2];
+  size_t h2d = 0, d2h = 0;
+  auto drain = [&](int si) -> int {
+    Pending& p = pend[si];
+    if (!p.busy) return GD_OK;
+    GD_CUDA(ctx, cudaEventSynchronize(ctx->slot[si].done));
+    // unpack: pinned output staging -> the caller's arrays (library order)
+    const unsigned char* src = static_cast<const unsigned char*>(ctx->slot[si].h_out);
+    size_t at = 0;
+    for (const OutCopy& c : p.copies) {
+      std::memcpy(c.dst, src + at, c.bytes);
+      at += (c.bytes + 255) & ~size_t(255);
+    }
+    closed_form_counts(P, lib, p.l0, p.l1, out);
+    p.busy = false;
+    return GD_OK;
+  };
+  for (uint32_t c = 0; c < n_chunks; ++c) {
+    const int si = int(c & 1);
+    auto& slot = ctx->slot[si];
+    rc = drain(si);
+    if (rc != GD_OK) return rc;
+    const uint32_t l0 = c * chunk, l1 = std::min(L, l0 + chunk);
+    rc = validate_range(ctx, lib, l0, l1);
+    if (rc != GD_OK) {
+      cudaDeviceSynchronize();
+      return rc;
+    }
+    SubLib sl;
+    sub_library(lib, l0, l1, sl);
+    Pending& p = pend[si];
+    p.l0 = l0;
+    p.l1 = l1;
+    p.y = plan_layout(&sl.v, P);
+    p.copies = result_copies(p.y, P, lib, l0, out);
+    size_t out_bytes = 0;
+    for (const OutCopy& oc : p.copies) out_bytes += (oc.bytes + 255) & ~size_t(255);
+    if ((rc = ensure_pinned(ctx, slot.h_in, slot.h_in_cap, p.y.host_bytes + 256)) != GD_OK) return rc;
+    if ((rc = ensure_pinned(ctx, slot.h_out, slot.h_out_cap, out_bytes + 256)) != GD_OK) return rc;
+    if ((rc = ensure_device(ctx, slot.d_arena, slot.d_cap, p.y.total)) != GD_OK) return rc;
+    pack_library(ctx, &sl.v, p.y, static_cast<unsigned char*>(slot.h_in));
+    unsigned char* D = static_cast<unsigned char*>(slot.d_arena);
+    GD_CUDA(ctx, cudaMemcpyAsync(D, slot.h_in, p.y.host_bytes, cudaMemcpyHostToDevice, slot.stream));
+    h2d += p.y.host_bytes;
+    rc = launch_batch(ctx, bind_batch(ctx, p.y, D), slot.stream, nullptr);
+    if (rc != GD_OK) return rc;
+    size_t at = 0;
+    for (const OutCopy& oc : p.copies) {
+      GD_CUDA(ctx, cudaMemcpyAsync(static_cast<unsigned char*>(slot.h_out) + at, D + oc.dev_off, oc.bytes,
+                                   cudaMemcpyDeviceToHost, slot.stream));
+      at += (oc.bytes + 255) & ~size_t(255);
+      d2h += oc.bytes;
+    }
+    GD_CUDA(ctx, cudaEventRecord(slot.done, slot.stream));
+    p.busy = true;
+  }
+  for (int si = 0; si < 2; ++si) {
+    rc = drain(si);
+    if (rc != GD_OK) return rc;
+  }
+  rc = read_device_status(ctx);
+  ctx->last.h2d_bytes = h2d;
+  ctx->last.d2h_bytes = d2h;
   return rc;
 }
 

@@ -1365,7 +1365,7 @@ static cudaError_t launch_persistent(K kernel, const SmemPlan& p, int n_sms, cud
 // K1a (coarse alignment, NTA threads) then K1b (exact refinement + dihedral sweep, NTB threads).
 template <int NS, int NTA, int NTB>
 static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, cudaEvent_t mid) {
   const uint32_t npad_max = (b.max_n + 3) & ~3u;
   const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
   const uint32_t slot_b = (4 + (NS > 2 ? NS : 2)) * npad_max;  // A + SURV/SCR (max(NS, 2) words per atom)
@@ -1374,16 +1374,17 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
                       ? launch_persistent(align_coarse_kernel<NS, NTA, true>, pa, n_sms, stream, pk, pr, b, slot_a)
                       : launch_persistent(align_coarse_kernel<NS, NTA, false>, pa, n_sms, stream, pk, pr, b, slot_a);
   if (e != cudaSuccess) return e;
+  if (mid && (e = cudaEventRecord(mid, stream)) != cudaSuccess) return e;
   const SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32);
   return pb.cells_in_smem ? launch_persistent(dock_fast_kernel<NS, NTB, true>, pb, n_sms, stream, pk, pr, b, slot_b)
                           : launch_persistent(dock_fast_kernel<NS, NTB, false>, pb, n_sms, stream, pk, pr, b, slot_b);
 }
 
 cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                        cudaStream_t stream) {
-  if (b.max_n <= 32) return launch_ns<1, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream);
-  if (b.max_n <= 64) return launch_ns<2, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream);
-  if (b.max_n <= 128) return launch_ns<4, GD_ALIGN_THREADS, GD_FAST_THREADS_NS4>(pk, pr, b, n_sms, stream);
+                        cudaStream_t stream, cudaEvent_t mid) {
+  if (b.max_n <= 32) return launch_ns<1, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream, mid);
+  if (b.max_n <= 64) return launch_ns<2, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream, mid);
+  if (b.max_n <= 128) return launch_ns<4, GD_ALIGN_THREADS, GD_FAST_THREADS_NS4>(pk, pr, b, n_sms, stream, mid);
   return cudaErrorNotSupported;  // launch_dock routes > 128 atoms to the exact kernel
 }
 

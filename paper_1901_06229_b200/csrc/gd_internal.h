@@ -31,15 +31,15 @@ static_assert(sizeof(LigMeta) == 32, "LigMeta layout");
 // Pocket as seen by the kernels.
 struct DevPocket {
   const double* field;   // FP64 x-fastest field (exact path)
-  const uint4* cells;    // 15-bit packed 8-corner cells (coarse path), (mx*my*mz) entries
+  const uint4* cells;    // coarse cells (four quantised x-edges each, gd_set_pocket), (mx*my*mz)+1 entries
   uint32_t dims[3];
   uint32_t cell_dims[3]; // dims - 1
   double origin[3];
   double spacing;
   double maxc[3];        // dims - 1 as doubles (sample_field's outside test, scoring.cpp:16-18)
   float inv_spacing_f;
-  float q_eps;           // quantisation bound of the 15-bit cells: 0.5/32767 (inf: fast path off)
-  float coarse_scale;    // 32768/32767: undoes the 15-bit encode scale
+  float q_eps;           // quantisation bound of one coarse sample (inf: fast path off)
+  float coarse_scale;    // scale of the decoded coarse values (1 with the current encoding)
   float max_step;        // max |v(i+1) - v(i)| along any axis: slope bound per grid unit
 };
 
@@ -99,8 +99,9 @@ struct DevBatch {
 };
 
 // Kernel launchers (gd_kernels.cu). Return cudaGetLastError() of the launches.
+// ev (nullable): 4 events recorded around K1a, K1b and K2 (per-kernel timing).
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                        cudaStream_t stream, int* launches);
+                        cudaStream_t stream, int* launches, cudaEvent_t* ev = nullptr);
 // Device top-k by (best_score desc, ligand asc) into out[0..k). Needs scratch from topk_scratch_bytes.
 size_t topk_scratch_bytes(uint32_t n_lig);
 cudaError_t launch_topk(const DevBatch& b, uint32_t k, void* scratch, size_t scratch_bytes,

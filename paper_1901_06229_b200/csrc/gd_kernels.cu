@@ -257,34 +257,43 @@ __global__ void finalize_kernel(DevParams pr, DevBatch b) {
 }
 
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                        cudaStream_t stream, int* launches) {
+                        cudaStream_t stream, int* launches, cudaEvent_t* ev) {
   *launches = 0;
   cudaError_t e = cudaMemsetAsync(b.work_counter, 0, 2 * sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
-  if (b.n_lig == 0) return cudaSuccess;
-  const int mode = pr.mode & 0xff;
-  if (mode == GD_MODE_EXACT || b.max_n > 128) {  // the fast kernel keeps <= 128 atoms in registers
-    const uint32_t stride = 7 * b.max_n;  // doubles per warp
-    const size_t per_warp = size_t(stride) * sizeof(double);
-    int warps = int((200 * 1024) / per_warp);
-    if (warps > 32) warps = 32;
-    if (warps < 1) warps = 1;
-    const size_t smem = per_warp * warps;
-    e = cudaFuncSetAttribute(dock_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (ev && (e = cudaEventRecord(ev[0], stream)) != cudaSuccess) return e;
+  if (b.n_lig > 0) {
+    const int mode = pr.mode & 0xff;
+    if (mode == GD_MODE_EXACT || b.max_n > 128) {  // the fast kernels keep <= 128 atoms in registers
+      const uint32_t stride = 7 * b.max_n;  // doubles per warp
+      const size_t per_warp = size_t(stride) * sizeof(double);
+      int warps = int((200 * 1024) / per_warp);
+      if (warps > 32) warps = 32;
+      if (warps < 1) warps = 1;
+      const size_t smem = per_warp * warps;
+      e = cudaFuncSetAttribute(dock_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      dock_exact_kernel<<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, stride);
+      ++*launches;
+      if (ev && (e = cudaEventRecord(ev[1], stream)) != cudaSuccess) return e;
+    } else {
+      e = launch_fast(pk, pr, b, n_sms, stream, ev ? ev[1] : nullptr);  // K1a + K1b
+      if (e != cudaSuccess) return e;
+      *launches += 2;
+    }
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    dock_exact_kernel<<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, stride);
-    ++*launches;
-  } else {
-    e = launch_fast(pk, pr, b, n_sms, stream);  // K1a + K1b
-    if (e != cudaSuccess) return e;
-    *launches += 2;
+  } else if (ev && (e = cudaEventRecord(ev[1], stream)) != cudaSuccess) {
+    return e;
   }
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  const uint32_t threads = 256;
-  const uint32_t blocks = (b.n_lig * 32 + threads - 1) / threads;
-  finalize_kernel<<<blocks, threads, 0, stream>>>(pr, b);
-  ++*launches;
+  if (ev && (e = cudaEventRecord(ev[2], stream)) != cudaSuccess) return e;
+  if (b.n_lig > 0) {
+    const uint32_t threads = 256;
+    const uint32_t blocks = (b.n_lig * 32 + threads - 1) / threads;
+    finalize_kernel<<<blocks, threads, 0, stream>>>(pr, b);
+    ++*launches;
+  }
+  if (ev && (e = cudaEventRecord(ev[3], stream)) != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
