@@ -43,6 +43,7 @@ constexpr int kAlphaChunk = GD_ALPHA_CHUNK;
 #define GD_QT_GROUPS 2
 #endif
 constexpr int kQtGroups = GD_QT_GROUPS;  // quarter-turn groups per pass over the atoms
+constexpr uint32_t kPairCap = 64;        // cross-pair list entries per warp (folded when full)
 // Optional device-side phase timers (build with -DGD_PHASE_TIMERS): per-warp clock64 deltas summed
 // into gd_stats-adjacent counters 8..15 (setup, align coarse, align refine, refresh, step head,
 // step coarse candidates, step decisions+commit, tail).
@@ -672,11 +673,12 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
   }
   float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
-  // Behind the atom slot, max(NS, 2) words per atom: the per-step survivor words (word t of moved
-  // atom m (DFS) at SURV[(m-s0-1)*NS+t]), reused as the FP64 scratch of the index-order sums (SCR1,
-  // n doubles, while A is live). Before the sweep A is not live yet and A + SURV hold 3 n doubles
+  // Behind the atom slot, one double per atom: the FP64 scratch of the index-order sums (SCR1, n
+  // doubles, while A is live). Before the sweep A is not live yet and A + SCR1 hold 3 n doubles
   // (SCR3, the centroid sums).
   uint32_t* SURV = reinterpret_cast<uint32_t*>(A + ((b.max_n + 3) & ~3u));
+  // per-step cross-pair list (alpha, beta, gamma) behind SCR1
+  float4* PL = reinterpret_cast<float4*>(SURV + 2 * ((b.max_n + 3) & ~3u));
   double* SCR1 = reinterpret_cast<double*>(SURV);
   double* SCR3 = reinterpret_cast<double*>(A);
   const CoarseGrid cg{cells,
@@ -844,6 +846,9 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t lg2_all = rem_all <= 1 ? 5 : rem_all <= 2 ? 4 : rem_all <= 4 ? 3 : rem_all <= 8 ? 2 : rem_all <= 16 ? 1 : 0;
       const float2 cq_p0 = lane + 1 <= n_cand_all ? __ldg(pr.dtab_f + lane + 1) : make_float2(1.f, 0.f);
       const float2 cq_p1 = (lane >> lg2_all) < rem_all ? __ldg(pr.dtab_f + 33 + (lane >> lg2_all)) : make_float2(1.f, 0.f);
+      // full-angle (cos, sin) of the same candidates, for the algebraic cross-pair margins
+      const float2 cf_p0 = make_float2(fmaf(-2.f * cq_p0.y, cq_p0.y, 1.f), 2.f * cq_p0.x * cq_p0.y);
+      const float2 cf_p1 = make_float2(fmaf(-2.f * cq_p1.y, cq_p1.y, 1.f), 2.f * cq_p1.x * cq_p1.y);
       // Per-pose caches, rebuilt after alignment and after every k != 0 commit:
       //   A[pos]     FP32 (gx, gy, gz, rho = cf*r/spacing) in DFS order,
       //   es, cs     exact FP64 and coarse per-atom samples, samb: coarse sample near a face,
@@ -863,9 +868,6 @@ __global__ void __launch_bounds__(NT, 1)
       // |computed - exact| of d^2 - t^2 for pairs near the threshold (d ~ t <= 2 rmax):
       // 2 d |dd| with |dd| <= 2 sqrt(3) ptol, plus FP32 rounding of t^2 and the chain.
       const float tau = 16.0f * rmax * ptol + 4e-6f * rmax * rmax + 1e-6f;
-      // survivor margin on the circle distance: (t + st)^2 - t^2 >= 4 tau, plus 1e-3 grid units for
-      // the FP32 rounding of the cylindrical coordinates (~1e-6 |w|)
-      const float st = 2.0f * sqrtf(tau) + 1e-3f;
 
       auto refresh = [&](bool all, const uint32_t (&mo)[NS]) {
 #pragma unroll
@@ -1078,57 +1080,88 @@ __global__ void __launch_bounds__(NT, 1)
               ay *= il;
               az *= il;
             }
-            // Cross-pair survivors. Rotating M' about the axis keeps each moved atom m on a circle
-            // (axial coordinate h, radius rho about the FP32 axis through pi). A fixed-side atom
-            // whose distance to that circle, sqrt(dh^2 + drho^2), is at least t + 2 sqrt(tau) + 1e-3
-            // passes bump_check at every candidate angle with margin, so its d^2 - t^2 is >= tau for
-            // every k and cannot change any candidate's status. Bit f of word
-            // SURV[(m - s0 - 1) NS + f / 32] marks the other partners of m on the fixed side
-            // [0, s0) U [e0, n) (pairs with atom_j are invariant, see above).
+            // Cross pairs. Rotating M' by theta about the unit axis a through pi
+            // maps u = m - pi to h a + cos(theta) u_perp + sin(theta) (a x u), so for a fixed-side
+            // atom f (w = f - pi) the bump margin of candidate k is
+            //   d_k^2 - t^2 = alpha + beta cos(theta_k) + gamma sin(theta_k),
+            //   alpha = (h_m - h_f)^2 + rho_m^2 + rho_f^2 - t^2, beta = -2 u_perp.w, gamma = -2 (a x u).w,
+            // whose minimum over theta is (h_m - h_f)^2 + (rho_m - rho_f)^2 - t^2 (the distance to
+            // the circle). A pair whose circle distance is >= t + 1e-3 grid units cannot clash at any
+            // angle (the FP32 geometry is good to ~1e-5) and is dropped; the others go to the
+            // per-warp list PL as (alpha, beta, gamma), which every candidate lane folds with two
+            // FFMAs per pair (pairs with atom_j are invariant, see above). The list is folded
+            // whenever the next moved atom's pairs might not fit.
+            float mmin0 = 1e30f, mmin1 = 1e30f;  // this lane's pass-0 candidate / pass-1 share
+            float tau_a;                           // tau plus the FP32 error of the algebraic form
             {
-              float hq[NS], rq[NS], tq[NS];
+              float hq[NS], rq[NS], tq[NS], wx_[NS], wy_[NS], wz_[NS];
+              float d2 = 0.f;
 #pragma unroll
               for (int t = 0; t < NS; ++t) {
                 const uint32_t q = lane + 32 * t;
-                hq[t] = rq[t] = tq[t] = 0.f;
+                hq[t] = rq[t] = tq[t] = wx_[t] = wy_[t] = wz_[t] = 0.f;
                 if (q < n) {
                   const float4 pq = A[q];
                   const float wx = pq.x - fpi.x, wy = pq.y - fpi.y, wz = pq.z - fpi.z;
                   const float h = fmaf(wx, ax, fmaf(wy, ay, wz * az));
-                  const float px = fmaf(-h, ax, wx), py = fmaf(-h, ay, wy), pz = fmaf(-h, az, wz);
+                  wx_[t] = fmaf(-h, ax, wx);
+                  wy_[t] = fmaf(-h, ay, wy);
+                  wz_[t] = fmaf(-h, az, wz);
                   hq[t] = h;
-                  rq[t] = sqrtf(fmaf(px, px, fmaf(py, py, pz * pz)));
-                  tq[t] = pq.w + st;
+                  rq[t] = sqrtf(fmaf(wx_[t], wx_[t], fmaf(wy_[t], wy_[t], wz_[t] * wz_[t])));
+                  tq[t] = pq.w;
+                  d2 = fmaxf(d2, fmaf(h, h, rq[t] * rq[t]));
                 }
               }
+              // |alpha|, |beta|, |gamma| <= 10 D^2 (D = largest distance from pi): FP32 rounding of
+              // the terms and of the fold, the FP32 (cos, sin) and the non-unit FP32 axis, <= 8e-6 D^2
+              tau_a = tau + 8e-6f * warp_max(d2);
+              const uint32_t sub1 = lane & ((1u << lg2_all) - 1u), gs1 = 1u << lg2_all;
+              uint32_t cnt = 0;
+              auto fold = [&]() {
+                __syncwarp();
+                for (uint32_t e = 0; e < cnt; ++e) {
+                  const float4 pe = PL[e];
+                  mmin0 = fminf(mmin0, fmaf(pe.y, cf_p0.x, fmaf(pe.z, cf_p0.y, pe.x)));
+                }
+                for (uint32_t e = sub1; e < cnt; e += gs1) {
+                  const float4 pe = PL[e];
+                  mmin1 = fminf(mmin1, fmaf(pe.y, cf_p1.x, fmaf(pe.z, cf_p1.y, pe.x)));
+                }
+                __syncwarp();
+                cnt = 0;
+              };
               for (uint32_t mq = s0 + 1; mq < e0; ++mq) {
-                const uint32_t sl = mq >> 5, src = mq & 31;
-                float hm = hq[0], rm = rq[0];
-#pragma unroll
-                for (int t = 1; t < NS; ++t)
-                  if (sl == uint32_t(t)) {
-                    hm = hq[t];
-                    rm = rq[t];
-                  }
-                hm = __shfl_sync(FULL, hm, src);
-                rm = __shfl_sync(FULL, rm, src);
-                const float tm = A[mq].w;
+                if (cnt + n > kPairCap) fold();  // at most n - 1 new pairs per moved atom
+                const float4 pm = A[mq];
+                const float ux = pm.x - fpi.x, uy = pm.y - fpi.y, uz = pm.z - fpi.z;
+                const float hm = fmaf(ux, ax, fmaf(uy, ay, uz * az));
+                const float upx = fmaf(-hm, ax, ux), upy = fmaf(-hm, ay, uy), upz = fmaf(-hm, az, uz);
+                const float rm2 = fmaf(upx, upx, fmaf(upy, upy, upz * upz)), rm = sqrtf(rm2);
+                const float vx = fmaf(ay, uz, -az * uy), vy = fmaf(az, ux, -ax * uz), vz = fmaf(ax, uy, -ay * ux);
 #pragma unroll
                 for (int t = 0; t < NS; ++t) {
                   const uint32_t q = lane + 32 * t;
                   const bool fixed = q < n && (q < s0 || q >= e0);
-                  const float dh = hq[t] - hm, dr = rq[t] - rm, T = tq[t] + tm;
-                  const uint32_t word = __ballot_sync(FULL, fixed && fmaf(dh, dh, dr * dr) < T * T);
-                  if (lane == uint32_t(t)) SURV[(mq - s0 - 1) * NS + t] = word;
+                  const float dh = hq[t] - hm, dr = rq[t] - rm, tt = tq[t] + pm.w, T = tt + 1e-3f;
+                  const bool surv = fixed && fmaf(dh, dh, dr * dr) < T * T;
+                  const uint32_t ball = __ballot_sync(FULL, surv);
+                  if (surv) {
+                    const float al = fmaf(dh, dh, fmaf(rq[t], rq[t], fmaf(-tt, tt, rm2)));
+                    const float be = -2.0f * fmaf(upx, wx_[t], fmaf(upy, wy_[t], upz * wz_[t]));
+                    const float ga = -2.0f * fmaf(vx, wx_[t], fmaf(vy, wy_[t], vz * wz_[t]));
+                    PL[cnt + __popc(ball & ((1u << lane) - 1u))] = make_float4(al, be, ga, 0.f);
+                  }
+                  cnt += __popc(ball);
                 }
               }
-              __syncwarp();
+              fold();
             }
             float res_s[2] = {-1e30f, -1e30f};
             uint32_t res_st[2] = {0u, 0u};
             const uint32_t n_cand = pr.S - 1;  // k = 1 .. S-1
             const uint32_t rem = n_cand > 32 ? n_cand - 32 : 0;
-            const uint32_t lg2 = rem <= 1 ? 5 : rem <= 2 ? 4 : rem <= 4 ? 3 : rem <= 8 ? 2 : rem <= 16 ? 1 : 0;
+            const uint32_t lg2 = lg2_all;
 #pragma unroll 1
             for (int pass = 0; pass < 2; ++pass) {
               if (pass == 1 && rem == 0) break;
@@ -1137,14 +1170,11 @@ __global__ void __launch_bounds__(NT, 1)
               const uint32_t grp = lane >> sh, sub = lane & (gs - 1);
               const uint32_t k = pass == 0 ? lane + 1 : 33 + grp;
               const bool active = pass == 0 ? (k <= n_cand) : (grp < rem);
-              // this lane's share of the survivors: bit positions congruent to sub modulo gs
-              uint32_t mypat = 1u;
-#pragma unroll
-              for (uint32_t w = 1; w < 32; w <<= 1)
-                if (w >= gs) mypat |= mypat << w;
-              mypat <<= sub;
-              float part = 0.f, amin = 1e30f, mmin = 1e30f, emin = 1e30f;
+              float part = 0.f, amin = 1e30f, emin = 1e30f;
+              float mmin = pass == 0 ? mmin0 : mmin1;
               if (active) {
+                // moved-atom samples at this lane's angle: the rotation matrix of the half-angle
+                // quaternion (about_axis, geometry.hpp:46-50) in FP32
                 const float2 cq = pass == 0 ? cq_p0 : cq_p1;
                 const float qw = cq.x, qx = ax * cq.y, qy = ay * cq.y, qz = az * cq.y;
                 const float xx = qx * qx, yy = qy * qy, zz = qz * qz, xy = qx * qy, xz = qx * qz, yz = qy * qz;
@@ -1155,22 +1185,12 @@ __global__ void __launch_bounds__(NT, 1)
                 const float tvx = fpi.x - fmaf(m00, fpi.x, fmaf(m01, fpi.y, m02 * fpi.z));
                 const float tvy = fpi.y - fmaf(m10, fpi.x, fmaf(m11, fpi.y, m12 * fpi.z));
                 const float tvz = fpi.z - fmaf(m20, fpi.x, fmaf(m21, fpi.y, m22 * fpi.z));
-                for (uint32_t mq = s0 + 1; mq < e0; ++mq) {
+                for (uint32_t mq = s0 + 1 + sub; mq < e0; mq += gs) {
                   const float4 pm = A[mq];
                   const float gx = fmaf(m00, pm.x, fmaf(m01, pm.y, fmaf(m02, pm.z, tvx)));
                   const float gy = fmaf(m10, pm.x, fmaf(m11, pm.y, fmaf(m12, pm.z, tvy)));
                   const float gz = fmaf(m20, pm.x, fmaf(m21, pm.y, fmaf(m22, pm.z, tvz)));
-                  if (((mq - s0 - 1) & (gs - 1)) == sub) part += coarse_sample_e(cg, gx, gy, gz, amin, emin);
-                  // surviving cross pairs (fixed side and atom_j unless bonded)
-                  const uint32_t* sv = SURV + (mq - s0 - 1) * NS;
-#pragma unroll
-                  for (int t = 0; t < NS; ++t) {
-                    for (uint32_t bits = sv[t] & mypat; bits; bits &= bits - 1) {
-                      const float4 pf = A[32 * t + __ffs(bits) - 1];
-                      const float dx = gx - pf.x, dy = gy - pf.y, dz = gz - pf.z, tt = pm.w + pf.w;
-                      mmin = fminf(mmin, fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -tt * tt))));
-                    }
-                  }
+                  part += coarse_sample_e(cg, gx, gy, gz, amin, emin);
                 }
               }
               for (uint32_t o = 1; o < gs; o <<= 1) {  // group reduction (pass 2)
@@ -1181,7 +1201,7 @@ __global__ void __launch_bounds__(NT, 1)
               }
               uint32_t st = 0;
               if (active) {
-                st = mmin < -tau ? ST_CLASH : (mmin >= tau ? ST_OK : ST_XAMB);
+                st = mmin < -tau_a ? ST_CLASH : (mmin >= tau_a ? ST_OK : ST_XAMB);
                 if (amin <= ptol) st |= ST_SAMB;
                 if (emin > ptol) st |= ST_ALLOUT;
               }
@@ -1368,7 +1388,7 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
                              cudaStream_t stream, cudaEvent_t mid) {
   const uint32_t npad_max = (b.max_n + 3) & ~3u;
   const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
-  const uint32_t slot_b = (4 + (NS > 2 ? NS : 2)) * npad_max;  // A + SURV/SCR (max(NS, 2) words per atom)
+  const uint32_t slot_b = 6 * npad_max + 4 * kPairCap;  // A (4 floats/atom) + SCR1 (1 double/atom) + PL
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32);
   cudaError_t e = pa.cells_in_smem
                       ? launch_persistent(align_coarse_kernel<NS, NTA, true>, pa, n_sms, stream, pk, pr, b, slot_a)
