@@ -376,6 +376,31 @@ int upload_grid_f(gd_ctx* ctx) {
   return GD_OK;
 }
 
+// The pocket cells as an L2-persisting, read-only window on every stream of the context: they
+// are re-read by every warp of every work item, so they should never be evicted by the batch
+// traffic (C5's 47^3 grid does not fit shared memory and is read through L1/L2). Best effort: a
+// device without persisting L2 simply keeps the normal policy.
+void apply_l2_window(gd_ctx* ctx, void* base, size_t bytes) {
+  int max_persist = 0, max_window = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
+  if (max_persist <= 0 || max_window <= 0 || !base || bytes == 0) return;
+  const size_t persist = std::min(bytes, size_t(max_persist));
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = base;
+  v.accessPolicyWindow.num_bytes = std::min(bytes, size_t(max_window));
+  v.accessPolicyWindow.hitRatio = 1.0f;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStream_t streams[3] = {ctx->stream, ctx->slot[0].stream, ctx->slot[1].stream};
+  for (cudaStream_t st : streams)
+    if (st && cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
+}
+
 DevPocket dev_pocket(const gd_ctx* ctx) {
   DevPocket pk{};
   pk.field = ctx->d_field;
@@ -582,6 +607,7 @@ int gd_set_pocket(gd_ctx* ctx, const uint32_t dims[3], const double origin[3], d
   // field outside [0,1] breaks the quantiser, so the fast path is disabled for it (q_eps = inf ->
   // exact kernel).
   ctx->q_eps = in_range ? float(q_err * (1.0 + 1e-6)) : INFINITY;
+  apply_l2_window(ctx, ctx->d_cells, cells.size() * sizeof(uint4));
   ctx->max_step = float(max_step);
   for (int i = 0; i < 3; ++i) {
     ctx->dims[i] = dims[i];

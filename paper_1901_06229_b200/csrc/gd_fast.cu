@@ -73,6 +73,19 @@ struct CoarseGrid {
 // One cell: the four x-edges (C = 1 + c', D = 3 + d' by byte permutes) give fma(fx, D, C) =
 // (c' + fx d') + (1 + 3 fx); the common bias survives the y- and z-lerps unchanged and is removed
 // at the end. Returns the trilinear value of the quantised field.
+// One cell by byte address: shared (SC, a 32-bit shared-window address) or global (an offset from
+// cg.cells, read through the read-only path).
+template <bool SC>
+__device__ __forceinline__ uint4 load_cell(const CoarseGrid& cg, uint32_t addr) {
+  uint4 w;
+  if (SC) {
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(addr));
+  } else {
+    w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(cg.cells) + addr));
+  }
+  return w;
+}
+
 // Byte permutes against one constant K = 0x3F400000: C = bits 0x3F | half0 << 8 (selector 0x7104,
 // half0 carries bit 15, so C = 1 + uc/32768), D = bits 0x40 | half1 << 8 (selector 0x6324, D = 2 +
 // ud/16384). One shared constant lets every PRMT take an immediate selector.
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(NT, 1)
     auto amb_to_g = [&](uint32_t bit) -> uint32_t {
       return separable ? (bit & 15u) * n_frames + lane + 32u * (bit >> 4) : lane + 32u * bit;
     };
-    if (SC && separable && pr.steps[0] % (4 * kQtGroups) == 0) {
+    if (separable && pr.steps[0] % (4 * kQtGroups) == 0) {
       // Quarter-turn symmetry: alpha_{c + q na/4} = alpha_c + q pi/2, so one 2D rotation
       // (rx, ry) = Rz(alpha_c) (wx, wy) gives the four samples t + (rx, ry), t + (-ry, rx),
       // t - (rx, ry), t + (ry, -rx): two FADDs per sample for x, y. kQtGroups consecutive c share
@@ -479,8 +492,9 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t nq = pr.steps[0] / 4;
       // byte offset of a cell from the three RZ-floor bit patterns: 16 bx + 16 cx by + zoff16
       const uint32_t cx16 = cg.cx * 16u, cxy16 = cg.cxy * 16u;
-      const uint32_t base16 = uint32_t(__cvta_generic_to_shared(cg.cells)) - cg.koff * 16u;
-      const uint32_t dummy16 = uint32_t(__cvta_generic_to_shared(cg.cells + cg.dummy));
+      // (shared: absolute 32-bit shared addresses; global: byte offsets from cg.cells)
+      const uint32_t base16 = (SC ? uint32_t(__cvta_generic_to_shared(cg.cells)) : 0u) - cg.koff * 16u;
+      const uint32_t dummy16 = (SC ? uint32_t(__cvta_generic_to_shared(cg.cells)) : 0u) + cg.dummy * 16u;
       for (uint32_t f = lane, m = 0; f < n_frames; f += 32, ++m) {
         const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
 #pragma unroll 1
@@ -517,11 +531,7 @@ __global__ void __launch_bounds__(NT, 1)
                 const float rxf = __fadd_rz(gx, kMagic), ryf = __fadd_rz(gy, kMagic);
                 const float fx = gx - (rxf - kMagic), fy = gy - (ryf - kMagic);
                 const uint32_t addr = __float_as_uint(ryf) * cx16 + (__float_as_uint(rxf) * 16u + zoff16);
-                uint4 w;
-                asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-                             : "r"(e < 0.0f ? addr : dummy16));
-                acc[4 * gi + q] += cell_lerp(w, fx, fy, fz);
+                acc[4 * gi + q] += cell_lerp(load_cell<SC>(cg, e < 0.0f ? addr : dummy16), fx, fy, fz);
               }
             }
           }
@@ -1132,7 +1142,6 @@ __global__ void __launch_bounds__(NT, 1)
                 cnt = 0;
               };
               for (uint32_t mq = s0 + 1; mq < e0; ++mq) {
-                if (cnt + n > kPairCap) fold();  // at most n - 1 new pairs per moved atom
                 const float4 pm = A[mq];
                 const float ux = pm.x - fpi.x, uy = pm.y - fpi.y, uz = pm.z - fpi.z;
                 const float hm = fmaf(ux, ax, fmaf(uy, ay, uz * az));
@@ -1145,6 +1154,7 @@ __global__ void __launch_bounds__(NT, 1)
                   const bool fixed = q < n && (q < s0 || q >= e0);
                   const float dh = hq[t] - hm, dr = rq[t] - rm, tt = tq[t] + pm.w, T = tt + 1e-3f;
                   const bool surv = fixed && fmaf(dh, dh, dr * dr) < T * T;
+                  if (cnt + 32u > kPairCap) fold();  // room for this slot's (<= 32) new pairs
                   const uint32_t ball = __ballot_sync(FULL, surv);
                   if (surv) {
                     const float al = fmaf(dh, dh, fmaf(rq[t], rq[t], fmaf(-tt, tt, rm2)));
@@ -1357,14 +1367,17 @@ struct SmemPlan {
   size_t smem;
 };
 
-static SmemPlan plan_smem(const DevPocket& pk, size_t slot_bytes, int max_warps) {
+// min_warps_sc: the cells go to shared memory only if at least this many warp slots still fit
+// beside them (K1a: 8, its gathers are the hot path; K1b: 12, its few samples can come from L1/L2
+// while more resident warps hide the sweep's latency).
+static SmemPlan plan_smem(const DevPocket& pk, size_t slot_bytes, int max_warps, int min_warps_sc) {
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
   const size_t cell_bytes = size_t(n_cells + 1) * sizeof(uint4);  // + the dummy cell
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   SmemPlan p{};
-  p.cells_in_smem = cell_bytes + 8 * slot_bytes <= size_t(optin);
+  p.cells_in_smem = cell_bytes + size_t(min_warps_sc) * slot_bytes <= size_t(optin);
   const size_t avail = size_t(optin) - (p.cells_in_smem ? cell_bytes : 0);
   p.warps = int(avail / slot_bytes);
   if (p.warps > max_warps) p.warps = max_warps;
@@ -1389,13 +1402,13 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   const uint32_t npad_max = (b.max_n + 3) & ~3u;
   const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
   const uint32_t slot_b = 6 * npad_max + 4 * kPairCap;  // A (4 floats/atom) + SCR1 (1 double/atom) + PL
-  const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32);
+  const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
   cudaError_t e = pa.cells_in_smem
                       ? launch_persistent(align_coarse_kernel<NS, NTA, true>, pa, n_sms, stream, pk, pr, b, slot_a)
                       : launch_persistent(align_coarse_kernel<NS, NTA, false>, pa, n_sms, stream, pk, pr, b, slot_a);
   if (e != cudaSuccess) return e;
   if (mid && (e = cudaEventRecord(mid, stream)) != cudaSuccess) return e;
-  const SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32);
+  const SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, 12);
   return pb.cells_in_smem ? launch_persistent(dock_fast_kernel<NS, NTB, true>, pb, n_sms, stream, pk, pr, b, slot_b)
                           : launch_persistent(dock_fast_kernel<NS, NTB, false>, pb, n_sms, stream, pk, pr, b, slot_b);
 }

@@ -1,0 +1,77 @@
+"""GPU parity at benchmark scale and the chunked executor.
+
+The exact kernel (GD_MODE_EXACT: the reference's FP64 arithmetic everywhere, pinned to the oracle
+by test_gpu_parity.py) is the checker for the fast two-stage kernels on library sizes the CPU
+oracle cannot cover in seconds: every decision and every output bit must agree. Library sizes
+exceed the executor's chunk (256 ligands), so gd_dock_batch runs several pipelined chunks.
+"""
+import numpy as np
+import pytest
+
+import paper_1901_06229_b200 as gd
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("best_score", "best_restart", "final_xyz", "final_dihedrals", "align_index", "align_score",
+          "restart_score", "step_k", "score_calls")
+
+
+@pytest.fixture(scope="module")
+def pair():
+    fast, exact = gd.Context(0, mode=gd.MODE_FAST), gd.Context(0, mode=gd.MODE_EXACT)
+    yield fast, exact
+    fast.close()
+    exact.close()
+
+
+def _same(a, b):
+    for k in FIELDS:
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+@pytest.mark.parametrize("count,atoms,rots,clash,grid", [
+    (1200, 40, 8, 0.75, None),            # C2 shape, the headline parameters
+    (1200, 40, 8, 0.1, None),             # C2 shape, commits live
+    (160, 120, 32, 0.75, None),           # C4 shape (NS = 4 kernels, cells from L1/L2 in K1b)
+    (160, 120, 32, 0.1, None),
+    (600, 40, 8, 0.3, ((47, 47, 47), 0.375)),  # C5 fine grid (cells do not fit shared memory)
+])
+def test_fast_equals_exact_at_scale(pair, count, atoms, rots, clash, grid):
+    fast, exact = pair
+    pocket = gd.make_pocket(gd.PocketSpec(dims=grid[0], spacing=grid[1]) if grid else gd.PocketSpec())
+    lib = gd.make_library(gd.LibrarySpec(count, atoms, rots, 5))
+    p = gd.DockParams(clash_factor=clash)
+    _same(fast.dock(lib, pocket, p, trace=True), exact.dock(lib, pocket, p, trace=True))
+
+
+def test_executor_chunks_match_staged_run(pair):
+    """gd_dock_batch (chunked, two streams) == gd_stage/gd_run/gd_fetch (one batch), bit for bit."""
+    fast, _ = pair
+    pocket = gd.make_pocket()
+    lib = gd.make_library(gd.LibrarySpec(1100, 28, 5, 3))
+    p = gd.DockParams(n_restarts=8, clash_factor=0.2)
+    a = fast.dock(lib, pocket, p, trace=True)
+    b = fast.stage(lib)
+    b.run()
+    c = b.fetch(trace=True)
+    b.free()
+    _same(a, c)
+    # and again through the same (now warm, grow-only) staging slots with a different size
+    _same(fast.dock(lib.slice(100, 900), pocket, p, trace=True), fast.dock(lib.slice(100, 900), pocket, p, trace=True))
+
+
+def test_executor_reports_first_invalid_ligand_in_a_late_chunk(pair):
+    fast, _ = pair
+    good = gd.make_library(gd.LibrarySpec(700, 12, 2, 1))
+    ligs = [dict(name=f"g{i}", xyz=good.xyz[good.atom_off[i]:good.atom_off[i + 1]],
+                 radius=good.radius[good.atom_off[i]:good.atom_off[i + 1]],
+                 bonds=good.bonds[good.bond_off[i]:good.bond_off[i + 1]],
+                 rots=good.rots[good.rot_off[i]:good.rot_off[i + 1]]) for i in range(700)]
+    ligs[650] = dict(name="late_bad", xyz=[[0, 0, 0], [9, 9, 9]], radius=[1.0, 1.0])
+    ligs[690] = dict(name="later_bad", xyz=[[0, 0, 0]], radius=[-1.0])
+    lib = gd.Library.from_ligands(ligs)
+    with pytest.raises(gd.ValidationError, match="ligand 'late_bad' is invalid"):
+        fast.dock(lib, gd.make_pocket(), gd.DockParams(n_restarts=2))
+    # the context recovers
+    out = fast.dock(lib.slice(0, 300), gd.make_pocket(), gd.DockParams(n_restarts=2))
+    assert out.best_score.shape == (300,)
