@@ -52,6 +52,9 @@ constexpr uint32_t kPairCap = 64;        // cross-pair list entries per warp (fo
 #else
 #define GD_T(slot) do { } while (0)
 #endif
+#ifndef GD_K1B_MIN_WARPS_SC
+#define GD_K1B_MIN_WARPS_SC 12  // K1b keeps the cells in shared memory only if this many warps still fit
+#endif
 #ifndef GD_ALIGN_THREADS
 #define GD_ALIGN_THREADS 512
 #endif
@@ -245,8 +248,19 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// Word w of a register bit set without dynamic indexing (a dynamic index would put the whole
+// array in local memory).
 template <int NW>
-__device__ __forceinline__ bool bit4(const uint32_t (&m)[NW], uint32_t a) { return (m[a >> 5] >> (a & 31)) & 1u; }
+__device__ __forceinline__ uint32_t word_of(const uint32_t (&m)[NW], uint32_t w) {
+  uint32_t v = m[0];
+#pragma unroll
+  for (int i = 1; i < NW; ++i)
+    if (w == uint32_t(i)) v = m[i];
+  return v;
+}
+
+template <int NW>
+__device__ __forceinline__ bool bit4(const uint32_t (&m)[NW], uint32_t a) { return (word_of<NW>(m, a >> 5) >> (a & 31)) & 1u; }
 
 // Bits [lo, hi) of a bit set, restricted to word w.
 __device__ __forceinline__ uint32_t range_word(uint32_t w, uint32_t lo, uint32_t hi) {
@@ -279,52 +293,74 @@ __device__ __noinline__ double exact_rotation_score(const DevPocket& pk, const d
   return __ddiv_rn(sum, double(n));
 }
 
+#define GD_MO4(mo) (mo)[0], NS > 1 ? (mo)[NS > 1 ? 1 : 0] : 0u, NS > 2 ? (mo)[NS > 2 ? 2 : 0] : 0u, \
+                   NS > 3 ? (mo)[NS > 3 ? 3 : 0] : 0u
+
+// The exact paths of the dihedral sweep read the warp's FP64 pose X (3n doubles, atom order) and
+// exact per-atom samples ES from its shared-memory slot: during the sweep the pose lives there,
+// not in registers (register pressure of the step loop).
+
 // Exact FP64 test of the non-bonded pairs of candidate k (rotate: M' atoms rotated by q about pi).
 // cross_only: only pairs with exactly one atom in M' (the invariant pairs are known exactly).
 template <int NS>
-__device__ bool exact_clash(const DevBatch& b, const Item& it, const Pose<NS>& P, const double (&rad)[NS],
-                            const uint32_t (&mo)[NS], bool rotate, V3d pi, const Qd& q, double clash,
-                            bool cross_only, uint32_t lane) {
+__device__ __forceinline__ bool exact_clash_g(const DevBatch& b, uint32_t atom_base, uint32_t adj_base, uint32_t n,
+                                           const double* X, uint32_t mo0, uint32_t mo1, uint32_t mo2, uint32_t mo3,
+                                           bool rotate, V3d pi, Qd q, double clash, bool cross_only, uint32_t lane) {
+  const uint32_t mo[4] = {mo0, mo1, mo2, mo3};
+  const uint32_t W = (n + 31) >> 5;
   V3d pa[NS];
+  double ra[NS];
 #pragma unroll
   for (int t = 0; t < NS; ++t) {
     const uint32_t a = lane + 32 * t;
-    pa[t] = own(P, t);
-    if (rotate && a < it.n && bit4(mo, a)) pa[t] = rotated_about(pa[t], pi, q);
+    pa[t] = V3d{0.0, 0.0, 0.0};
+    ra[t] = 0.0;
+    if (a < n) {
+      pa[t] = V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]};
+      ra[t] = b.atoms[atom_base + a].w;
+      if (rotate && bit4<4>(mo, a)) pa[t] = rotated_about(pa[t], pi, q);
+    }
   }
   bool hit = false;
-  for (uint32_t bb = 0; bb < it.n; ++bb) {
-    V3d pb = fetch<NS>(P, bb);
-    const bool bm = bit4(mo, bb);
+  for (uint32_t bb = 0; bb < n; ++bb) {
+    V3d pb{X[3 * bb], X[3 * bb + 1], X[3 * bb + 2]};
+    const bool bm = bit4<4>(mo, bb);
     if (rotate && bm) pb = rotated_about(pb, pi, q);
-    const double rb = b.atoms[it.m.atom_base + bb].w;
-    const uint32_t* row = b.adj + it.m.adj_base + bb * it.W;
+    const double rb = b.atoms[atom_base + bb].w;
+    const uint32_t* row = b.adj + adj_base + bb * W;
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
       const uint32_t a = lane + 32 * t;
-      if (a >= it.n || a <= bb) continue;
-      if (cross_only && bit4(mo, a) == bm) continue;
+      if (a >= n || a <= bb) continue;
+      if (cross_only && bit4<4>(mo, a) == bm) continue;
       if ((__ldg(row + (a >> 5)) >> (a & 31)) & 1u) continue;
-      hit |= pair_clash_exact(pa[t], pb, rad[t], rb, clash);
+      hit |= pair_clash_exact(pa[t], pb, ra[t], rb, clash);
     }
   }
   return __any_sync(FULL, hit);
 }
 
-// Exact score of dihedral candidate k > 0 (score_pose, scoring.cpp:40-45): M' atoms rotated and
-// sampled in FP64, the others from the exact per-atom cache, summed in atom order.
+// Exact score of dihedral candidate k (score_pose, scoring.cpp:40-45): M' atoms rotated by q about
+// pi and sampled in FP64 (none when rotate is false: the current pose, k = 0), the others from the
+// exact per-atom cache, summed in atom order.
 template <int NS>
-__device__ double exact_candidate_score(const DevPocket& pk, const Item& it, const Pose<NS>& P,
-                                        const double (&es)[NS], const uint32_t (&mo)[NS], V3d pi,
-                                        const Qd& q, uint32_t lane, double* scr) {
+__device__ __forceinline__ double exact_candidate_score_g(const DevPocket& pk, uint32_t n, const double* X,
+                                                       const double* ES, uint32_t mo0, uint32_t mo1, uint32_t mo2,
+                                                       uint32_t mo3, bool rotate, V3d pi, Qd q, uint32_t lane,
+                                                       double* scr) {
+  const uint32_t mo[4] = {mo0, mo1, mo2, mo3};
   double ns[NS];
 #pragma unroll
   for (int t = 0; t < NS; ++t) {
     const uint32_t a = lane + 32 * t;
-    ns[t] = es[t];
-    if (a < it.n && bit4(mo, a)) ns[t] = sample_exact_ni(pk, rotated_about(own(P, t), pi, q));
+    ns[t] = 0.0;
+    if (a < n) {
+      ns[t] = ES[a];
+      if (rotate && bit4<4>(mo, a))
+        ns[t] = sample_exact(pk, rotated_about(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, pi, q));
+    }
   }
-  return __ddiv_rn(ordered_sum_smem<NS>(ns, it.n, scr, lane), double(it.n));
+  return __ddiv_rn(ordered_sum_smem<NS>(ns, n, scr, lane), double(n));
 }
 
 }  // namespace
@@ -687,8 +723,11 @@ __global__ void __launch_bounds__(NT, 1)
   // doubles, while A is live). Before the sweep A is not live yet and A + SCR1 hold 3 n doubles
   // (SCR3, the centroid sums).
   uint32_t* SURV = reinterpret_cast<uint32_t*>(A + ((b.max_n + 3) & ~3u));
-  // per-step cross-pair list (alpha, beta, gamma) behind SCR1
+  // per-step cross-pair list (alpha, beta, gamma) behind SCR1, then the sweep's FP64 pose X (3 per
+  // atom, atom order) and exact per-atom samples ES
   float4* PL = reinterpret_cast<float4*>(SURV + 2 * ((b.max_n + 3) & ~3u));
+  double* X = reinterpret_cast<double*>(PL + kPairCap);
+  double* ES = X + 3 * ((b.max_n + 3) & ~3u);
   double* SCR1 = reinterpret_cast<double*>(SURV);
   double* SCR3 = reinterpret_cast<double*>(A);
   const CoarseGrid cg{cells,
@@ -827,7 +866,13 @@ __global__ void __launch_bounds__(NT, 1)
         set_own(P, s, rotated_about(own(P, s), cen, q));
         rad[s] = a < n ? b.atoms[it.m.atom_base + a].w : 0.0;
         pos[s] = a < n ? b.dfs_pos[it.m.atom_base + a] : 0;
+        if (a < n) {  // from here on the pose lives in the warp's shared slot
+          X[3 * a] = P.x[s];
+          X[3 * a + 1] = P.y[s];
+          X[3 * a + 2] = P.z[s];
+        }
       }
+      __syncwarp();
     }
     double score = best_s;
     if (lane == 0) {
@@ -863,7 +908,6 @@ __global__ void __launch_bounds__(NT, 1)
       //   A[pos]     FP32 (gx, gy, gz, rho = cf*r/spacing) in DFS order,
       //   es, cs     exact FP64 and coarse per-atom samples, samb: coarse sample near a face,
       //   crow       exact clash partners (DFS bit rows), arow: pairs within tau of the threshold.
-      double es[NS];
       float cs[NS];
       bool samb[NS];
       uint32_t crow[NS][NS], arow[NS][NS];
@@ -884,11 +928,12 @@ __global__ void __launch_bounds__(NT, 1)
         for (int s = 0; s < NS; ++s) {
           const uint32_t a = lane + 32 * s;
           if (a < n && (all || bit4(mo, a))) {
-            const float gx = float(__ddiv_rn(__dsub_rn(P.x[s], pk.origin[0]), pk.spacing));
-            const float gy = float(__ddiv_rn(__dsub_rn(P.y[s], pk.origin[1]), pk.spacing));
-            const float gz = float(__ddiv_rn(__dsub_rn(P.z[s], pk.origin[2]), pk.spacing));
+            const V3d pa{X[3 * a], X[3 * a + 1], X[3 * a + 2]};
+            const float gx = float(__ddiv_rn(__dsub_rn(pa.x, pk.origin[0]), pk.spacing));
+            const float gy = float(__ddiv_rn(__dsub_rn(pa.y, pk.origin[1]), pk.spacing));
+            const float gz = float(__ddiv_rn(__dsub_rn(pa.z, pk.origin[2]), pk.spacing));
             A[pos[s]] = make_float4(gx, gy, gz, rho[s]);
-            es[s] = sample_exact_ni(pk, own(P, s));
+            ES[a] = sample_exact_ni(pk, pa);
             float am = 1e30f;
             cs[s] = coarse_sample(cg, gx, gy, gz, am);
             samb[s] = am <= ptol;
@@ -930,19 +975,28 @@ __global__ void __launch_bounds__(NT, 1)
         }
         if (__any_sync(FULL, any_amb)) {  // near-threshold pairs: exact FP64 verdict
           for (uint32_t bb = 0; bb < n; ++bb) {
-            const V3d pb = fetch<NS>(P, bb);
+            const V3d pb{X[3 * bb], X[3 * bb + 1], X[3 * bb + 2]};
             const uint32_t q = b.dfs_pos[it.m.atom_base + bb];
             const double rb = b.atoms[it.m.atom_base + bb].w;
+            const uint32_t bit = 1u << (q & 31), qw = q >> 5;
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
-              const uint32_t bit = 1u << (q & 31);
-              if (arow[s][q >> 5] & bit) {
+              // word qw of row s without a dynamic index (keeps crow/arow in registers)
+              const uint32_t aw = word_of<NS>(arow[s], qw);
+              if (aw & bit) {
                 // exact verdict (scoring.cpp:52-58: clash iff d^2 < thr^2 iff d^2 - thr^2 < 0); the
                 // pair stays flagged ("razor") only if its exact margin is within 1e-8 A^2, where
                 // the FP64 rounding of a rotated candidate (~1e-12 A^2) could flip an invariant pair
-                const double mg = pair_margin_exact(own(P, s), pb, rad[s], rb, pr.clash);
-                if (mg < 0.0) crow[s][q >> 5] |= bit;
-                if (!(fabs(mg) <= 1e-8)) arow[s][q >> 5] &= ~bit;
+                const uint32_t a = lane + 32 * s;
+                const double mg = pair_margin_exact(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, pb,
+                                                    b.atoms[it.m.atom_base + a].w, rb, pr.clash);
+                const uint32_t set_c = mg < 0.0 ? bit : 0u, clr_a = fabs(mg) <= 1e-8 ? 0u : bit;
+#pragma unroll
+                for (int w = 0; w < NS; ++w)
+                  if (qw == uint32_t(w)) {
+                    crow[s][w] |= set_c;
+                    arow[s][w] &= ~clr_a;
+                  }
               }
             }
           }
@@ -991,7 +1045,9 @@ __global__ void __launch_bounds__(NT, 1)
               mo[w] = uint32_t(w) < it.W ? __ldg(b.masks + it.m.mask_base + r * it.W + w) : 0u;
               md[w] = 0u;
             }
-            mo[ij.y >> 5] &= ~(1u << (ij.y & 31));
+#pragma unroll
+            for (int w = 0; w < NS; ++w)
+              if ((ij.y >> 5) == uint32_t(w)) mo[w] &= ~(1u << (ij.y & 31));
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
               const uint32_t a = lane + 32 * s;
@@ -1036,8 +1092,8 @@ __global__ void __launch_bounds__(NT, 1)
           bool have_axis = false;
           auto get_axis = [&]() {
             if (have_axis) return;
-            pi = fetch<NS>(P, ij.x);
-            const V3d delta = vsub(fetch<NS>(P, ij.y), pi);
+            pi = V3d{X[3 * ij.x], X[3 * ij.x + 1], X[3 * ij.x + 2]};
+            const V3d delta = vsub(V3d{X[3 * ij.y], X[3 * ij.y + 1], X[3 * ij.y + 2]}, pi);
             axis = vscale(__ddiv_rn(1.0, __dsqrt_rn(vdot(delta, delta))), delta);
             have_axis = true;
           };
@@ -1045,8 +1101,8 @@ __global__ void __launch_bounds__(NT, 1)
             const float4 fi = A[it.m.fast_ok ? ipos : 0u], fj = A[it.m.fast_ok ? s0 : 0u];
             const float dx = fj.x - fi.x, dy = fj.y - fi.y, dz = fj.z - fi.z;
             if (!it.m.fast_ok || dx * dx + dy * dy + dz * dz < 1e-6f) {
-              const V3d qi = fetch<NS>(P, ij.x);
-              const V3d delta = vsub(fetch<NS>(P, ij.y), qi);
+              const V3d qi{X[3 * ij.x], X[3 * ij.x + 1], X[3 * ij.x + 2]};
+              const V3d delta = vsub(V3d{X[3 * ij.y], X[3 * ij.y + 1], X[3 * ij.y + 2]}, qi);
               if (__dsqrt_rn(vdot(delta, delta)) < 1e-12) {
                 if (lane == 0 && atomicCAS(b.error, 0, GD_ERR_DEGENERATE_AXIS) == 0) b.error[1] = int(it.lig);
                 break;
@@ -1066,12 +1122,13 @@ __global__ void __launch_bounds__(NT, 1)
             get_axis();
             for (uint32_t k = 0; k < pr.S; ++k) {
               const Qd q = frag_quat(pr.dtab[k], axis);
-              const double sk = k == 0 ? __ddiv_rn(ordered_sum_smem<NS>(es, n, SCR1, lane), double(n))
-                                       : exact_candidate_score<NS>(pk, it, P, es, mo, pi, q, lane, SCR1);
+              const double sk = exact_candidate_score_g<NS>(pk, n, X, ES, GD_MO4(mo), k != 0, pi, q, lane, SCR1);
               bool clash;
               if (k == 0) clash = !elig0;
-              else if (frag) clash = exact_clash<NS>(b, it, P, rad, mo, true, pi, q, pr.clash, false, lane);
-              else clash = inv || exact_clash<NS>(b, it, P, rad, mo, true, pi, q, pr.clash, true, lane);
+              else if (frag) clash = exact_clash_g<NS>(b, it.m.atom_base, it.m.adj_base, n, X, GD_MO4(mo), true, pi, q,
+                                                       pr.clash, false, lane);
+              else clash = inv || exact_clash_g<NS>(b, it.m.atom_base, it.m.adj_base, n, X, GD_MO4(mo), true, pi, q,
+                                                    pr.clash, true, lane);
               if (!clash && (!committed || sk > bs)) {
                 committed = true;
                 bk = k;
@@ -1247,8 +1304,8 @@ __global__ void __launch_bounds__(NT, 1)
                   const uint32_t k = (h == 0 ? 1u : 33u) + src;
                   ++st_sexact;
                   get_axis();
-                  const bool cl = exact_clash<NS>(b, it, P, rad, mo, true, pi, frag_quat(pr.dtab[k], axis),
-                                                  pr.clash, true, lane);
+                  const bool cl = exact_clash_g<NS>(b, it.m.atom_base, it.m.adj_base, n, X, GD_MO4(mo), true, pi,
+                                                    frag_quat(pr.dtab[k], axis), pr.clash, true, lane);
                   if (lane == src) res_st[h] = (res_st[h] & (ST_SAMB | ST_ALLOUT)) | (cl ? ST_CLASH : ST_OK);
                 }
               }
@@ -1296,7 +1353,8 @@ __global__ void __launch_bounds__(NT, 1)
                   const uint32_t k = (h == 0 ? 1u : 33u) + src;
                   ++st_sexact;
                   get_axis();
-                  const double sk = exact_candidate_score<NS>(pk, it, P, es, mo, pi, frag_quat(pr.dtab[k], axis), lane, SCR1);
+                  const double sk = exact_candidate_score_g<NS>(pk, n, X, ES, GD_MO4(mo), true, pi,
+                                                                frag_quat(pr.dtab[k], axis), lane, SCR1);
                   if (!committed || sk > bs || (sk == bs && k < bk)) {
                     committed = true;
                     bk = k;
@@ -1316,7 +1374,14 @@ __global__ void __launch_bounds__(NT, 1)
               const Qd q = frag_quat(dt, axis);
 #pragma unroll
               for (int s = 0; s < NS; ++s)
-                if (inm[s]) set_own(P, s, rotated_about(own(P, s), pi, q));
+                if (inm[s]) {
+                  const uint32_t a = lane + 32 * s;
+                  const V3d v = rotated_about(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, pi, q);
+                  X[3 * a] = v.x;
+                  X[3 * a + 1] = v.y;
+                  X[3 * a + 2] = v.z;
+                }
+              __syncwarp();
               if (lane == 0) {  // molecule.cpp:170-172
                 double d = fmod(__dadd_rn(dih[r], dt.z), kTwoPiD);
                 if (d < 0.0) d = __dadd_rn(d, kTwoPiD);
@@ -1338,9 +1403,9 @@ __global__ void __launch_bounds__(NT, 1)
     for (int s = 0; s < NS; ++s) {
       const uint32_t a = lane + 32 * s;
       if (a < n) {
-        gpose[3 * a] = P.x[s];
-        gpose[3 * a + 1] = P.y[s];
-        gpose[3 * a + 2] = P.z[s];
+        gpose[3 * a] = X[3 * a];
+        gpose[3 * a + 1] = X[3 * a + 1];
+        gpose[3 * a + 2] = X[3 * a + 2];
       }
     }
     __syncwarp();
@@ -1401,14 +1466,15 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
                              cudaStream_t stream, cudaEvent_t mid) {
   const uint32_t npad_max = (b.max_n + 3) & ~3u;
   const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
-  const uint32_t slot_b = 6 * npad_max + 4 * kPairCap;  // A (4 floats/atom) + SCR1 (1 double/atom) + PL
+  // A (4 floats/atom) + SCR1 (1 double/atom) + PL + X (3 doubles/atom) + ES (1 double/atom)
+  const uint32_t slot_b = 6 * npad_max + 4 * kPairCap + 8 * npad_max;
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
   cudaError_t e = pa.cells_in_smem
                       ? launch_persistent(align_coarse_kernel<NS, NTA, true>, pa, n_sms, stream, pk, pr, b, slot_a)
                       : launch_persistent(align_coarse_kernel<NS, NTA, false>, pa, n_sms, stream, pk, pr, b, slot_a);
   if (e != cudaSuccess) return e;
   if (mid && (e = cudaEventRecord(mid, stream)) != cudaSuccess) return e;
-  const SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, 12);
+  const SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC);
   return pb.cells_in_smem ? launch_persistent(dock_fast_kernel<NS, NTB, true>, pb, n_sms, stream, pk, pr, b, slot_b)
                           : launch_persistent(dock_fast_kernel<NS, NTB, false>, pb, n_sms, stream, pk, pr, b, slot_b);
 }

@@ -1,1 +1,1 @@
-for r in 0 3; do echo "== main reps=$r"; python tools/prof_run.py --ligands 4000 --runs 3 --reps $r | grep "run 2"; done
+for c in 0.75 0.1; do echo "== main clash $c"; python tools/prof_run.py --ligands 4000 --runs 3 --clash $c | grep "run 2"; done
