@@ -741,7 +741,8 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t N = pr.n_restarts;
   const uint64_t total = uint64_t(b.n_lig) * N;
   const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
-  unsigned long long st_aexact = 0, st_afall = 0, st_sexact = 0, st_sfall = 0, st_commit = 0, st_items = 0;
+  // per-warp counters (32-bit: a warp's share of one launch stays far below 2^32)
+  uint32_t st_aexact = 0, st_afall = 0, st_sexact = 0, st_sfall = 0, st_commit = 0, st_items = 0;
 #ifdef GD_PHASE_TIMERS
   long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_ph = clock64();
@@ -1411,12 +1412,12 @@ __global__ void __launch_bounds__(NT, 1)
     __syncwarp();
   }
   if (lane == 0) {
-    atomicAdd(b.stats + 0, st_items);
-    atomicAdd(b.stats + 1, st_aexact);
-    atomicAdd(b.stats + 2, st_afall);
-    atomicAdd(b.stats + 3, st_sexact);
-    atomicAdd(b.stats + 4, st_sfall);
-    atomicAdd(b.stats + 5, st_commit);
+    atomicAdd(b.stats + 0, (unsigned long long)st_items);
+    atomicAdd(b.stats + 1, (unsigned long long)st_aexact);
+    atomicAdd(b.stats + 2, (unsigned long long)st_afall);
+    atomicAdd(b.stats + 3, (unsigned long long)st_sexact);
+    atomicAdd(b.stats + 4, (unsigned long long)st_sfall);
+    atomicAdd(b.stats + 5, (unsigned long long)st_commit);
 #ifdef GD_PHASE_TIMERS
     GD_T(7);
     for (int i = 0; i < 8; ++i) atomicAdd(b.stats + 8 + i, (unsigned long long)ph[i]);
