@@ -47,8 +47,9 @@ __device__ __forceinline__ V3d rotated_about(V3d p, V3d c, const Qd& q) {
   return vadd(qapply(q, vsub(p, c)), c);
 }
 
+// Generic load: the field may be staged in shared memory (K1b) or read from global memory.
 __device__ __forceinline__ double fld(const DevPocket& pk, uint32_t ix, uint32_t iy, uint32_t iz) {
-  return __ldg(pk.field + (size_t(iz) * pk.dims[1] + iy) * pk.dims[0] + ix);  // scoring.hpp:24-26
+  return pk.field[(size_t(iz) * pk.dims[1] + iy) * pk.dims[0] + ix];  // scoring.hpp:24-26
 }
 
 // sample_field (scoring.cpp:9-38).

@@ -704,10 +704,11 @@ __global__ void __launch_bounds__(NT, 1)
 // the hot loops, so the kernel trades warps for registers.
 template <int NS, int NT, bool SC>
 __global__ void __launch_bounds__(NT, 1)
-    dock_fast_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t slot_floats) {
+    dock_fast_kernel(DevPocket pk_in, DevParams pr, DevBatch b, uint32_t slot_floats, uint32_t field_in_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
+  DevPocket pk = pk_in;
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
   // SC: the pocket cells are staged once per CTA into shared memory (every warp of every work item
   // reads them; a compile-time flag so the gather is an LDS.128, not a generic load)
@@ -717,6 +718,15 @@ __global__ void __launch_bounds__(NT, 1)
   if (SC) {
     for (uint32_t i = threadIdx.x; i <= n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
     __syncthreads();
+  }
+  if (field_in_smem) {
+    // the FP64 field (exact samples of the refinement, refresh and exact decisions) behind the
+    // warp slots: shared-memory latency instead of L2 for every exact sample
+    double* sf = reinterpret_cast<double*>(slots + size_t(blockDim.x >> 5) * slot_floats);
+    const uint32_t nv = pk.dims[0] * pk.dims[1] * pk.dims[2];
+    for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) sf[v] = pk_in.field[v];
+    __syncthreads();
+    pk.field = sf;
   }
   float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
   // Behind the atom slot, one double per atom: the FP64 scratch of the index-order sums (SCR1, n
@@ -1475,9 +1485,20 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
                       : launch_persistent(align_coarse_kernel<NS, NTA, false>, pa, n_sms, stream, pk, pr, b, slot_a);
   if (e != cudaSuccess) return e;
   if (mid && (e = cudaEventRecord(mid, stream)) != cudaSuccess) return e;
-  const SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC);
-  return pb.cells_in_smem ? launch_persistent(dock_fast_kernel<NS, NTB, true>, pb, n_sms, stream, pk, pr, b, slot_b)
-                          : launch_persistent(dock_fast_kernel<NS, NTB, false>, pb, n_sms, stream, pk, pr, b, slot_b);
+  SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC);
+  if (pb.warps < 1) return cudaErrorInvalidConfiguration;
+  // the FP64 field goes to shared memory too when it fits beside the slots (24^3: 110 KB)
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t field_bytes = size_t(pk.dims[0]) * pk.dims[1] * pk.dims[2] * sizeof(double);
+  const uint32_t fs = pb.smem + field_bytes <= size_t(optin) ? 1u : 0u;
+  if (fs) pb.smem += field_bytes;
+  auto kb = pb.cells_in_smem ? dock_fast_kernel<NS, NTB, true> : dock_fast_kernel<NS, NTB, false>;
+  e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pb.smem));
+  if (e != cudaSuccess) return e;
+  kb<<<n_sms, 32 * pb.warps, pb.smem, stream>>>(pk, pr, b, slot_b, fs);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
