@@ -17,6 +17,8 @@
 // rotations; dihedral sweep = lanes over candidate angles k (32 per pass, the remainder split
 // 2..32 lanes per candidate over the fixed atoms); FP64 master pose = atom a lives in lane a%32,
 // register slot a/32.
+#include <type_traits>
+
 #include "gd_exact.cuh"
 #include "gd_fast.cuh"
 
@@ -447,20 +449,50 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     const float cmx = warp_sum(sx) * inv_n, cmy = warp_sum(sy) * inv_n, cmz = warp_sum(sz) * inv_n;
-    float ext = 0.f;
+    const V3d cen{t4.x + double(cmx), t4.y + double(cmy), t4.z + double(cmz)};
+    const float tx = float(__ddiv_rn(__dsub_rn(cen.x, pk.origin[0]), pk.spacing));
+    const float ty = float(__ddiv_rn(__dsub_rn(cen.y, pk.origin[1]), pk.spacing));
+    const float tz = float(__ddiv_rn(__dsub_rn(cen.z, pk.origin[2]), pk.spacing));
+    // Relative coordinates into A, "safe" atoms first: an atom at distance r from the centroid
+    // stays within r of it under every rotation, so if that ball (plus 2e-3 grid units, far above
+    // the FP32 error and ptol) is strictly inside the grid, every sample of it is inside and away
+    // from the faces: its coarse samples need no box test. Order within A does
+    // not matter for the coarse score (its error bound is order-free).
+    float ext = 0.f, vxs[NS], vys[NS], vzs[NS];
+    bool safe[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const uint32_t a = lane + 32 * s;
-      if (a < n) {
-        const float vx = px[s] - cmx, vy = py[s] - cmy, vz = pz[s] - cmz;
-        A[a] = make_float4(vx, vy, vz, 0.f);
-        ext = fmaxf(ext, sqrtf(fmaf(vx, vx, fmaf(vy, vy, vz * vz))));
-      } else if (a < meta.npad) {
-        A[a] = make_float4(1e6f, 1e6f, 1e6f, 0.f);  // padding: far outside, contributes exactly 1.0
+      vxs[s] = px[s] - cmx;
+      vys[s] = py[s] - cmy;
+      vzs[s] = pz[s] - cmz;
+      const float r = sqrtf(fmaf(vxs[s], vxs[s], fmaf(vys[s], vys[s], vzs[s] * vzs[s])));
+      const float rg = fmaf(r, pk.inv_spacing_f * (1.0f + 1e-5f), 2e-3f);
+      safe[s] = a < n && tx - rg > 0.f && ty - rg > 0.f && tz - rg > 0.f && tx + rg < 2.f * cg.hx &&
+                ty + rg < 2.f * cg.hy && tz + rg < 2.f * cg.hz;
+      if (a < n) ext = fmaxf(ext, r);
+    }
+    uint32_t nsafe = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) nsafe += __popc(__ballot_sync(FULL, safe[s]));
+    {
+      uint32_t before_safe = 0, before_uns = 0;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const uint32_t a = lane + 32 * s;
+        const uint32_t bs = __ballot_sync(FULL, safe[s]), bu = __ballot_sync(FULL, a < n && !safe[s]);
+        const uint32_t lt = (1u << lane) - 1u;
+        if (a < n) {
+          const uint32_t at = safe[s] ? before_safe + __popc(bs & lt) : nsafe + before_uns + __popc(bu & lt);
+          A[at] = make_float4(vxs[s], vys[s], vzs[s], 0.f);
+        } else if (a < meta.npad) {
+          A[a] = make_float4(1e6f, 1e6f, 1e6f, 0.f);  // padding: far outside, contributes exactly 0
+        }
+        before_safe += __popc(bs);
+        before_uns += __popc(bu);
       }
     }
     __syncwarp();
-    const V3d cen{t4.x + double(cmx), t4.y + double(cmy), t4.z + double(cmz)};
     // Position error bound (grid units, per axis) of every FP32 coordinate of this restart, as in
     // K1b; the ligand extent gets a 1e-3 grid-unit allowance for FP32 rounding.
     const float ext_g = warp_max(ext) * pk.inv_spacing_f + 1e-3f;
@@ -478,9 +510,6 @@ __global__ void __launch_bounds__(NT, 1)
     // of a face, the interval bounds from the second pass). Kept per lane: the KTOP largest key_hi,
     // the largest key_hi that was dropped, the largest key_lo. A rotation can be the exact argmax
     // only if key_hi >= max(key_lo) - 2 eps.
-    const float tx = float(__ddiv_rn(__dsub_rn(cen.x, pk.origin[0]), pk.spacing));
-    const float ty = float(__ddiv_rn(__dsub_rn(cen.y, pk.origin[1]), pk.spacing));
-    const float tz = float(__ddiv_rn(__dsub_rn(cen.z, pk.origin[2]), pk.spacing));
     float top_s[KTOP];
     uint32_t top_g[KTOP];
 #pragma unroll
@@ -544,13 +573,14 @@ __global__ void __launch_bounds__(NT, 1)
           }
 #pragma unroll
           for (int gi = 0; gi < kQtGroups; ++gi) cs[gi] = pr.acs[(c0 + gi) & 15];
-#pragma unroll 1
-          for (uint32_t a = 0; a < npad; ++a) {
+          // one atom: SAFE atoms (see above) skip the box test, the face tracking and the dummy
+          auto atom = [&](uint32_t a, auto safe_tag) {
+            constexpr bool SAFE = decltype(safe_tag)::value;
             const float4 v = A[a];
             const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
             const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
             const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
-            const float ez = fabsf(gz - cg.hz) - cg.hz;
+            const float ez = SAFE ? 0.f : fabsf(gz - cg.hz) - cg.hz;
             const float rz = __fadd_rz(gz, kMagic);
             const float fz = gz - (rz - kMagic);
             const uint32_t zoff16 = __float_as_uint(rz) * cxy16 + base16;
@@ -562,15 +592,22 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const float gx = px[q], gy = py[q];
-                const float e = fmaxf(fmaxf(fabsf(gx - cg.hx) - cg.hx, fabsf(gy - cg.hy) - cg.hy), ez);
-                amn[4 * gi + q] = fminf(amn[4 * gi + q], fabsf(e));
                 const float rxf = __fadd_rz(gx, kMagic), ryf = __fadd_rz(gy, kMagic);
                 const float fx = gx - (rxf - kMagic), fy = gy - (ryf - kMagic);
-                const uint32_t addr = __float_as_uint(ryf) * cx16 + (__float_as_uint(rxf) * 16u + zoff16);
-                acc[4 * gi + q] += cell_lerp(load_cell<SC>(cg, e < 0.0f ? addr : dummy16), fx, fy, fz);
+                uint32_t addr = __float_as_uint(ryf) * cx16 + (__float_as_uint(rxf) * 16u + zoff16);
+                if (!SAFE) {
+                  const float e = fmaxf(fmaxf(fabsf(gx - cg.hx) - cg.hx, fabsf(gy - cg.hy) - cg.hy), ez);
+                  amn[4 * gi + q] = fminf(amn[4 * gi + q], fabsf(e));
+                  addr = e < 0.0f ? addr : dummy16;
+                }
+                acc[4 * gi + q] += cell_lerp(load_cell<SC>(cg, addr), fx, fy, fz);
               }
             }
-          }
+          };
+#pragma unroll 1
+          for (uint32_t a = 0; a < nsafe; ++a) atom(a, std::true_type{});
+#pragma unroll 1
+          for (uint32_t a = nsafe; a < npad; ++a) atom(a, std::false_type{});
 #pragma unroll
           for (int gi = 0; gi < kQtGroups; ++gi)
 #pragma unroll
