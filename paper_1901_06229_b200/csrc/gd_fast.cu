@@ -458,8 +458,10 @@ __global__ void __launch_bounds__(NT, 1)
     // the FP32 error and ptol) is strictly inside the grid, every sample of it is inside and away
     // from the faces: its coarse samples need no box test. Order within A does
     // not matter for the coarse score (its error bound is order-free).
+    // Class 0 (safe): the ball is inside in x, y and z. Class 1 (xy-safe): inside in x and y only,
+    // so a sample's box term is its frame's z term (per atom, not per sample). Class 2: the rest.
     float ext = 0.f, vxs[NS], vys[NS], vzs[NS];
-    bool safe[NS];
+    uint32_t cls[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const uint32_t a = lane + 32 * s;
@@ -468,28 +470,35 @@ __global__ void __launch_bounds__(NT, 1)
       vzs[s] = pz[s] - cmz;
       const float r = sqrtf(fmaf(vxs[s], vxs[s], fmaf(vys[s], vys[s], vzs[s] * vzs[s])));
       const float rg = fmaf(r, pk.inv_spacing_f * (1.0f + 1e-5f), 2e-3f);
-      safe[s] = a < n && tx - rg > 0.f && ty - rg > 0.f && tz - rg > 0.f && tx + rg < 2.f * cg.hx &&
-                ty + rg < 2.f * cg.hy && tz + rg < 2.f * cg.hz;
+      const bool xy = tx - rg > 0.f && ty - rg > 0.f && tx + rg < 2.f * cg.hx && ty + rg < 2.f * cg.hy;
+      const bool z = tz - rg > 0.f && tz + rg < 2.f * cg.hz;
+      cls[s] = a >= n ? 3u : (xy ? (z ? 0u : 1u) : 2u);
       if (a < n) ext = fmaxf(ext, r);
     }
-    uint32_t nsafe = 0;
+    uint32_t nsafe = 0, nxy = 0;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) nsafe += __popc(__ballot_sync(FULL, safe[s]));
+    for (int s = 0; s < NS; ++s) {
+      nsafe += __popc(__ballot_sync(FULL, cls[s] == 0u));
+      nxy += __popc(__ballot_sync(FULL, cls[s] == 1u));
+    }
     {
-      uint32_t before_safe = 0, before_uns = 0;
+      uint32_t before[3] = {0u, nsafe, nsafe + nxy};
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const uint32_t a = lane + 32 * s;
-        const uint32_t bs = __ballot_sync(FULL, safe[s]), bu = __ballot_sync(FULL, a < n && !safe[s]);
         const uint32_t lt = (1u << lane) - 1u;
+        uint32_t at = 0u;
+#pragma unroll
+        for (uint32_t c = 0; c < 3u; ++c) {
+          const uint32_t bc = __ballot_sync(FULL, cls[s] == c);
+          if (cls[s] == c) at = before[c] + __popc(bc & lt);
+          before[c] += __popc(bc);
+        }
         if (a < n) {
-          const uint32_t at = safe[s] ? before_safe + __popc(bs & lt) : nsafe + before_uns + __popc(bu & lt);
           A[at] = make_float4(vxs[s], vys[s], vzs[s], 0.f);
         } else if (a < meta.npad) {
           A[a] = make_float4(1e6f, 1e6f, 1e6f, 0.f);  // padding: far outside, contributes exactly 0
         }
-        before_safe += __popc(bs);
-        before_uns += __popc(bu);
       }
     }
     __syncwarp();
@@ -573,14 +582,18 @@ __global__ void __launch_bounds__(NT, 1)
           }
 #pragma unroll
           for (int gi = 0; gi < kQtGroups; ++gi) cs[gi] = pr.acs[(c0 + gi) & 15];
-          // one atom: SAFE atoms (see above) skip the box test, the face tracking and the dummy
-          auto atom = [&](uint32_t a, auto safe_tag) {
-            constexpr bool SAFE = decltype(safe_tag)::value;
+          // one atom of class CLS (see above): 0 skips the box test, the face tracking and the
+          // dummy select; 1 uses its frame's z term for all its samples (one face-tracking update
+          // per atom, a select per sample); 2 tests every sample
+          float amz = 1e30f;
+          auto atom = [&](uint32_t a, auto cls_tag) {
+            constexpr int CLS = decltype(cls_tag)::value;
             const float4 v = A[a];
             const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
             const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
             const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
-            const float ez = SAFE ? 0.f : fabsf(gz - cg.hz) - cg.hz;
+            const float ez = CLS == 0 ? 0.f : fabsf(gz - cg.hz) - cg.hz;
+            if (CLS == 1) amz = fminf(amz, fabsf(ez));
             const float rz = __fadd_rz(gz, kMagic);
             const float fz = gz - (rz - kMagic);
             const uint32_t zoff16 = __float_as_uint(rz) * cxy16 + base16;
@@ -595,7 +608,8 @@ __global__ void __launch_bounds__(NT, 1)
                 const float rxf = __fadd_rz(gx, kMagic), ryf = __fadd_rz(gy, kMagic);
                 const float fx = gx - (rxf - kMagic), fy = gy - (ryf - kMagic);
                 uint32_t addr = __float_as_uint(ryf) * cx16 + (__float_as_uint(rxf) * 16u + zoff16);
-                if (!SAFE) {
+                if (CLS == 1) addr = ez < 0.0f ? addr : dummy16;
+                if (CLS == 2) {
                   const float e = fmaxf(fmaxf(fabsf(gx - cg.hx) - cg.hx, fabsf(gy - cg.hy) - cg.hy), ez);
                   amn[4 * gi + q] = fminf(amn[4 * gi + q], fabsf(e));
                   addr = e < 0.0f ? addr : dummy16;
@@ -605,9 +619,13 @@ __global__ void __launch_bounds__(NT, 1)
             }
           };
 #pragma unroll 1
-          for (uint32_t a = 0; a < nsafe; ++a) atom(a, std::true_type{});
+          for (uint32_t a = 0; a < nsafe; ++a) atom(a, std::integral_constant<int, 0>{});
 #pragma unroll 1
-          for (uint32_t a = nsafe; a < npad; ++a) atom(a, std::false_type{});
+          for (uint32_t a = nsafe; a < nsafe + nxy; ++a) atom(a, std::integral_constant<int, 1>{});
+#pragma unroll 1
+          for (uint32_t a = nsafe + nxy; a < npad; ++a) atom(a, std::integral_constant<int, 2>{});
+#pragma unroll
+          for (int i = 0; i < 4 * kQtGroups; ++i) amn[i] = fminf(amn[i], amz);
 #pragma unroll
           for (int gi = 0; gi < kQtGroups; ++gi)
 #pragma unroll
