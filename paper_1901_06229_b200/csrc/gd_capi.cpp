@@ -6,6 +6,7 @@
 // the reference's own FP64 formulas evaluated with the same libm, so the device sees the same
 // bits the reference computes (compiled with -ffp-contract=off, no -march).
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -27,6 +28,10 @@ using gdk::DevBatch;
 using gdk::DevParams;
 using gdk::DevPocket;
 using gdk::LigMeta;
+
+// executor staging slots: three, so one chunk is always queued on the GPU while the host packs the
+// next and unpacks the previous
+constexpr int kSlots = 3;
 
 struct gd_ctx {
   int device = 0;
@@ -70,9 +75,12 @@ struct gd_ctx {
     size_t h_out_cap = 0;
     void* d_arena = nullptr;
     size_t d_cap = 0;
-    cudaStream_t stream = nullptr;
-    cudaEvent_t done = nullptr;
-  } slot[2];
+    cudaStream_t stream = nullptr;  // copies of this slot
+    cudaEvent_t in = nullptr, mid = nullptr, k = nullptr, done = nullptr;  // H2D | K1a | K2 | D2H done
+  } slot[kSlots];
+  // executor compute streams: all chunks' K1a in order on sa, their K1b + K2 on sb (so chunk c+1's
+  // alignment overlaps chunk c's sweep, and chunks complete in order)
+  cudaStream_t sa = nullptr, sb = nullptr;
 };
 
 struct Layout {
@@ -396,9 +404,11 @@ void apply_l2_window(gd_ctx* ctx, void* base, size_t bytes) {
   v.accessPolicyWindow.hitRatio = 1.0f;
   v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
   v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  cudaStream_t streams[3] = {ctx->stream, ctx->slot[0].stream, ctx->slot[1].stream};
-  for (cudaStream_t st : streams)
+  for (cudaStream_t st : {ctx->stream, ctx->sa, ctx->sb})
     if (st && cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
+  for (auto& sl : ctx->slot)
+    if (sl.stream && cudaStreamSetAttribute(sl.stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess)
+      cudaGetLastError();
 }
 
 DevPocket dev_pocket(const gd_ctx* ctx) {
@@ -479,10 +489,13 @@ int gd_create(int device, gd_ctx** out) {
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_error, sizeof(int) * 2);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_counter, sizeof(unsigned int) * 4);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
-  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+  for (int i = 0; i < kSlots && e == cudaSuccess; ++i) {
     e = cudaStreamCreateWithFlags(&ctx->slot[i].stream, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->slot[i].done, cudaEventDisableTiming);
+    for (cudaEvent_t* ev : {&ctx->slot[i].in, &ctx->slot[i].mid, &ctx->slot[i].k, &ctx->slot[i].done})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
   }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->sa, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->sb, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     static thread_local std::string msg;
     msg = std::string("gd_create: ") + cudaGetErrorString(e);
@@ -513,9 +526,12 @@ void gd_destroy(gd_ctx* ctx) {
     if (sl.h_in) cudaFreeHost(sl.h_in);
     if (sl.h_out) cudaFreeHost(sl.h_out);
     cudaFree(sl.d_arena);
-    if (sl.done) cudaEventDestroy(sl.done);
+    for (cudaEvent_t ev : {sl.in, sl.mid, sl.k, sl.done})
+      if (ev) cudaEventDestroy(ev);
     if (sl.stream) cudaStreamDestroy(sl.stream);
   }
+  if (ctx->sa) cudaStreamDestroy(ctx->sa);
+  if (ctx->sb) cudaStreamDestroy(ctx->sb);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -901,11 +917,12 @@ int reset_device_status(gd_ctx* ctx, cudaStream_t s) {
   return GD_OK;
 }
 
-int launch_batch(gd_ctx* ctx, const DevBatch& d, cudaStream_t s, cudaEvent_t* ev) {
+int launch_batch(gd_ctx* ctx, const DevBatch& d, cudaStream_t s, cudaEvent_t* ev, cudaStream_t s_b = nullptr,
+                 cudaEvent_t mid = nullptr) {
   int launches = 0;
   DevParams pr = dev_params(ctx);
   if (!(ctx->q_eps < 1.0f)) pr.mode = (pr.mode & ~0xff) | GD_MODE_EXACT;
-  const cudaError_t e = gdk::launch_dock(dev_pocket(ctx), pr, d, ctx->n_sms, s, &launches, ev);
+  const cudaError_t e = gdk::launch_dock(dev_pocket(ctx), pr, d, ctx->n_sms, s, &launches, ev, s_b, mid);
   ctx->last.launches = uint32_t(launches);
   if (e != cudaSuccess) return cuda_err(ctx, e, "launch_dock");
   return GD_OK;
@@ -1170,12 +1187,14 @@ int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
 }
 
 // The executor (run_screening, pipeline.cpp:187-290, re-designed for one GPU): the library is
-// cut into chunks; two staging slots (pinned host input/output + device arena, one stream each)
-// alternate, so the host packs chunk c+1 while the GPU runs chunk c, the H2D of c+1 overlaps the
-// kernels of c, and the next chunk's persistent kernels fill the SMs the previous chunk's tail
-// frees. Results are written in library order; an invalid ligand is reported before any of its
-// chunk's work (earlier chunks' results are discarded with the error, as the reference's rethrow
-// after join discards them, pipeline.cpp:262-272).
+// cut into chunks; three staging slots (pinned host input/output + device arena + copy stream)
+// rotate, so the host validates and packs chunk c+1 while the GPU runs earlier chunks. Every
+// chunk's K1a runs in order on one compute stream and its K1b + K2 on a second one, so chunk c+1's
+// alignment overlaps chunk c's sweep (their persistent CTAs share the SMs) and chunks complete in
+// order, one at a time. H2D and D2H run on the slot's copy stream, ordered by events. Results are
+// written in library order; an invalid ligand is reported before any of its chunk's work
+// (earlier chunks' results are discarded with the error, as the reference's rethrow after join
+// discards them, pipeline.cpp:262-272).
 int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
   if (!ctx || !lib || !out || !out->best_score || !out->best_restart) return GD_ERR_ARGUMENT;
   if (!ctx->have_pocket) return set_err(ctx, GD_ERR_NO_POCKET, "no pocket set");
@@ -1195,17 +1214,24 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
   rc = reset_device_status(ctx, ctx->stream);
   if (rc != GD_OK) return rc;
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  // a slot's device arena may be reused only after the K1b that last read it: its done event
+  // (D2H complete) already orders after that K1b, and drain() waits for it before reuse
   struct Pending {
     bool busy = false;
     uint32_t l0 = 0, l1 = 0;
     Layout y;
     std::vector<OutCopy> copies;
-  } pend[2];
+  } pend[kSlots];
   size_t h2d = 0, d2h = 0;
+  // GD_TRACE_EXECUTOR=1: per-chunk host timings (validate, pack, wait for the slot) to stderr
+  const bool trace = std::getenv("GD_TRACE_EXECUTOR") != nullptr;
+  auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   auto drain = [&](int si) -> int {
     Pending& p = pend[si];
     if (!p.busy) return GD_OK;
+    const double t0 = trace ? now() : 0.0;
     GD_CUDA(ctx, cudaEventSynchronize(ctx->slot[si].done));
+    if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) wait %.3f ms\n", p.l0, p.l1, now() - t0);
     // unpack: pinned output staging -> the caller's arrays (library order)
     const unsigned char* src = static_cast<const unsigned char*>(ctx->slot[si].h_out);
     size_t at = 0;
@@ -1218,7 +1244,7 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     return GD_OK;
   };
   for (uint32_t c = 0; c < n_chunks; ++c) {
-    const int si = int(c & 1);
+    const int si = int(c % kSlots);
     auto& slot = ctx->slot[si];
     rc = drain(si);
     if (rc != GD_OK) return rc;
@@ -1240,12 +1266,18 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     if ((rc = ensure_pinned(ctx, slot.h_in, slot.h_in_cap, p.y.host_bytes + 256)) != GD_OK) return rc;
     if ((rc = ensure_pinned(ctx, slot.h_out, slot.h_out_cap, out_bytes + 256)) != GD_OK) return rc;
     if ((rc = ensure_device(ctx, slot.d_arena, slot.d_cap, p.y.total)) != GD_OK) return rc;
+    const double tp = trace ? now() : 0.0;
     pack_library(ctx, &sl.v, p.y, static_cast<unsigned char*>(slot.h_in));
+    if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) pack %.3f ms\n", l0, l1, now() - tp);
     unsigned char* D = static_cast<unsigned char*>(slot.d_arena);
     GD_CUDA(ctx, cudaMemcpyAsync(D, slot.h_in, p.y.host_bytes, cudaMemcpyHostToDevice, slot.stream));
+    GD_CUDA(ctx, cudaEventRecord(slot.in, slot.stream));
     h2d += p.y.host_bytes;
-    rc = launch_batch(ctx, bind_batch(ctx, p.y, D), slot.stream, nullptr);
+    GD_CUDA(ctx, cudaStreamWaitEvent(ctx->sa, slot.in, 0));
+    rc = launch_batch(ctx, bind_batch(ctx, p.y, D), ctx->sa, nullptr, ctx->sb, slot.mid);
     if (rc != GD_OK) return rc;
+    GD_CUDA(ctx, cudaEventRecord(slot.k, ctx->sb));
+    GD_CUDA(ctx, cudaStreamWaitEvent(slot.stream, slot.k, 0));
     size_t at = 0;
     for (const OutCopy& oc : p.copies) {
       GD_CUDA(ctx, cudaMemcpyAsync(static_cast<unsigned char*>(slot.h_out) + at, D + oc.dev_off, oc.bytes,
@@ -1256,7 +1288,8 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     GD_CUDA(ctx, cudaEventRecord(slot.done, slot.stream));
     p.busy = true;
   }
-  for (int si = 0; si < 2; ++si) {
+  for (uint32_t k = 0; k < kSlots; ++k) {
+    const int si = int((n_chunks + k) % kSlots);  // remaining chunks in submission order
     rc = drain(si);
     if (rc != GD_OK) return rc;
   }

@@ -1529,7 +1529,7 @@ static cudaError_t launch_persistent(K kernel, const SmemPlan& p, int n_sms, cud
 // K1a (coarse alignment, NTA threads) then K1b (exact refinement + dihedral sweep, NTB threads).
 template <int NS, int NTA, int NTB>
 static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                             cudaStream_t stream, cudaEvent_t mid) {
+                             cudaStream_t stream, cudaEvent_t mid, cudaStream_t stream_b) {
   const uint32_t npad_max = (b.max_n + 3) & ~3u;
   const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
   // A (4 floats/atom) + SCR1 (1 double/atom) + PL + X (3 doubles/atom) + ES (1 double/atom)
@@ -1540,6 +1540,10 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
                       : launch_persistent(align_coarse_kernel<NS, NTA, false>, pa, n_sms, stream, pk, pr, b, slot_a);
   if (e != cudaSuccess) return e;
   if (mid && (e = cudaEventRecord(mid, stream)) != cudaSuccess) return e;
+  if (stream_b && stream_b != stream) {  // K1b on its own stream, after this batch's K1a
+    if ((e = cudaStreamWaitEvent(stream_b, mid, 0)) != cudaSuccess) return e;
+    stream = stream_b;
+  }
   SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC);
   if (pb.warps < 1) return cudaErrorInvalidConfiguration;
   // the FP64 field goes to shared memory too when it fits beside the slots (24^3: 110 KB)
@@ -1557,10 +1561,11 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
 }
 
 cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                        cudaStream_t stream, cudaEvent_t mid) {
-  if (b.max_n <= 32) return launch_ns<1, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream, mid);
-  if (b.max_n <= 64) return launch_ns<2, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream, mid);
-  if (b.max_n <= 128) return launch_ns<4, GD_ALIGN_THREADS, GD_FAST_THREADS_NS4>(pk, pr, b, n_sms, stream, mid);
+                        cudaStream_t stream, cudaEvent_t mid, cudaStream_t stream_b) {
+  if (b.max_n <= 32) return launch_ns<1, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream, mid, stream_b);
+  if (b.max_n <= 64) return launch_ns<2, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream, mid, stream_b);
+  if (b.max_n <= 128)
+    return launch_ns<4, GD_ALIGN_THREADS, GD_FAST_THREADS_NS4>(pk, pr, b, n_sms, stream, mid, stream_b);
   return cudaErrorNotSupported;  // launch_dock routes > 128 atoms to the exact kernel
 }
 

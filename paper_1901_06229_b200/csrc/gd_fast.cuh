@@ -5,8 +5,9 @@
 
 namespace gdk {
 
-// K1a then K1b; `mid` (nullable) is recorded between them.
+// K1a then K1b; `mid` (nullable) is recorded between them. With stream_b (and mid), K1b runs on
+// stream_b after mid, so the next batch's K1a can follow on `stream` while this K1b runs.
 cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                        cudaStream_t stream, cudaEvent_t mid = nullptr);
+                        cudaStream_t stream, cudaEvent_t mid = nullptr, cudaStream_t stream_b = nullptr);
 
 }  // namespace gdk

@@ -100,8 +100,11 @@ struct DevBatch {
 
 // Kernel launchers (gd_kernels.cu). Return cudaGetLastError() of the launches.
 // ev (nullable): 4 events recorded around K1a, K1b and K2 (per-kernel timing).
+// Pipelined form (stream_b and mid non-null): K1a on `stream`, then K1b and K2 on stream_b after
+// `mid` — the executor keeps the alignment of chunk c+1 and the sweep of chunk c in flight together.
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                        cudaStream_t stream, int* launches, cudaEvent_t* ev = nullptr);
+                        cudaStream_t stream, int* launches, cudaEvent_t* ev = nullptr,
+                        cudaStream_t stream_b = nullptr, cudaEvent_t mid = nullptr);
 // Device top-k by (best_score desc, ligand asc) into out[0..k). Needs scratch from topk_scratch_bytes.
 size_t topk_scratch_bytes(uint32_t n_lig);
 cudaError_t launch_topk(const DevBatch& b, uint32_t k, void* scratch, size_t scratch_bytes,

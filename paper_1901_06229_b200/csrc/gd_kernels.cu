@@ -257,7 +257,9 @@ __global__ void finalize_kernel(DevParams pr, DevBatch b) {
 }
 
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
-                        cudaStream_t stream, int* launches, cudaEvent_t* ev) {
+                        cudaStream_t stream, int* launches, cudaEvent_t* ev, cudaStream_t stream_b,
+                        cudaEvent_t mid) {
+  const bool split = stream_b && mid && stream_b != stream;
   *launches = 0;
   cudaError_t e = cudaMemsetAsync(b.work_counter, 0, 2 * sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
@@ -276,11 +278,16 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
       dock_exact_kernel<<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, stride);
       ++*launches;
       if (ev && (e = cudaEventRecord(ev[1], stream)) != cudaSuccess) return e;
+      if (split) {
+        if ((e = cudaEventRecord(mid, stream)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(stream_b, mid, 0)) != cudaSuccess) return e;
+      }
     } else {
-      e = launch_fast(pk, pr, b, n_sms, stream, ev ? ev[1] : nullptr);  // K1a + K1b
+      e = launch_fast(pk, pr, b, n_sms, stream, split ? mid : (ev ? ev[1] : nullptr), split ? stream_b : nullptr);
       if (e != cudaSuccess) return e;
       *launches += 2;
     }
+    if (split) stream = stream_b;  // K2 follows K1b
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   } else if (ev && (e = cudaEventRecord(ev[1], stream)) != cudaSuccess) {
