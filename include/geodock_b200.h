@@ -36,12 +36,14 @@ extern "C" {
 #define GD_ERR_CUDA 5            /* device / runtime failure (no CPU fallback exists)           */
 #define GD_ERR_NO_POCKET 6       /* gd_dock_* before gd_set_pocket                              */
 #define GD_ERR_UNSUPPORTED 7     /* ligand larger than the kernel's atom limit (GD_MAX_ATOMS)   */
+#define GD_ERR_PARSE 8           /* ParseError        (errors.hpp:15-27): malformed .lgd text     */
 
 #define GD_MAX_ATOMS 256          /* per ligand; the reference has no fixed limit               */
 #define GD_MAX_ROTAMERS 128       /* kMaxRotamers, molecule.hpp:29                              */
 
 typedef struct gd_ctx gd_ctx;
 typedef struct gd_batch gd_batch;
+typedef struct gd_libbuf gd_libbuf;
 
 /* DockParams (docking.hpp:15-22). gd_default_params() returns the reference defaults. */
 typedef struct {
@@ -163,6 +165,16 @@ uint64_t gd_count_score_calls(const gd_params* params, uint64_t n_rotamers);
 int gd_validate_ligand(const gd_library* lib, uint32_t l, char* msg, uint32_t cap);
 /* Moving set of rotamer r of ligand l (finalize_ligand, molecule.cpp:80-99), sorted. */
 int gd_moving_set(const gd_library* lib, uint32_t l, uint32_t r, uint32_t* out, uint32_t* out_len);
+
+/* Ligand ingest: parse_ligand_library (io.cpp:96-140) over a whole .lgd text (len bytes, not
+ * NUL-terminated), multi-threaded on the host. Every record is validated like the reference's
+ * parser does (validate_ligand after "end"); the first failure in stream order is reported with
+ * the reference's message (ParseError text with its 1-based line, or ValidationError) into err.
+ * On success *out owns the library; gd_libbuf_view points a gd_library at it (dihedrals zero,
+ * io.cpp:134); gd_libbuf_free releases it. No GPU needed. */
+int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, uint32_t cap);
+int gd_libbuf_view(const gd_libbuf* buf, gd_library* view);
+void gd_libbuf_free(gd_libbuf* buf);
 
 /* Synthetic inputs (generate.hpp:12-31), host-side and deterministic in the seed. */
 int gd_make_pocket(const uint32_t dims[3], double spacing, const double origin[3], uint32_t blobs,

@@ -134,6 +134,7 @@ class OracleError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"oracle status {code}: {msg}")
         self.code = code
+        self.msg = msg
 
 
 class Oracle:
@@ -153,6 +154,55 @@ class Oracle:
 
     def _fn(self, name):
         return getattr(self.lib, self.p + name)
+
+    # ---- data formats (reference only: io.cpp through the shim)
+    def parse_library(self, text: bytes) -> FlatLibrary:
+        """parse_ligand_library (io.cpp:96-140); raises OracleError(8 parse / 2 validation)."""
+        assert self.kind == "reference", "the port has no parser"
+        f = self._fn("parse_library")
+        f.argtypes = [C.c_char_p, C.c_uint64]
+        self._check(f(text, len(text)))
+        cnt = [C.c_uint64() for _ in range(5)]
+        self._fn("parse_counts")(*[C.byref(c) for c in cnt])
+        L, A, B, R, N = (c.value for c in cnt)
+        lib = FlatLibrary(atom_off=np.zeros(L + 1, np.uint32), xyz=np.zeros((A, 3)), radius=np.zeros(A),
+                          bond_off=np.zeros(L + 1, np.uint32), bonds=np.zeros((B, 2), np.uint32),
+                          rot_off=np.zeros(L + 1, np.uint32), rots=np.zeros((R, 2), np.uint32),
+                          dihedrals=np.zeros(R), name_off=np.zeros(L + 1, np.uint32), names=b"")
+        names = C.create_string_buffer(max(1, N))
+        u32, f64 = C.POINTER(C.c_uint32), C.POINTER(C.c_double)
+        self._fn("parse_fetch")(_ptr(lib.atom_off, u32), _ptr(lib.xyz, f64), _ptr(lib.radius, f64),
+                                _ptr(lib.bond_off, u32), _ptr(lib.bonds, u32), _ptr(lib.rot_off, u32),
+                                _ptr(lib.rots, u32), _ptr(lib.dihedrals, f64), _ptr(lib.name_off, u32), names)
+        lib.names = names.raw[:N]
+        return lib
+
+    def serialize_parsed(self) -> bytes:
+        """serialize_ligand_library (io.cpp:143-160) of the last parse_library result."""
+        f = self._fn("serialize_parsed")
+        f.restype = C.c_uint64
+        n = f(None, 0)
+        buf = C.create_string_buffer(n + 1)
+        f(buf, n)
+        return buf.raw[:n]
+
+    def write_results(self, names: list, best_score, best_restart, score_calls, phase) -> bytes:
+        """write_results (io.cpp:216-223)."""
+        f = self._fn("write_results")
+        f.restype = C.c_uint64
+        enc = [x.encode() for x in names]
+        off = np.zeros(len(enc) + 1, np.uint32)
+        off[1:] = np.cumsum([len(x) for x in enc])
+        u32, f64, u64 = C.POINTER(C.c_uint32), C.POINTER(C.c_double), C.POINTER(C.c_uint64)
+        args = [C.c_uint64(len(enc)), _ptr(off, u32), b"".join(enc),
+                _ptr(np.ascontiguousarray(best_score, np.float64), f64),
+                _ptr(np.ascontiguousarray(best_restart, np.uint32), u32),
+                _ptr(np.ascontiguousarray(score_calls, np.uint64), u64),
+                _ptr(np.ascontiguousarray(phase, np.float64).reshape(-1), f64)]
+        n = f(*args, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        f(*args, buf, n)
+        return buf.raw[:n]
 
     def _check(self, rc):
         if rc != 0:

@@ -18,12 +18,14 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "geodock/docking.hpp"
 #include "geodock/errors.hpp"
 #include "geodock/generate.hpp"
+#include "geodock/io.hpp"
 #include "geodock/molecule.hpp"
 #include "geodock/pipeline.hpp"
 #include "geodock/prng.hpp"
@@ -384,6 +386,101 @@ int ref_run_screening(uint32_t n_lig, const uint32_t* atom_off, const double* xy
   } catch (const std::exception& e) {
     return fail(e, kOther);
   }
+}
+
+// parse_ligand_library (io.cpp:96-140) over a text, flattened like gd_library: the result stays
+// in a thread-local holder; ref_parse_counts / ref_parse_fetch read it out. Returns 0, or the
+// status of the exception (8 ParseError, 2 ValidationError, 9 other) with ref_last_error().
+thread_local std::vector<Ligand> g_parsed;
+
+int ref_parse_library(const char* text, uint64_t len) {
+  g_parsed.clear();
+  try {
+    std::istringstream in(std::string(text, len));
+    g_parsed = parse_ligand_library(in);
+    return kOk;
+  } catch (const ValidationError& e) {
+    return fail(e, kInvalidLigand);
+  } catch (const ParseError& e) {
+    return fail(e, 8);
+  } catch (const std::exception& e) {
+    return fail(e, kOther);
+  }
+}
+
+void ref_parse_counts(uint64_t* n_lig, uint64_t* n_atoms, uint64_t* n_bonds, uint64_t* n_rots, uint64_t* n_chars) {
+  *n_lig = g_parsed.size();
+  *n_atoms = *n_bonds = *n_rots = *n_chars = 0;
+  for (const Ligand& l : g_parsed) {
+    *n_atoms += l.atoms.size();
+    *n_bonds += l.bonds.size();
+    *n_rots += l.rotamers.size();
+    *n_chars += l.name.size();
+  }
+}
+
+void ref_parse_fetch(uint32_t* atom_off, double* xyz, double* radius, uint32_t* bond_off, uint32_t* bonds,
+                     uint32_t* rot_off, uint32_t* rots, double* dihedrals, uint32_t* name_off, char* names) {
+  uint32_t a = 0, b = 0, r = 0, c = 0;
+  for (std::size_t l = 0; l < g_parsed.size(); ++l) {
+    const Ligand& lig = g_parsed[l];
+    atom_off[l] = a;
+    bond_off[l] = b;
+    rot_off[l] = r;
+    name_off[l] = c;
+    for (const Atom& at : lig.atoms) {
+      xyz[3 * a] = at.position.x;
+      xyz[3 * a + 1] = at.position.y;
+      xyz[3 * a + 2] = at.position.z;
+      radius[a++] = at.radius;
+    }
+    for (const Bond& bd : lig.bonds) {
+      bonds[2 * b] = uint32_t(bd.first);
+      bonds[2 * b + 1] = uint32_t(bd.second);
+      ++b;
+    }
+    for (std::size_t q = 0; q < lig.rotamers.size(); ++q) {
+      rots[2 * r] = uint32_t(lig.rotamers[q].atom_i);
+      rots[2 * r + 1] = uint32_t(lig.rotamers[q].atom_j);
+      dihedrals[r++] = lig.dihedrals[q];
+    }
+    for (char ch : lig.name) names[c++] = ch;
+  }
+  const std::size_t L = g_parsed.size();
+  atom_off[L] = a;
+  bond_off[L] = b;
+  rot_off[L] = r;
+  name_off[L] = c;
+}
+
+// serialize_ligand_library (io.cpp:143-160) of the last parsed library into out (cap bytes);
+// returns the full length.
+uint64_t ref_serialize_parsed(char* out, uint64_t cap) {
+  std::ostringstream os;
+  serialize_ligand_library(os, g_parsed);
+  const std::string s = os.str();
+  if (out && cap) std::memcpy(out, s.data(), std::min<uint64_t>(cap, s.size()));
+  return s.size();
+}
+
+// write_results (io.cpp:216-223) of n flat DockResults into out (cap bytes); returns the length.
+uint64_t ref_write_results(uint64_t n, const uint32_t* name_off, const char* names, const double* best_score,
+                           const uint32_t* best_restart, const uint64_t* score_calls, const double* phase,
+                           char* out, uint64_t cap) {
+  std::vector<DockResult> rs(n);
+  for (uint64_t l = 0; l < n; ++l) {
+    rs[l].ligand_name.assign(names + name_off[l], names + name_off[l + 1]);
+    rs[l].best_score = best_score[l];
+    rs[l].best_restart_id = best_restart[l];
+    rs[l].score_calls = score_calls[l];
+    rs[l].phase_times.align_seconds = phase[2 * l];
+    rs[l].phase_times.optimize_seconds = phase[2 * l + 1];
+  }
+  std::ostringstream os;
+  write_results(os, rs);
+  const std::string s = os.str();
+  if (out && cap) std::memcpy(out, s.data(), std::min<uint64_t>(cap, s.size()));
+  return s.size();
 }
 
 }  // extern "C"

@@ -26,7 +26,8 @@ __all__ = [
     "DockParams", "PocketSpec", "LibrarySpec", "Pocket", "Library", "DockResult", "DockResults",
     "RunMetrics", "Context", "make_pocket", "make_library", "make_ligand", "dock_ligand",
     "run_screening", "count_score_calls", "validate_ligand", "moving_set", "GeoDockError",
-    "ValidationError", "ContractError", "DegenerateAxisError", "DeviceError", "lib_path",
+    "ValidationError", "ContractError", "DegenerateAxisError", "DeviceError", "ParseError", "lib_path",
+    "parse_library", "load_library", "serialize_library", "format_double", "write_results",
     "MODE_FAST", "MODE_EXACT", "FLAG_SKIP_INVARIANT_CLASH",
 ]
 
@@ -34,7 +35,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libgeodock_b200.so")
 
 GD_OK, GD_ERR_ARGUMENT, GD_ERR_INVALID_LIGAND, GD_ERR_CONTRACT = 0, 1, 2, 3
-GD_ERR_DEGENERATE_AXIS, GD_ERR_CUDA, GD_ERR_NO_POCKET, GD_ERR_UNSUPPORTED = 4, 5, 6, 7
+GD_ERR_DEGENERATE_AXIS, GD_ERR_CUDA, GD_ERR_NO_POCKET, GD_ERR_UNSUPPORTED, GD_ERR_PARSE = 4, 5, 6, 7, 8
 MODE_FAST, MODE_EXACT, FLAG_SKIP_INVARIANT_CLASH = 0, 1, 0x100
 
 
@@ -59,8 +60,12 @@ class DeviceError(GeoDockError):
     code = GD_ERR_CUDA
 
 
+class ParseError(GeoDockError):        # errors.hpp:15-27 (message carries " (line N)")
+    code = GD_ERR_PARSE
+
+
 _ERRORS = {GD_ERR_INVALID_LIGAND: ValidationError, GD_ERR_CONTRACT: ContractError,
-           GD_ERR_DEGENERATE_AXIS: DegenerateAxisError, GD_ERR_CUDA: DeviceError}
+           GD_ERR_DEGENERATE_AXIS: DegenerateAxisError, GD_ERR_CUDA: DeviceError, GD_ERR_PARSE: ParseError}
 
 
 # ----------------------------------------------------------------------------- ctypes layer
@@ -143,6 +148,9 @@ def _load():
             "gd_validate_ligand": (C.c_int, [C.POINTER(_Library), C.c_uint32, C.c_char_p, C.c_uint32]),
             "gd_moving_set": (C.c_int, [C.POINTER(_Library), C.c_uint32, C.c_uint32, _u32p, _u32p]),
             "gd_make_pocket": (C.c_int, [_u32p, C.c_double, _f64p, C.c_uint32, C.c_uint64, _f64p]),
+            "gd_parse_library": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(vp), C.c_char_p, C.c_uint32]),
+            "gd_libbuf_view": (C.c_int, [vp, C.POINTER(_Library)]),
+            "gd_libbuf_free": (None, [vp]),
             "gd_make_library": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _f64p,
                                           _f64p, _u32p, _u32p]),
         }
@@ -412,6 +420,71 @@ def validate_ligand(lib: Library, i: int = 0) -> List[str]:
     buf = C.create_string_buffer(4096)
     n = _load().gd_validate_ligand(C.byref(L), i, buf, len(buf))
     return [s for s in buf.value.decode().split("\n") if s][:max(n, 0)]
+
+
+# ----------------------------------------------------------------------------- data formats
+def parse_library(text) -> Library:
+    """parse_ligand_library (io.cpp:96-140) over a whole .lgd text (str or bytes), multi-threaded
+    in the C++ host library; every record is validated like the reference's parser does. Raises
+    ParseError / ValidationError with the reference's message."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    lib = _load()
+    h = C.c_void_p()
+    err = C.create_string_buffer(4096)
+    rc = lib.gd_parse_library(data, len(data), C.byref(h), err, len(err))
+    if rc:
+        raise _ERRORS.get(rc, GeoDockError)(err.value.decode(errors="replace"))
+    try:
+        v = _Library()
+        lib.gd_libbuf_view(h, C.byref(v))
+        L = v.n_ligands
+        off = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0, np.uint32)
+        ao, bo, ro, no = (off(getattr(v, k), L + 1) for k in ("atom_off", "bond_off", "rot_off", "name_off"))
+        A, B, R, N = int(ao[-1]), int(bo[-1]), int(ro[-1]), int(no[-1])
+        arr = lambda p, n, dt: (np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0, dt))
+        return Library(atom_off=ao, xyz=arr(v.xyz, 3 * A, np.float64).reshape(-1, 3), radius=arr(v.radius, A, np.float64),
+                       bond_off=bo, bonds=arr(v.bonds, 2 * B, np.uint32).reshape(-1, 2), rot_off=ro,
+                       rots=arr(v.rots, 2 * R, np.uint32).reshape(-1, 2), dihedrals=arr(v.dihedrals, R, np.float64),
+                       name_off=no, names=C.string_at(v.names, N) if N else b"")
+    finally:
+        lib.gd_libbuf_free(h)
+
+
+def load_library(path: str) -> Library:
+    """load_ligand_library (io.cpp:266-269)."""
+    with open(path, "rb") as f:
+        return parse_library(f.read())
+
+
+def format_double(v: float) -> str:
+    """format_double (io.cpp:14-18): %.9g."""
+    return "%.9g" % v
+
+
+def serialize_library(lib: Library) -> str:
+    """serialize_ligand_library (io.cpp:143-160)."""
+    out = []
+    for i in range(lib.n_ligands):
+        a0, a1 = int(lib.atom_off[i]), int(lib.atom_off[i + 1])
+        b0, b1 = int(lib.bond_off[i]), int(lib.bond_off[i + 1])
+        r0, r1 = int(lib.rot_off[i]), int(lib.rot_off[i + 1])
+        out.append(f"ligand {lib.name(i)}\natoms {a1 - a0}\n")
+        for a in range(a0, a1):
+            x, y, z = lib.xyz[a]
+            out.append(f"{format_double(x)} {format_double(y)} {format_double(z)} {format_double(lib.radius[a])}\n")
+        out.append(f"bonds {b1 - b0}\n" + "".join(f"{int(p)} {int(q)}\n" for p, q in lib.bonds[b0:b1]))
+        out.append(f"rotamers {r1 - r0}\n" + "".join(f"{int(p)} {int(q)}\n" for p, q in lib.rots[r0:r1]) + "end\n")
+    return "".join(out)
+
+
+def write_results(lib: Library, res: "DockResults") -> str:
+    """write_results (io.cpp:216-223): the results CSV, one row per ligand in library order."""
+    rows = ["ligand_name,best_score,best_restart_id,score_calls,align_seconds,optimize_seconds\n"]
+    for i in range(lib.n_ligands):
+        rows.append(f"{lib.name(i)},{format_double(res.best_score[i])},{int(res.best_restart[i])},"
+                    f"{int(res.score_calls[i])},{format_double(res.phase_times[2 * i])},"
+                    f"{format_double(res.phase_times[2 * i + 1])}\n")
+    return "".join(rows)
 
 
 def moving_set(lib: Library, i: int, r: int) -> np.ndarray:

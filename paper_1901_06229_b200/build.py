@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INC = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 CU = ["gd_kernels.cu", "gd_fast.cu"]
-CPP = ["gd_capi.cpp", "gd_generate.cpp"]
+CPP = ["gd_capi.cpp", "gd_generate.cpp", "gd_io.cpp"]
 
 
 def _run(cmd):

@@ -1,0 +1,112 @@
+"""Data formats either side of the hot path (CPU): the .lgd library parser (gd_parse_library,
+multi-threaded C++) against the reference's parse_ligand_library (io.cpp:96-140, through the
+oracle/_ref shim), the serializer (io.cpp:143-160) and the results CSV (io.cpp:216-223).
+
+Parity bar: identical arrays (bit-exact doubles), identical bytes for the writers, and for
+malformed input the same exception class and the same message (ParseError text with its line).
+"""
+import numpy as np
+import pytest
+
+import paper_1901_06229_b200 as gd
+from oracle import OracleError
+
+TWO_ATOM = ("ligand probe\n"
+            "atoms 2\n"
+            "0 0 0 0.5\n"
+            "1.5 0 0 0.5\n"
+            "bonds 1\n"
+            "0 1\n"
+            "rotamers 0\n"
+            "end\n")
+
+RING = ("ligand ringy\natoms 3\n0 0 0 0.5\n1.5 0 0 0.5\n0.75 1.3 0 0.5\n"
+        "bonds 3\n0 1\n1 2\n2 0\nrotamers 1\n0 1\nend\n")
+
+# malformed or edge-case texts; each is parsed by both implementations
+CASES = [
+    "", "\n\n  \n", TWO_ATOM, TWO_ATOM * 3, RING,
+    "ligand broken\natoms 2\n0 0 0 0.5\noops 0 0 0.5\n",                      # io_test: line 4
+    "ligand a atoms 1 0 0 0 0.5 bonds 0 rotamers 0 end",                       # one line, no LF
+    TWO_ATOM.replace("\n", "\r\n"),                                            # CRLF
+    "ligand hx\natoms 2\n0x0p+0 0 0 0x1p-1\n+1.5 -0 0 .5\nbonds 1\n0 1\nrotamers 0\nend\n",
+    "ligand big\natoms 2\n1e999 0 0 0.5\n1.5 0 0 0.5\nbonds 1\n0 1\nrotamers 0\nend\n",   # ERANGE
+    "ligand tiny\natoms 2\n1e-400 0 0 0.5\n1.5 0 0 0.5\nbonds 1\n0 1\nrotamers 0\nend\n",  # underflow
+    "ligand nanr\natoms 2\n0 0 0 nan\n1.5 0 0 0.5\nbonds 1\n0 1\nrotamers 0\nend\n",     # validation
+    "ligand infx\natoms 2\ninf 0 0 0.5\n1.5 0 0 0.5\nbonds 1\n0 1\nrotamers 0\nend\n",
+    "ligand neg\natoms -1\n",
+    "ligand cnt\natoms 2x\n",
+    "ligand huge\natoms 99999999999999999999\n",
+    "ligand many\natoms 3\n0 0 0 0.5\n1.5 0 0 0.5\nbonds 1\n0 1\nrotamers 0\nend\n",   # 'bonds' as atom x
+    "ligand trunc\natoms 2\n0 0 0 0.5\n1.5 0",                                 # EOF inside atoms
+    "ligand trunc\natoms 2\n0 0 0 0.5\n1.5 0 0 0.5\n",                         # EOF before bonds
+    "ligand trunc\natoms 2\n0 0 0 0.5\n1.5 0 0 0.5\nbonds 1\n0",               # EOF inside bonds
+    "ligand trunc\natoms 2\n0 0 0 0.5\n1.5 0 0 0.5\nbonds 1\n0 1\nrotamers 1\n0 1\n",  # no end
+    "ligand",                                                                  # EOF before name
+    "ligand x\natoms 1\n0 0 0 0.5\nbond 0\n",                                  # bad keyword
+    "molecule x\n",
+    TWO_ATOM + "garbage\n",
+    "ligand selfbig\natoms 2\n0 0 0 0.5\n1.5 0 0 0.5\nbonds 2\n5000000000 5000000000\n"
+    "5000000000 6000000000\nrotamers 0\nend\n",
+    "ligand rotbig\natoms 2\n0 0 0 0.5\n1.5 0 0 0.5\nbonds 1\n0 1\nrotamers 1\n0 7000000000\nend\n",
+    RING + "ligand later\natoms 2\n0 0 0 0.5\noops\n",                          # validation first
+    "ligand first\natoms 2\n0 0 0 0.5\noops\n" + RING,                         # parse error first
+    TWO_ATOM + "ligand nobond\natoms 2\n0 0 0 0.5\n9 9 9 0.5\nbonds 0\nrotamers 0\nend\n",
+]
+
+
+def _same_lib(a, b):
+    for k in ("atom_off", "bond_off", "rot_off", "name_off"):
+        assert np.array_equal(np.asarray(getattr(a, k), np.uint32), np.asarray(getattr(b, k), np.uint32)), k
+    for k in ("xyz", "radius", "dihedrals"):
+        x, y = np.asarray(getattr(a, k), np.float64).ravel(), np.asarray(getattr(b, k), np.float64).ravel()
+        assert x.tobytes() == y.tobytes(), k  # bit-exact, NaNs included
+    for k in ("bonds", "rots"):
+        assert np.array_equal(np.asarray(getattr(a, k), np.uint32).ravel(), np.asarray(getattr(b, k), np.uint32).ravel()), k
+    assert bytes(a.names) == bytes(b.names)
+
+
+@pytest.mark.parametrize("i", range(len(CASES)))
+def test_parse_matches_reference(reference, i):
+    text = CASES[i].encode()
+    try:
+        ref = reference.parse_library(text)
+        ref_err = None
+    except OracleError as e:
+        ref, ref_err = None, e
+    if ref_err is None:
+        _same_lib(gd.parse_library(text), ref)
+    else:
+        want = {8: gd.ParseError, 2: gd.ValidationError}[ref_err.code]
+        with pytest.raises(want) as got:
+            gd.parse_library(text)
+        assert str(got.value) == ref_err.msg
+
+
+def test_parse_error_reports_line_like_io_test():
+    with pytest.raises(gd.ParseError, match=r"\(line 4\)$"):
+        gd.parse_library(CASES[5])
+
+
+def test_roundtrip_generated_library_matches_reference(reference):
+    lib = gd.make_library(gd.LibrarySpec(3000, 32, 4, 11))  # large enough for several parse threads
+    text = gd.serialize_library(lib).encode()
+    ours = gd.parse_library(text)
+    ref = reference.parse_library(text)
+    _same_lib(ours, ref)
+    assert reference.serialize_parsed() == text  # our writer == the reference's bytes
+    assert gd.serialize_library(ours).encode() == text  # serialize . parse is idempotent
+    # and the parsed library is the generated one up to the 9-digit text format
+    assert np.allclose(ours.xyz, lib.xyz, rtol=1e-8, atol=1e-9)
+    assert np.array_equal(ours.bonds, lib.bonds) and np.array_equal(ours.rots, lib.rots)
+
+
+def test_results_csv_matches_reference(reference):
+    lib = gd.make_library(gd.LibrarySpec(5, 8, 2, 3))
+    rng = np.random.default_rng(0)
+    res = gd.DockResults(best_score=rng.random(5), best_restart=np.arange(5, dtype=np.uint32),
+                         score_calls=np.arange(5, dtype=np.uint64) * 1000 + 79360,
+                         phase_times=rng.random(10) * 1e-3, final_xyz=None, final_dihedrals=None)
+    names = [lib.name(i) for i in range(5)]
+    want = reference.write_results(names, res.best_score, res.best_restart, res.score_calls, res.phase_times)
+    assert gd.write_results(lib, res).encode() == want
