@@ -44,6 +44,7 @@ extern "C" {
 typedef struct gd_ctx gd_ctx;
 typedef struct gd_batch gd_batch;
 typedef struct gd_libbuf gd_libbuf;
+typedef struct gd_pocketbuf gd_pocketbuf;
 
 /* DockParams (docking.hpp:15-22). gd_default_params() returns the reference defaults. */
 typedef struct {
@@ -175,6 +176,12 @@ int gd_moving_set(const gd_library* lib, uint32_t l, uint32_t r, uint32_t* out, 
 int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, uint32_t cap);
 int gd_libbuf_view(const gd_libbuf* buf, gd_library* view);
 void gd_libbuf_free(gd_libbuf* buf);
+/* parse_pocket (io.cpp:162-206): .pkt text -> dims, origin, spacing, x-fastest field (ParseError /
+ * RangeError messages as the reference's). gd_pocketbuf_view's field pointer lives until free. */
+int gd_parse_pocket(const char* text, size_t len, gd_pocketbuf** out, char* err, uint32_t cap);
+int gd_pocketbuf_view(const gd_pocketbuf* buf, uint32_t dims[3], double origin[3], double* spacing,
+                      const double** field);
+void gd_pocketbuf_free(gd_pocketbuf* buf);
 
 /* Synthetic inputs (generate.hpp:12-31), host-side and deterministic in the seed. */
 int gd_make_pocket(const uint32_t dims[3], double spacing, const double origin[3], uint32_t blobs,

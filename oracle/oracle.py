@@ -186,6 +186,30 @@ class Oracle:
         f(buf, n)
         return buf.raw[:n]
 
+    def parse_pocket(self, text: bytes, cap: int = 1 << 22):
+        """parse_pocket (io.cpp:162-206) -> (dims, origin, spacing, field); OracleError(8) on error."""
+        f = self._fn("parse_pocket")
+        dims, origin, field = np.zeros(3, np.uint32), np.zeros(3), np.zeros(cap)
+        sp = C.c_double()
+        f.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(C.c_uint32), C.POINTER(C.c_double),
+                      C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_uint64]
+        self._check(f(text, len(text), _ptr(dims, C.POINTER(C.c_uint32)), _ptr(origin, C.POINTER(C.c_double)),
+                      C.byref(sp), _ptr(field, C.POINTER(C.c_double)), cap))
+        n = int(np.prod(dims.astype(np.uint64)))
+        return tuple(int(x) for x in dims), tuple(float(x) for x in origin), sp.value, field[:n].copy()
+
+    def serialize_pocket(self, dims, origin, spacing, field) -> bytes:
+        """serialize_pocket (io.cpp:208-214)."""
+        f = self._fn("serialize_pocket")
+        f.restype = C.c_uint64
+        d, o, fl = np.asarray(dims, np.uint32), np.asarray(origin, np.float64), np.ascontiguousarray(field, np.float64)
+        args = [_ptr(d, C.POINTER(C.c_uint32)), _ptr(o, C.POINTER(C.c_double)), C.c_double(spacing),
+                _ptr(fl, C.POINTER(C.c_double))]
+        n = f(*args, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        f(*args, buf, n)
+        return buf.raw[:n]
+
     def write_results(self, names: list, best_score, best_restart, score_calls, phase) -> bytes:
         """write_results (io.cpp:216-223)."""
         f = self._fn("write_results")

@@ -483,4 +483,36 @@ uint64_t ref_write_results(uint64_t n, const uint32_t* name_off, const char* nam
   return s.size();
 }
 
+// parse_pocket (io.cpp:162-206) of a text: 0 and the pocket (field_out gets min(cap, n) values),
+// or 8 with ref_last_error() (ParseError / RangeError text).
+int ref_parse_pocket(const char* text, uint64_t len, uint32_t dims[3], double origin[3], double* spacing,
+                     double* field_out, uint64_t cap) {
+  try {
+    std::istringstream in(std::string(text, len));
+    const Pocket p = parse_pocket(in);
+    for (int a = 0; a < 3; ++a) {
+      dims[a] = uint32_t(p.dims[a]);
+      origin[a] = a == 0 ? p.origin.x : a == 1 ? p.origin.y : p.origin.z;
+    }
+    *spacing = p.spacing;
+    for (uint64_t v = 0; v < p.field.size() && v < cap; ++v) field_out[v] = p.field[v];
+    return kOk;
+  } catch (const ParseError& e) {
+    return fail(e, 8);
+  } catch (const std::exception& e) {
+    return fail(e, kOther);
+  }
+}
+
+// serialize_pocket (io.cpp:208-214) into out; returns the full length.
+uint64_t ref_serialize_pocket(const uint32_t dims[3], const double origin[3], double spacing, const double* field,
+                              char* out, uint64_t cap) {
+  const Pocket p = make_pocket_from(dims, origin, spacing, field);
+  std::ostringstream os;
+  serialize_pocket(os, p);
+  const std::string s = os.str();
+  if (out && cap) std::memcpy(out, s.data(), std::min<uint64_t>(cap, s.size()));
+  return s.size();
+}
+
 }  // extern "C"

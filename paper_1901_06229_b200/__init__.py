@@ -28,6 +28,7 @@ __all__ = [
     "run_screening", "count_score_calls", "validate_ligand", "moving_set", "GeoDockError",
     "ValidationError", "ContractError", "DegenerateAxisError", "DeviceError", "ParseError", "lib_path",
     "parse_library", "load_library", "serialize_library", "format_double", "write_results",
+    "parse_pocket", "load_pocket", "serialize_pocket",
     "MODE_FAST", "MODE_EXACT", "FLAG_SKIP_INVARIANT_CLASH",
 ]
 
@@ -151,6 +152,10 @@ def _load():
             "gd_parse_library": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(vp), C.c_char_p, C.c_uint32]),
             "gd_libbuf_view": (C.c_int, [vp, C.POINTER(_Library)]),
             "gd_libbuf_free": (None, [vp]),
+            "gd_parse_pocket": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(vp), C.c_char_p, C.c_uint32]),
+            "gd_pocketbuf_view": (C.c_int, [vp, _u32p, _f64p, C.POINTER(C.c_double),
+                                            C.POINTER(C.POINTER(C.c_double))]),
+            "gd_pocketbuf_free": (None, [vp]),
             "gd_make_library": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _f64p,
                                           _f64p, _u32p, _u32p]),
         }
@@ -454,6 +459,43 @@ def load_library(path: str) -> Library:
     """load_ligand_library (io.cpp:266-269)."""
     with open(path, "rb") as f:
         return parse_library(f.read())
+
+
+def parse_pocket(text) -> Pocket:
+    """parse_pocket (io.cpp:162-206); raises ParseError (RangeError included) with the reference's
+    message."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    lib = _load()
+    h = C.c_void_p()
+    err = C.create_string_buffer(4096)
+    rc = lib.gd_parse_pocket(data, len(data), C.byref(h), err, len(err))
+    if rc:
+        raise _ERRORS.get(rc, GeoDockError)(err.value.decode(errors="replace"))
+    try:
+        dims, origin = np.zeros(3, np.uint32), np.zeros(3)
+        sp, fp = C.c_double(), C.POINTER(C.c_double)()
+        lib.gd_pocketbuf_view(h, _p(dims, _u32p), _p(origin, _f64p), C.byref(sp), C.byref(fp))
+        n = int(np.prod(dims.astype(np.uint64)))
+        field = np.ctypeslib.as_array(fp, shape=(n,)).copy()
+        return Pocket(tuple(int(x) for x in dims), tuple(float(x) for x in origin), float(sp.value), field)
+    finally:
+        lib.gd_pocketbuf_free(h)
+
+
+def load_pocket(path: str) -> Pocket:
+    """load_pocket (io.cpp:271-274)."""
+    with open(path, "rb") as f:
+        return parse_pocket(f.read())
+
+
+def serialize_pocket(p: Pocket) -> str:
+    """serialize_pocket (io.cpp:208-214): header lines, then 12 values per line."""
+    out = [f"origin {format_double(p.origin[0])} {format_double(p.origin[1])} {format_double(p.origin[2])}\n",
+           f"spacing {format_double(p.spacing)}\n", f"dims {p.dims[0]} {p.dims[1]} {p.dims[2]}\n"]
+    f = np.asarray(p.field).ravel()
+    for i, v in enumerate(f):
+        out.append(format_double(v) + ("\n" if (i + 1) % 12 == 0 or i + 1 == len(f) else " "))
+    return "".join(out)
 
 
 def format_double(v: float) -> str:

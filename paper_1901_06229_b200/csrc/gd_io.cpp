@@ -27,6 +27,13 @@
 #include "gd_ligand.h"
 #include "geodock_b200.h"
 
+struct gd_pocketbuf {
+  uint32_t dims[3] = {0, 0, 0};
+  double origin[3] = {0, 0, 0};
+  double spacing = 0;
+  std::vector<double> field;
+};
+
 struct gd_libbuf {
   std::vector<uint32_t> atom_off, bond_off, rot_off, name_off, bonds, rots;
   std::vector<double> xyz, radius, dihedrals;
@@ -110,6 +117,9 @@ bool tok_is(const Tok& tk, size_t i, const char* kw) {
   const size_t n = std::strlen(kw);
   return tk.end_of(i) - tk.start[i] == n && std::memcmp(tk.text + tk.start[i], kw, n) == 0;
 }
+
+// ParseError's message suffix (errors.hpp:18-20): none when the line is unknown (0)
+std::string line_suffix(size_t line) { return line > 0 ? " (line " + std::to_string(line) + ")" : std::string(); }
 
 struct Err {  // a ParseError / ValidationError candidate at a stream position
   uint64_t pos = ~0ull;  // token index (validation: the record's "end" token + 0.5 -> 2*idx+1)
@@ -195,11 +205,10 @@ int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, u
   const uint64_t T = tk.start.size();
   const double t_tok = now();
   auto at_eof = [&](const char* what) {
-    return Err{T, GD_ERR_PARSE, std::string("unexpected end of input, expected ") + what + " (line " +
-                                    std::to_string(tk.lines()) + ")"};
+    return Err{T, GD_ERR_PARSE, std::string("unexpected end of input, expected ") + what + line_suffix(tk.lines())};
   };
   auto tok_err = [&](uint64_t i, const std::string& m) {
-    return m + " (line " + std::to_string(tk.line_of(tk.start[i])) + ")";
+    return m + line_suffix(tk.line_of(tk.start[i]));
   };
   // (2) record headers, sequential
   std::vector<Rec> recs;
@@ -460,5 +469,136 @@ int gd_libbuf_view(const gd_libbuf* b, gd_library* v) {
 }
 
 void gd_libbuf_free(gd_libbuf* b) { delete b; }
+
+// parse_pocket (io.cpp:162-206): header, then dims[0]*dims[1]*dims[2] field values in [0, 1]
+// (x-fastest), nothing after them. Sequential (a pocket is at most a few hundred thousand values);
+// messages as ParseError / RangeError (errors.hpp:15-33).
+int gd_parse_pocket(const char* text, size_t len, gd_pocketbuf** out, char* err, uint32_t cap) {
+  if (!out || (!text && len)) return GD_ERR_ARGUMENT;
+  *out = nullptr;
+  auto fail = [&](const std::string& msg) {
+    if (err && cap) std::snprintf(err, cap, "%s", msg.c_str());
+    return GD_ERR_PARSE;
+  };
+  Tok tk{text, {}, len};
+  bool in = false;
+  for (size_t i = 0; i < len; ++i) {
+    const bool sp = is_space(text[i]);
+    if (!sp && !in) tk.start.push_back(i);
+    in = !sp;
+  }
+  const uint64_t T = tk.start.size();
+  uint64_t i = 0;
+  // line of the reader after consuming token i (its own line) / at the end of input
+  auto at_line = [&](uint64_t t) { return line_suffix(tk.line_of(tk.start[t])); };
+  auto eof_line = [&]() { return line_suffix(tk.lines()); };
+  std::string msg;
+  auto keyword = [&](const char* kw) -> bool {
+    if (i >= T) {
+      msg = std::string("unexpected end of input, expected ") + kw + eof_line();
+      return false;
+    }
+    if (!tok_is(tk, i, kw)) {
+      msg = std::string("expected '") + kw + "', got '" + tk.str(i) + "'" + at_line(i);
+      return false;
+    }
+    ++i;
+    return true;
+  };
+  auto number = [&](const char* what, double& v) -> bool {
+    if (i >= T) {
+      msg = std::string("unexpected end of input, expected ") + what + eof_line();
+      return false;
+    }
+    if (!to_double(tk, i, v)) {
+      msg = std::string("expected a number for ") + what + ", got '" + tk.str(i) + "'" + at_line(i);
+      return false;
+    }
+    ++i;
+    return true;
+  };
+  auto index = [&](const char* what, uint64_t& v) -> bool {
+    if (i >= T) {
+      msg = std::string("unexpected end of input, expected ") + what + eof_line();
+      return false;
+    }
+    if (!to_index(tk, i, v)) {
+      msg = std::string("expected a non-negative integer for ") + what + ", got '" + tk.str(i) + "'" + at_line(i);
+      return false;
+    }
+    ++i;
+    return true;
+  };
+  auto* p = new gd_pocketbuf();
+  uint64_t d[3] = {0, 0, 0};
+  const bool ok = keyword("origin") && number("origin x", p->origin[0]) && number("origin y", p->origin[1]) &&
+                  number("origin z", p->origin[2]) && keyword("spacing") && number("spacing", p->spacing) &&
+                  ([&] {
+                    if (!(p->spacing > 0.0)) {
+                      msg = "spacing must be positive" + at_line(i - 1);
+                      return false;
+                    }
+                    return true;
+                  }()) &&
+                  keyword("dims") && index("nx", d[0]) && index("ny", d[1]) && index("nz", d[2]) && ([&] {
+                    if (d[0] < 2 || d[1] < 2 || d[2] < 2) {
+                      msg = "dims must each be >= 2" + at_line(i - 1);
+                      return false;
+                    }
+                    if (d[0] > 0xffffffffull || d[1] > 0xffffffffull || d[2] > 0xffffffffull) {
+                      msg = "dims too large for this build";
+                      return false;
+                    }
+                    return true;
+                  }());
+  if (!ok) {
+    delete p;
+    return fail(msg);
+  }
+  const uint64_t expected = d[0] * d[1] * d[2];
+  while (p->field.size() < expected && i < T) {
+    double v;
+    if (!to_double(tk, i, v)) {
+      delete p;
+      return fail("expected a field value, got '" + tk.str(i) + "'" + at_line(i));
+    }
+    if (v < 0.0 || v > 1.0) {
+      char num[40];
+      std::snprintf(num, sizeof num, "%.9g", v);  // format_double, io.cpp:14-18
+      const std::string m = std::string("field value ") + num + " outside [0,1]" + at_line(i);
+      delete p;
+      return fail(m);
+    }
+    p->field.push_back(v);
+    ++i;
+  }
+  if (p->field.size() != expected) {
+    const std::string m = "expected " + std::to_string(expected) + " values, got " + std::to_string(p->field.size()) +
+                          eof_line();
+    delete p;
+    return fail(m);
+  }
+  if (i < T) {
+    const std::string m = "trailing content after field values: '" + tk.str(i) + "'" + at_line(i);
+    delete p;
+    return fail(m);
+  }
+  for (int a = 0; a < 3; ++a) p->dims[a] = uint32_t(d[a]);
+  *out = p;
+  return GD_OK;
+}
+
+int gd_pocketbuf_view(const gd_pocketbuf* p, uint32_t dims[3], double origin[3], double* spacing, const double** field) {
+  if (!p || !dims || !origin || !spacing || !field) return GD_ERR_ARGUMENT;
+  for (int a = 0; a < 3; ++a) {
+    dims[a] = p->dims[a];
+    origin[a] = p->origin[a];
+  }
+  *spacing = p->spacing;
+  *field = p->field.data();
+  return GD_OK;
+}
+
+void gd_pocketbuf_free(gd_pocketbuf* p) { delete p; }
 
 }  // extern "C"

@@ -110,3 +110,49 @@ def test_results_csv_matches_reference(reference):
     names = [lib.name(i) for i in range(5)]
     want = reference.write_results(names, res.best_score, res.best_restart, res.score_calls, res.phase_times)
     assert gd.write_results(lib, res).encode() == want
+
+
+POCKETS = [
+    "origin 0 0 0\nspacing 1\ndims 2 2 2\n0 0.25 0.5 1 0 0 1 1\n",              # io_test minimal grid
+    "origin 0 0 0\nspacing 1\ndims 2 2 2\n0 0 0 0 0 0 0\n",                       # value count
+    "origin 0 0 0\nspacing 1\ndims 2 2 2\n0 0 0 1.5 0 0 0 0\n",                   # RangeError
+    "origin 0 0 0\nspacing 1\ndims 2 2 2\n0 0 0 -0.1 0 0 0 0\n",
+    "origin 0 0 0\nspacing 1\ndims 2 2 2\n0 0 0 0 0 0 0 0 extra\n",               # trailing
+    "origin 0 0 0\nspacing 0\ndims 2 2 2\n",
+    "origin 0 0 0\nspacing -1\ndims 2 2 2\n",
+    "origin 0 0 0\nspacing 1\ndims 2 1 2\n",
+    "origin 0 0\nspacing 1\n",
+    "origin 0 0 0\nspacing 1\ndims 2 2 2\n0 0 x 0 0 0 0 0\n",
+    "origin 0 0 0\r\nspacing 0.375\r\ndims 2 2 2\r\n0 0 0 0 0 0 0 0\r\n",
+    "origin 0 0 0 spacing 1 dims 2 2 2 0 0 0 0 0 0 0 0",
+    "",
+    "grid 0 0 0\n",
+    "origin 0 0 0\nspacing 1\ndims 2 2 2\n0 0 0 0\n0 0 0 nan\n",
+]
+
+
+@pytest.mark.parametrize("i", range(len(POCKETS)))
+def test_parse_pocket_matches_reference(reference, i):
+    text = POCKETS[i].encode()
+    try:
+        ref = reference.parse_pocket(text)
+        ref_err = None
+    except OracleError as e:
+        ref, ref_err = None, e
+    if ref_err is None:
+        p = gd.parse_pocket(text)
+        assert p.dims == ref[0] and p.origin == ref[1] and p.spacing == ref[2]
+        assert np.asarray(p.field).tobytes() == ref[3].tobytes()
+    else:
+        with pytest.raises(gd.ParseError) as got:
+            gd.parse_pocket(text)
+        assert str(got.value) == ref_err.msg
+
+
+def test_pocket_roundtrip_matches_reference(reference):
+    p = gd.make_pocket(gd.PocketSpec(dims=(47, 47, 47), spacing=0.375))
+    text = gd.serialize_pocket(p).encode()
+    assert reference.serialize_pocket(p.dims, p.origin, p.spacing, p.field) == text
+    q = gd.parse_pocket(text)
+    ref = reference.parse_pocket(text)
+    assert q.dims == ref[0] and np.asarray(q.field).tobytes() == ref[3].tobytes()
