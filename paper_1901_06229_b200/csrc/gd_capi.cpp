@@ -89,7 +89,7 @@ struct Layout {
   size_t n_items = 0;
   std::vector<uint32_t> mask_base, adj_base;
   size_t o_meta, o_atoms, o_start, o_rots, o_dih0, o_masks, o_adj, o_dfs, o_rdfs, o_adjd, host_bytes;
-  size_t o_cand, o_ncand, o_rs_score, o_rs_ascore, o_rs_aidx, o_rs_stepk, o_rs_xyz, o_rs_dih;
+  size_t o_cand, o_ncand, o_rs_score, o_rs_ascore, o_rs_aidx, o_rs_stepk;
   size_t o_best, o_brs, o_fxyz, o_fdih, o_ctr, total;
 };
 
@@ -582,8 +582,6 @@ Layout plan_layout(const gd_library* lib, const gd_params& P) {
   y.o_rs_ascore = ar.take<double>(y.n_items);
   y.o_rs_aidx = ar.take<uint32_t>(y.n_items);
   y.o_rs_stepk = ar.take<int32_t>(size_t(y.Rt) * N * reps);
-  y.o_rs_xyz = ar.take<double>(size_t(y.A) * N * 3);
-  y.o_rs_dih = ar.take<double>(size_t(y.Rt) * N);
   y.o_best = ar.take<double>(L);
   y.o_brs = ar.take<uint32_t>(L);
   y.o_fxyz = ar.take<double>(size_t(y.A) * 3);
@@ -780,8 +778,6 @@ DevBatch bind_batch(const gd_ctx* ctx, const Layout& y, unsigned char* D) {
   d.rs_align_score = reinterpret_cast<double*>(D + y.o_rs_ascore);
   d.rs_align_index = reinterpret_cast<uint32_t*>(D + y.o_rs_aidx);
   d.rs_step_k = reinterpret_cast<int32_t*>(D + y.o_rs_stepk);
-  d.rs_xyz = reinterpret_cast<double*>(D + y.o_rs_xyz);
-  d.rs_dih = reinterpret_cast<double*>(D + y.o_rs_dih);
   d.best_score = reinterpret_cast<double*>(D + y.o_best);
   d.best_restart = reinterpret_cast<uint32_t*>(D + y.o_brs);
   d.final_xyz = reinterpret_cast<double*>(D + y.o_fxyz);

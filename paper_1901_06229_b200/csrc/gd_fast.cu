@@ -28,7 +28,6 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr float kMagic = 8388608.0f;  // 2^23: RZ-add leaves floor(g) in the mantissa
 constexpr int KTOP = 4;               // per-lane top coarse alignment candidates kept
-constexpr double kTwoPiD = 2.0 * 3.14159265358979323846;
 
 #ifndef GD_ALIGN_UNROLL
 #define GD_ALIGN_UNROLL 1
@@ -829,7 +828,6 @@ __global__ void __launch_bounds__(NT, 1)
     it.n = it.m.n;
     it.W = (it.n + 31) >> 5;
     const uint32_t n = it.n, R = it.m.nr;
-    double* gpose = b.rs_xyz + (size_t(it.m.atom_base) * N + size_t(it.rs) * n) * 3;
 
     // ------------------------------------------------ starting pose (docking.cpp:52-69), FP64
     Pose<NS> P;
@@ -854,16 +852,16 @@ __global__ void __launch_bounds__(NT, 1)
       for (int s = 0; s < NS; ++s) set_own(P, s, vadd(qapply(qs, vsub(own(P, s), c0)), tgt));
     }
     const V3d cen = centroid_smem<NS>(P, n, SCR3, lane);  // best_rotation_in_range's centroid (docking.cpp:76)
-    // FP64 start pose to global (read back by the full FP64 alignment); the ligand extent about the
-    // centroid sets the position error bound of the FP32 sweep below.
+    // FP64 start pose to the warp's X slot (read by the full FP64 alignment); the ligand extent
+    // about the centroid sets the position error bound of the FP32 sweep below.
     float ext = 0.f;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const uint32_t a = lane + 32 * s;
       if (a < n) {
-        gpose[3 * a] = P.x[s];
-        gpose[3 * a + 1] = P.y[s];
-        gpose[3 * a + 2] = P.z[s];
+        X[3 * a] = P.x[s];
+        X[3 * a + 1] = P.y[s];
+        X[3 * a + 2] = P.z[s];
         const V3d v = vsub(own(P, s), cen);
         ext = fmaxf(ext, float(__dsqrt_rn(vdot(v, v))));
       }
@@ -889,7 +887,7 @@ __global__ void __launch_bounds__(NT, 1)
       ++st_afall;
       for (uint32_t g = lane; g < pr.G; g += 32) {
         const double4 gq = pr.grid[g];
-        const double s = exact_rotation_score(pk, gpose, n, cen, Qd{gq.x, gq.y, gq.z, gq.w});
+        const double s = exact_rotation_score(pk, X, n, cen, Qd{gq.x, gq.y, gq.z, gq.w});
         if (best_g == 0xffffffffu || s > best_s) {  // g ascending within a lane: first max wins
           best_s = s;
           best_g = g;
@@ -945,8 +943,7 @@ __global__ void __launch_bounds__(NT, 1)
       b.rs_align_index[item] = best_g;
       b.rs_align_score[item] = best_s;
     }
-    double* dih = b.rs_dih + size_t(it.m.rot_base) * N + size_t(it.rs) * R;
-    for (uint32_t r = lane; r < R; r += 32) dih[r] = b.dih0[it.m.rot_base + r];
+    // (the final pose and dihedrals are replayed by K2 from the decision trace)
 
     // ------------------------------------------------ dihedral sweep (docking.cpp:155-167, 197-215)
     if (R > 0 && pr.reps > 0 && pr.S > 0) {
@@ -1448,11 +1445,6 @@ __global__ void __launch_bounds__(NT, 1)
                   X[3 * a + 2] = v.z;
                 }
               __syncwarp();
-              if (lane == 0) {  // molecule.cpp:170-172
-                double d = fmod(__dadd_rn(dih[r], dt.z), kTwoPiD);
-                if (d < 0.0) d = __dadd_rn(d, kTwoPiD);
-                dih[r] = d;
-              }
               refresh(false, mo);
             }
           }
@@ -1463,17 +1455,8 @@ __global__ void __launch_bounds__(NT, 1)
     }
     if (*(volatile int*)b.error != 0) break;
     GD_T(7);
-    // ------------------------------------------------ restart result
+    // ------------------------------------------------ restart result (K2 replays its pose)
     if (lane == 0) b.rs_score[item] = score;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const uint32_t a = lane + 32 * s;
-      if (a < n) {
-        gpose[3 * a] = X[3 * a];
-        gpose[3 * a + 1] = X[3 * a + 1];
-        gpose[3 * a + 2] = X[3 * a + 2];
-      }
-    }
     __syncwarp();
   }
   if (lane == 0) {

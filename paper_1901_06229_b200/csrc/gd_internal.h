@@ -85,8 +85,6 @@ struct DevBatch {
   double* rs_align_score;
   uint32_t* rs_align_index;
   int32_t* rs_step_k;      // rot_base*N*reps + (restart*reps + rep)*R + r
-  double* rs_xyz;          // (atom_base*N + restart*n + a)*3
-  double* rs_dih;          // rot_base*N + restart*R + r
   // per-ligand results
   double* best_score;
   uint32_t* best_restart;

@@ -127,9 +127,7 @@ __global__ void __launch_bounds__(1024, 1)
       b.rs_align_index[item] = best_g;
       b.rs_align_score[item] = best_s;
     }
-    double* dih = b.rs_dih + size_t(m.rot_base) * N + size_t(rs) * R;
-    for (uint32_t r = lane; r < R; r += 32) dih[r] = b.dih0[m.rot_base + r];
-    __syncwarp();
+    // (the final pose and dihedrals are replayed by K2 from the decision trace)
 
     // ---- dihedral sweep: num_repetitions x optimize_pass (docking.cpp:155-167, 197-215)
     bool failed = false;
@@ -201,11 +199,6 @@ __global__ void __launch_bounds__(1024, 1)
               const bool mv = ((__ldg(mm + (a >> 5)) >> (a & 31)) & 1u) && a != ij.y;
               if (mv) st3(P, a, rotated_about(ld3(P, a), pi, q));
             }
-            if (lane == 0) {  // molecule.cpp:170-172
-              double d = fmod(__dadd_rn(dih[r], dt.z), 2.0 * 3.14159265358979323846);
-              if (d < 0.0) d = __dadd_rn(d, 2.0 * 3.14159265358979323846);
-              dih[r] = d;
-            }
           }
           score = bs;
         }
@@ -219,22 +212,28 @@ __global__ void __launch_bounds__(1024, 1)
     if (failed) break;
     // ---- restart result
     if (lane == 0) b.rs_score[item] = score;
-    double* out = b.rs_xyz + (size_t(m.atom_base) * N + size_t(rs) * n) * 3;
-    for (uint32_t a = lane; a < 3 * n; a += 32) out[a] = P[a];
     if (lane == 0) atomicAdd(b.stats + 0, 1ull);
     __syncwarp();
   }
 }
 
 // --------------------------------------------------------------------------------------------
-// K2: best restart per ligand (finish_dock, docking.cpp:208-225).
+// K2: best restart per ligand (finish_dock, docking.cpp:208-225), then its final pose and
+// dihedrals REPLAYED in FP64 from the decision trace instead of stored per restart: start pose
+// (docking.cpp:52-69) -> the chosen grid rotation (apply_rotation_choice, :110-118) -> every
+// committed k != 0 in order (rotate_fragment, molecule.cpp:145-174). The operations are K1's, in
+// K1's order, so the bits are K1's; no per-restart pose or dihedral scratch exists. Warp per
+// ligand, the pose in the warp's shared slot (3 max_n doubles).
 // --------------------------------------------------------------------------------------------
 __global__ void finalize_kernel(DevParams pr, DevBatch b) {
+  extern __shared__ double k2_smem[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lig = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (lig >= b.n_lig) return;
+  double* P = k2_smem + size_t(threadIdx.x >> 5) * 3 * b.max_n;
   const uint32_t N = pr.n_restarts;
   const LigMeta m = b.meta[lig];
+  const uint32_t n = m.n, R = m.nr, W = (n + 31) / 32;
   double best = 0.0;
   uint32_t id = 0;
   for (uint32_t p = 0; p < N; ++p) {  // strict >: lowest restart id on ties
@@ -249,11 +248,57 @@ __global__ void finalize_kernel(DevParams pr, DevBatch b) {
     b.best_restart[lig] = id;
   }
   if (N == 0) return;
-  const double* src = b.rs_xyz + (size_t(m.atom_base) * N + size_t(id) * m.n) * 3;
+  const size_t item = size_t(lig) * N + id;
+  for (uint32_t a = lane; a < n; a += 32) {
+    const double4 at = b.atoms[m.atom_base + a];
+    st3(P, a, V3d{at.x, at.y, at.z});
+  }
+  __syncwarp();
+  {  // generate_starting_pose (docking.cpp:52-69)
+    const V3d c0 = centroid_smem(P, n);
+    const double4 q4 = b.start[2 * item], t4 = b.start[2 * item + 1];
+    const Qd qs{q4.x, q4.y, q4.z, q4.w};
+    const V3d tgt{t4.x, t4.y, t4.z};
+    __syncwarp();
+    for (uint32_t a = lane; a < n; a += 32) st3(P, a, vadd(qapply(qs, vsub(ld3(P, a), c0)), tgt));
+    __syncwarp();
+  }
+  {  // apply_rotation_choice (docking.cpp:110-118) of the restart's alignment decision
+    const V3d cen = centroid_smem(P, n);
+    const double4 gq = pr.grid[b.rs_align_index[item]];
+    const Qd q{gq.x, gq.y, gq.z, gq.w};
+    __syncwarp();
+    for (uint32_t a = lane; a < n; a += 32) st3(P, a, rotated_about(ld3(P, a), cen, q));
+    __syncwarp();
+  }
+  for (uint32_t r = lane; r < R; r += 32) b.final_dih[m.rot_base + r] = b.dih0[m.rot_base + r];
+  __syncwarp();
+  const int32_t* trace = b.rs_step_k + size_t(m.rot_base) * N * pr.reps + size_t(id) * pr.reps * R;
+  for (uint32_t st = 0; st < pr.reps * R; ++st) {
+    const int32_t k = trace[st];
+    if (k <= 0) continue;
+    const uint32_t r = st % R;
+    const uint2 ij = b.rots[m.rot_base + r];
+    const uint32_t* mm = b.masks + m.mask_base + r * W;
+    const V3d pi = ld3(P, ij.x);
+    const V3d delta = vsub(ld3(P, ij.y), pi);
+    const V3d axis = vscale(__ddiv_rn(1.0, __dsqrt_rn(vdot(delta, delta))), delta);
+    const double4 dt = pr.dtab[k];
+    const Qd q{dt.x, __dmul_rn(axis.x, dt.y), __dmul_rn(axis.y, dt.y), __dmul_rn(axis.z, dt.y)};
+    __syncwarp();
+    for (uint32_t a = lane; a < n; a += 32) {
+      const bool mv = ((__ldg(mm + (a >> 5)) >> (a & 31)) & 1u) && a != ij.y;
+      if (mv) st3(P, a, rotated_about(ld3(P, a), pi, q));
+    }
+    if (lane == 0) {  // molecule.cpp:170-172
+      double d = fmod(__dadd_rn(b.final_dih[m.rot_base + r], dt.z), 2.0 * 3.14159265358979323846);
+      if (d < 0.0) d = __dadd_rn(d, 2.0 * 3.14159265358979323846);
+      b.final_dih[m.rot_base + r] = d;
+    }
+    __syncwarp();
+  }
   double* dst = b.final_xyz + size_t(m.atom_base) * 3;
-  for (uint32_t a = lane; a < 3u * m.n; a += 32) dst[a] = src[a];
-  const double* sd = b.rs_dih + size_t(m.rot_base) * N + size_t(id) * m.nr;
-  for (uint32_t r = lane; r < m.nr; r += 32) b.final_dih[m.rot_base + r] = sd[r];
+  for (uint32_t a = lane; a < 3u * n; a += 32) dst[a] = P[a];
 }
 
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
@@ -295,9 +340,10 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
   }
   if (ev && (e = cudaEventRecord(ev[2], stream)) != cudaSuccess) return e;
   if (b.n_lig > 0) {
-    const uint32_t threads = 256;
+    const uint32_t threads = 128;  // 4 warps, one ligand each, 3 max_n doubles of pose per warp
     const uint32_t blocks = (b.n_lig * 32 + threads - 1) / threads;
-    finalize_kernel<<<blocks, threads, 0, stream>>>(pr, b);
+    const size_t smem = size_t(threads / 32) * 3 * b.max_n * sizeof(double);
+    finalize_kernel<<<blocks, threads, smem, stream>>>(pr, b);
     ++*launches;
   }
   if (ev && (e = cudaEventRecord(ev[3], stream)) != cudaSuccess) return e;
