@@ -643,6 +643,50 @@ class Context:
         self._check(self._lib.gd_last_stats(self._h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in s._fields_ if k != "reserved"}
 
+    def profile(self, lib: Library, pocket: Pocket = None, params: DockParams = None) -> dict:
+        """The reference's `profile` subcommand (geodock_main.cpp:189-232) for the GPU path: the
+        DockStats counters (docking.hpp:46-55, the closed forms the reference records: score calls
+        N G + N reps R S, bump checks N reps R S, fragment rotations N reps R (S - 1)) and the
+        align / optimize time split, here the device time of K1a (alignment) and K1b (exact
+        refinement + dihedral sweep), plus the two-stage search's own counters."""
+        if pocket is not None:
+            self.set_pocket(pocket)
+        if params is not None:
+            self.set_params(params)
+        p = self.params
+        b = self.stage(lib)
+        try:
+            b.run()
+            self.sync()
+            ms = self.kernel_ms()
+            st = self.stats()
+        finally:
+            b.free()
+        N, reps, S = p.n_restarts, p.num_repetitions, p.dihedral_steps
+        G = int(np.prod(p.rotation_steps))
+        R = int(lib.rot_off[-1] - lib.rot_off[0]) if lib.n_ligands else 0
+        t_a, t_o = ms["k1a_align"], ms["k1b_sweep"]
+        tot = t_a + t_o
+        return {"align_ligand": {"time_pct": 100.0 * t_a / tot if tot else 0.0, "visits": N * lib.n_ligands},
+                "optimize_pose": {"time_pct": 100.0 * t_o / tot if tot else 0.0, "visits": N * reps * lib.n_ligands},
+                "score_pose[align]": N * G * lib.n_ligands, "score_pose[optimize]": N * reps * R * S,
+                "bump_check": N * reps * R * S, "rotate_fragment": N * reps * R * (S - 1),
+                "total_score_calls": N * G * lib.n_ligands + N * reps * R * S,
+                "expected_score_calls": sum(count_score_calls(p, int(lib.rot_off[i + 1] - lib.rot_off[i]))
+                                            for i in range(lib.n_ligands)),
+                "device_ms": ms, "kernel_stats": st}
+
+    @staticmethod
+    def format_profile(prof: dict) -> str:
+        """The reference's profile table text (geodock_main.cpp:215-229)."""
+        lines = ["function time_pct visits",
+                 f"align_ligand {prof['align_ligand']['time_pct']:.2f} {prof['align_ligand']['visits']}",
+                 f"optimize_pose {prof['optimize_pose']['time_pct']:.2f} {prof['optimize_pose']['visits']}"]
+        for k in ("score_pose[align]", "score_pose[optimize]", "bump_check", "rotate_fragment",
+                  "total_score_calls", "expected_score_calls"):
+            lines.append(f"{k} - {prof[k]}")
+        return "\n".join(lines) + "\n"
+
     def kernel_ms(self) -> dict:
         """Device time of the last gd_run's kernels (CUDA events on the context stream)."""
         ms = (C.c_float * 3)()

@@ -75,3 +75,18 @@ def test_executor_reports_first_invalid_ligand_in_a_late_chunk(pair):
     # the context recovers
     out = fast.dock(lib.slice(0, 300), gd.make_pocket(), gd.DockParams(n_restarts=2))
     assert out.best_score.shape == (300,)
+
+
+def test_profile_table_matches_reference_counters(pair, reference=None):
+    """The profile subcommand's counters (geodock_main.cpp:189-232): DockStats closed forms."""
+    fast, _ = pair
+    lib = gd.make_library(gd.LibrarySpec(20, 32, 4, 0))
+    p = gd.DockParams(n_restarts=8)
+    prof = fast.profile(lib, gd.make_pocket(), p)
+    G, R = 16 * 16 * 8, int(lib.rot_off[-1])
+    assert prof["score_pose[align]"] == 8 * G * 20 and prof["score_pose[optimize]"] == 8 * 3 * R * 36
+    assert prof["bump_check"] == 8 * 3 * R * 36 and prof["rotate_fragment"] == 8 * 3 * R * 35
+    assert prof["total_score_calls"] == prof["expected_score_calls"]
+    assert abs(prof["align_ligand"]["time_pct"] + prof["optimize_pose"]["time_pct"] - 100.0) < 1e-6
+    text = gd.Context.format_profile(prof)
+    assert text.splitlines()[0] == "function time_pct visits" and "expected_score_calls" in text
