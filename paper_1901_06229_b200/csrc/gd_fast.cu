@@ -1221,9 +1221,12 @@ __global__ void __launch_bounds__(NT, 1)
             // per-warp list PL as (alpha, beta, gamma), which every candidate lane folds with two
             // FFMAs per pair (pairs with atom_j are invariant, see above). The list is folded
             // whenever the next moved atom's pairs might not fit.
+            // With an invariant clash every candidate fails bump_check on that pair, where the
+            // reference's bump_check returns (scoring.cpp:47-60 stops at the first clashing pair):
+            // the cross pairs are not needed, only the candidates' scores (score_pose) are.
             float mmin0 = 1e30f, mmin1 = 1e30f;  // this lane's pass-0 candidate / pass-1 share
-            float tau_a;                           // tau plus the FP32 error of the algebraic form
-            {
+            float tau_a = 0.f;                     // tau plus the FP32 error of the algebraic form
+            if (!inv) {
               float hq[NS], rq[NS], tq[NS], wx_[NS], wy_[NS], wz_[NS];
               float d2 = 0.f;
 #pragma unroll
