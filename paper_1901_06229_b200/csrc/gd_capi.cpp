@@ -50,6 +50,7 @@ struct gd_ctx {
   uint4* d_cells = nullptr;
   float q_eps = 0.f;
   float max_step = 0.f;
+  float dz_bias = 3.f;
 
   // params
   gd_params params{};
@@ -307,6 +308,7 @@ DevPocket dev_pocket(const gd_ctx* ctx) {
   pk.q_eps = ctx->q_eps;
   pk.max_step = ctx->max_step;
   pk.coarse_scale = 1.0f;
+  pk.dz_bias = ctx->dz_bias;
   return pk;
 }
 
@@ -459,32 +461,79 @@ int gd_set_pocket(gd_ctx* ctx, const uint32_t dims[3], const double origin[3], d
   GD_CUDA(ctx, cudaMalloc(&ctx->d_field, nv * sizeof(double)));
   GD_CUDA(ctx, cudaMemcpy(ctx->d_field, field, nv * sizeof(double), cudaMemcpyHostToDevice));
 
-  // Coarse-path cells: for every grid cell (ix,iy,iz) < dims-1, its four x-edges
-  // (y, z in {0,1}) as a base value c = v(x) and a difference d = v(x+1) - v(x), one 32-bit word
-  // each: low half 0x8000 | uc with uc = round(32768 c) (a byte permute makes it the float
-  // C = 1 + uc/32768), high half ud = round(16384 (d + 1)) (the float D = 2 + ud/16384 = 3 + d').
-  // Then fma(fx, D, C) = (c' + fx d') + (1 + 3 fx): every x-lerp is one FFMA carrying the same
-  // bias, which cancels in the y- and z-lerps and is subtracted once. Word order: (y,z) = (0,0),
-  // (1,0), (0,1), (1,1). One extra dummy cell (c' = d' = 0) at index cx*cy*cz evaluates to exactly
-  // 0 for any fractions: samples outside the grid read it.
+  // Coarse-path cells: for every grid cell (ix,iy,iz) < dims-1 and each of its two
+  // y-edges j, the bilinear form in (fx, fz) of the face's corners v(x+a, y+j, z+b):
+  //   v = C0 + fz dC + fx (D0 + fz dD),
+  // quantised with error feedback (each field absorbs the rounding of the ones before it, so every
+  // corner is within half a step of its own field), two words per edge:
+  //   word 2j   = (0x8000 | round(32768 C0)) | round(16384 (1 - dC)) << 16
+  //   word 2j+1 = round(16384 (1 + D0))      | dD field << 16
+  // with the dD field round(16384 (1 - dD)) (B = 3) or 0x8000 | round(8192 (2 - dD)) (B = 6, when a
+  // second difference leaves (-1, 1]). The kernel's byte permutes decode 1 + C0, dC - 3, 3 + D0 and
+  // dD - B (cell_lerp_b). One extra dummy cell (all fields zero) at index cx*cy*cz evaluates to ~0
+  // for any fractions: samples outside the grid read it.
   const uint32_t cx = dims[0] - 1, cy = dims[1] - 1, cz = dims[2] - 1;
   std::vector<uint4> cells(size_t(cx) * cy * cz + 1);
   double max_step = 0.0;  // largest |v(i+1) - v(i)| along any axis: Lipschitz bound per cell
-  double q_err = 0.0;     // largest |c' - c| + |d' - d| over all x-edges: quantisation bound
+  double q_err = 0.0;     // largest |decoded - v| over all face corners: quantisation bound
   auto at = [&](uint32_t x, uint32_t y, uint32_t z) { return field[(size_t(z) * dims[1] + y) * dims[0] + x]; };
   auto clamp01 = [](double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); };
-  auto edge = [&](uint32_t x, uint32_t y, uint32_t z) -> uint32_t {
-    const double c = clamp01(at(x, y, z)), d = clamp01(at(x + 1, y, z)) - c;
-    const long uc = std::min(32767L, std::lround(c * 32768.0));
-    const long ud = std::min(32767L, std::max(0L, std::lround((d + 1.0) * 16384.0)));
-    q_err = std::max(q_err, std::fabs(double(uc) / 32768.0 - c) + std::fabs((double(ud) / 16384.0 - 1.0) - d));
-    return (0x8000u | uint32_t(uc)) | (uint32_t(ud) << 16);
+  auto q15 = [](double v) { return std::min(32767L, std::max(0L, std::lround(v))); };
+  struct Face {
+    long uc, udc, ud0;
+    double c0, dc, d0, rest;  // quantised C0, dC, D0; the second difference dD still to quantise
+    double v[4];              // corners (fx, fz) = (0,0), (1,0), (0,1), (1,1)
+  };
+  auto face = [&](uint32_t x, uint32_t y, uint32_t z) -> Face {
+    Face f{};
+    f.v[0] = clamp01(at(x, y, z));
+    f.v[1] = clamp01(at(x + 1, y, z));
+    f.v[2] = clamp01(at(x, y, z + 1));
+    f.v[3] = clamp01(at(x + 1, y, z + 1));
+    f.uc = q15(f.v[0] * 32768.0);
+    f.c0 = double(f.uc) / 32768.0;
+    f.ud0 = q15((1.0 + (f.v[1] - f.c0)) * 16384.0);
+    f.d0 = double(f.ud0) / 16384.0 - 1.0;
+    f.udc = q15((1.0 - (f.v[2] - f.c0)) * 16384.0);
+    f.dc = 1.0 - double(f.udc) / 16384.0;
+    f.rest = f.v[3] - f.c0 - f.d0 - f.dc;
+    return f;
+  };
+  // pass 1: the dD range decides B
+  bool wide = false;
+  for (uint32_t z = 0; z < cz && !wide; ++z)
+    for (uint32_t y = 0; y < dims[1] && !wide; ++y)
+      for (uint32_t x = 0; x < cx; ++x) {
+        const double r = face(x, y, z).rest;
+        if (!(r > -0.99 && r <= 0.99)) {
+          wide = true;
+          break;
+        }
+      }
+  auto words = [&](uint32_t x, uint32_t y, uint32_t z, uint32_t& w0, uint32_t& w1) {
+    const Face f = face(x, y, z);
+    long udd;
+    double dd;
+    if (!wide) {
+      udd = q15((1.0 - f.rest) * 16384.0);
+      dd = 1.0 - double(udd) / 16384.0;
+    } else {
+      udd = q15((2.0 - f.rest) * 8192.0);
+      dd = 2.0 - double(udd) / 8192.0;
+      udd |= 0x8000L;
+    }
+    const double got[4] = {f.c0, f.c0 + f.d0, f.c0 + f.dc, f.c0 + f.d0 + f.dc + dd};
+    for (int c = 0; c < 4; ++c) q_err = std::max(q_err, std::fabs(got[c] - f.v[c]));
+    w0 = (0x8000u | uint32_t(f.uc)) | (uint32_t(f.udc) << 16);
+    w1 = uint32_t(f.ud0) | (uint32_t(udd) << 16);
   };
   for (uint32_t z = 0; z < cz; ++z)
     for (uint32_t y = 0; y < cy; ++y)
       for (uint32_t x = 0; x < cx; ++x) {
-        cells[(size_t(z) * cy + y) * cx + x] =
-            make_uint4(edge(x, y, z), edge(x, y + 1, z), edge(x, y, z + 1), edge(x, y + 1, z + 1));
+        uint4 w;
+        words(x, y, z, w.x, w.y);
+        words(x, y + 1, z, w.z, w.w);
+        cells[(size_t(z) * cy + y) * cx + x] = w;
         for (int c = 0; c < 8; ++c) {
           const double v0 = at(x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1));
           if (!(c & 1)) max_step = std::max(max_step, std::fabs(at(x + 1, y + ((c >> 1) & 1), z + ((c >> 2) & 1)) - v0));
@@ -492,16 +541,19 @@ int gd_set_pocket(gd_ctx* ctx, const uint32_t dims[3], const double origin[3], d
           if (!(c & 4)) max_step = std::max(max_step, std::fabs(at(x + (c & 1), y + ((c >> 1) & 1), z + 1) - v0));
         }
       }
-  const uint32_t dummy_half_c = 0x8000u, dummy_half_d = 16384u;  // c' = 0, d' = 0
-  const uint32_t dw = dummy_half_c | (dummy_half_d << 16);
-  cells.back() = make_uint4(dw, dw, dw, dw);
+  {  // dummy: C0 = dC = D0 = dD = 0
+    const uint32_t w0 = 0x8000u | (16384u << 16);
+    const uint32_t w1 = 16384u | ((wide ? (0x8000u | 16384u) : 16384u) << 16);
+    cells.back() = make_uint4(w0, w1, w0, w1);
+  }
+  ctx->dz_bias = wide ? 6.0f : 3.0f;
   bool in_range = true;
   for (size_t i = 0; i < nv; ++i) in_range &= (field[i] >= 0.0 && field[i] <= 1.0);
   GD_CUDA(ctx, cudaMalloc(&ctx->d_cells, cells.size() * sizeof(uint4)));
   GD_CUDA(ctx, cudaMemcpy(ctx->d_cells, cells.data(), cells.size() * sizeof(uint4), cudaMemcpyHostToDevice));
-  // Coarse error model: quantisation q_err per sample (the y- and z-lerps are
-  // convex combinations of x-edges); the kernel adds 3 * max_step * (its FP32 position bound). A
-  // field outside [0,1] breaks the quantiser, so the fast path is disabled for it (q_eps = inf ->
+  // Coarse error model: quantisation q_err per sample (each face's decoded form
+  // is the bilinear interpolant of its decoded corners, the y-lerp a convex combination); the
+  // kernel adds 3 * max_step * (its FP32 position bound). A field outside [0,1] breaks the quantiser, so the fast path is disabled for it (q_eps = inf ->
   // exact kernel).
   ctx->q_eps = in_range ? float(q_err * (1.0 + 1e-6)) : INFINITY;
   apply_l2_window(ctx, ctx->d_cells, cells.size() * sizeof(uint4));

@@ -71,12 +71,10 @@ struct CoarseGrid {
   float hx, hy, hz;    // half extents (dims-1)/2 in grid units
   uint32_t cx, cxy;    // cells per row / per plane
   uint32_t koff;       // 0x4B000000 * (1 + cx + cxy): removes the 2^23 exponent bits of the three floors
-  uint32_t dummy;      // index of the dummy cell (every fraction evaluates to exactly 0)
+  uint32_t dummy;      // index of the dummy cell (every fraction evaluates to ~0)
+  float nb;            // -B: the dD field's bias (gd_set_pocket)
 };
 
-// One cell: the four x-edges (C = 1 + c', D = 3 + d' by byte permutes) give fma(fx, D, C) =
-// (c' + fx d') + (1 + 3 fx); the common bias survives the y- and z-lerps unchanged and is removed
-// at the end. Returns the trilinear value of the quantised field.
 // One cell by byte address: shared (SC, a 32-bit shared-window address) or global (an offset from
 // cg.cells, read through the read-only path).
 template <bool SC>
@@ -90,20 +88,37 @@ __device__ __forceinline__ uint4 load_cell(const CoarseGrid& cg, uint32_t addr) 
   return w;
 }
 
-// Byte permutes against one constant K = 0x3F400000: C = bits 0x3F | half0 << 8 (selector 0x7104,
-// half0 carries bit 15, so C = 1 + uc/32768), D = bits 0x40 | half1 << 8 (selector 0x6324, D = 2 +
-// ud/16384). One shared constant lets every PRMT take an immediate selector.
-__device__ __forceinline__ float dec_c(uint32_t w) { return __uint_as_float(__byte_perm(w, 0x3F400000u, 0x7104)); }
-__device__ __forceinline__ float dec_d(uint32_t w) { return __uint_as_float(__byte_perm(w, 0x3F400000u, 0x6324)); }
+// One cell: per y-edge j (words 2j, 2j+1) the bilinear form in (fx, fz) of its
+// four corners, v = C0 + fz dC + fx (D0 + fz dD), as 16-bit fields that byte permutes against one
+// constant K turn into floats: 1 + C0 (selector 0x5104, the field carries bit 15), 3 + D0 (0x6104),
+// dC - 3 and dD - B (0x7324, negative; dD's field carries bit 15 when B = 6). z first:
+// c = fma(fz, dC - 3, 1 + C0), d = fma(fz, dD - B, 3 + D0), x = fma(fx, d, c) is the edge value plus
+// the bias b0 + fx k (b0 = 1 - 3 fz, k = 3 - B fz), the same for both edges: fx k is removed in the
+// y-lerp, b0 once per atom by the caller (cell_lerp_b) or here (cell_lerp). The dummy cell (all
+// fields zero) decodes to the bias itself: ~0 after the removal (within the rounding bound).
+constexpr uint32_t kDecK = 0xC0403F00u;
+__device__ __forceinline__ float dec_c0(uint32_t w) { return __uint_as_float(__byte_perm(w, kDecK, 0x5104)); }
+__device__ __forceinline__ float dec_d0(uint32_t w) { return __uint_as_float(__byte_perm(w, kDecK, 0x6104)); }
+__device__ __forceinline__ float dec_dz(uint32_t w) { return __uint_as_float(__byte_perm(w, kDecK, 0x7324)); }
 
-__device__ __forceinline__ float cell_lerp(const uint4 w, float fx, float fy, float fz) {
-  const float x00 = fmaf(fx, dec_d(w.x), dec_c(w.x));
-  const float x10 = fmaf(fx, dec_d(w.y), dec_c(w.y));
-  const float x01 = fmaf(fx, dec_d(w.z), dec_c(w.z));
-  const float x11 = fmaf(fx, dec_d(w.w), dec_c(w.w));
-  const float y0 = fmaf(fy, x10 - x00, x00);
-  const float y1 = fmaf(fy, x11 - x01, x01);
-  return fmaf(fz, y1 - y0, y0) - fmaf(fx, 3.0f, 1.0f);
+struct CellBias {
+  float k, b0;
+};
+__device__ __forceinline__ CellBias cell_bias(float fz, float nb) { return {fmaf(fz, nb, 3.0f), fmaf(fz, -3.0f, 1.0f)}; }
+
+// quantised trilinear value + b0 (k from cell_bias of the same fz)
+__device__ __forceinline__ float cell_lerp_b(const uint4 w, float fx, float fy, float fz, float k) {
+  const float c0 = fmaf(fz, dec_dz(w.x), dec_c0(w.x));
+  const float d0 = fmaf(fz, dec_dz(w.y), dec_d0(w.y));
+  const float c1 = fmaf(fz, dec_dz(w.z), dec_c0(w.z));
+  const float d1 = fmaf(fz, dec_dz(w.w), dec_d0(w.w));
+  const float x0 = fmaf(fx, d0, c0), x1 = fmaf(fx, d1, c1);
+  return fmaf(fy, x1 - x0, fmaf(fx, -k, x0));
+}
+
+__device__ __forceinline__ float cell_lerp(const uint4 w, float fx, float fy, float fz, float nb) {
+  const CellBias cb = cell_bias(fz, nb);
+  return cell_lerp_b(w, fx, fy, fz, cb.k) - cb.b0;
 }
 
 // One coarse sample at grid coordinates g: the quantised trilinear value when
@@ -117,7 +132,7 @@ __device__ __forceinline__ float coarse_sample(const CoarseGrid& cg, float gx, f
   const float rx = __fadd_rz(gx, kMagic), ry = __fadd_rz(gy, kMagic), rz = __fadd_rz(gz, kMagic);
   const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic), fz = gz - (rz - kMagic);
   const uint32_t cell = __float_as_uint(rx) + __float_as_uint(ry) * cg.cx + __float_as_uint(rz) * cg.cxy - cg.koff;
-  return cell_lerp(cg.cells[e < 0.0f ? cell : cg.dummy], fx, fy, fz);
+  return cell_lerp(cg.cells[e < 0.0f ? cell : cg.dummy], fx, fy, fz, cg.nb);
 }
 
 // coarse_sample that also tracks the smallest signed box distance (emin > ptol: clearly outside).
@@ -137,7 +152,7 @@ __device__ __forceinline__ float coarse_sample_z(const CoarseGrid& cg, float gx,
   const float rx = __fadd_rz(gx, kMagic), ry = __fadd_rz(gy, kMagic);
   const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic);
   const uint32_t cell = __float_as_uint(rx) + __float_as_uint(ry) * cg.cx + zoff;
-  return cell_lerp(cg.cells[e < 0.0f ? cell : cg.dummy], fx, fy, fz);
+  return cell_lerp(cg.cells[e < 0.0f ? cell : cg.dummy], fx, fy, fz, cg.nb);
 }
 
 // Interval form of coarse_sample for rotations with a sample near a face: a sample within ptol of
@@ -395,7 +410,8 @@ __global__ void __launch_bounds__(NT, 1)
                       pk.cell_dims[0],
                       pk.cell_dims[0] * pk.cell_dims[1],
                       0x4B000000u * (1u + pk.cell_dims[0] + pk.cell_dims[0] * pk.cell_dims[1]),
-                      n_cells};
+                      n_cells,
+                      -pk.dz_bias};
   const uint32_t N = pr.n_restarts;
   const uint64_t total = uint64_t(b.n_lig) * N;
   for (;;) {
@@ -507,9 +523,10 @@ __global__ void __launch_bounds__(NT, 1)
     const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
     const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
     const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
-    // coarse score error bound: per-sample FP32 rounding of the biased lerps (<= 1.3e-6), the
-    // accumulation of n values in [0, 1] (<= n 2^-24 after the 1/n), the final scaling
-    const float eps = eps_s + 1.3e-6f + 6e-8f * float(n) + 2e-7f;
+    // coarse score error bound: per-sample FP32 rounding of the decode and lerps (<= 3e-6, values
+    // below 8 in magnitude), the accumulation of n values carrying their bias b0 in [-2, 1] and of
+    // the b0 themselves (partial sums below 2.1 n: <= 2.5e-7 n after the 1/n), the final scaling
+    const float eps = eps_s + 3e-6f + 3e-7f * float(n) + 2e-7f;
     const float inv_n_scale = pk.coarse_scale / float(n);
 
     // ------------------------------------------------ coarse alignment sweep (all G rotations)
@@ -584,7 +601,7 @@ __global__ void __launch_bounds__(NT, 1)
           // one atom of class CLS (see above): 0 skips the box test, the face tracking and the
           // dummy select; 1 uses its frame's z term for all its samples (one face-tracking update
           // per atom, a select per sample); 2 tests every sample
-          float amz = 1e30f;
+          float amz = 1e30f, bsum = 0.f;
           auto atom = [&](uint32_t a, auto cls_tag) {
             constexpr int CLS = decltype(cls_tag)::value;
             const float4 v = A[a];
@@ -596,6 +613,8 @@ __global__ void __launch_bounds__(NT, 1)
             const float rz = __fadd_rz(gz, kMagic);
             const float fz = gz - (rz - kMagic);
             const uint32_t zoff16 = __float_as_uint(rz) * cxy16 + base16;
+            const CellBias cb = cell_bias(fz, cg.nb);
+            bsum += cb.b0;  // every sample of this atom carries it
 #pragma unroll
             for (int gi = 0; gi < kQtGroups; ++gi) {
               const float rx = fmaf(cs[gi].x, wx, -cs[gi].y * wy), ry = fmaf(cs[gi].y, wx, cs[gi].x * wy);
@@ -613,7 +632,7 @@ __global__ void __launch_bounds__(NT, 1)
                   amn[4 * gi + q] = fminf(amn[4 * gi + q], fabsf(e));
                   addr = e < 0.0f ? addr : dummy16;
                 }
-                acc[4 * gi + q] += cell_lerp(load_cell<SC>(cg, addr), fx, fy, fz);
+                acc[4 * gi + q] += cell_lerp_b(load_cell<SC>(cg, addr), fx, fy, fz, cb.k);
               }
             }
           };
@@ -622,7 +641,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll 1
           for (uint32_t a = nsafe; a < nsafe + nxy; ++a) atom(a, std::integral_constant<int, 1>{});
 #pragma unroll 1
-          for (uint32_t a = nsafe + nxy; a < npad; ++a) atom(a, std::integral_constant<int, 2>{});
+          for (uint32_t a = nsafe + nxy; a < n; ++a) atom(a, std::integral_constant<int, 2>{});
 #pragma unroll
           for (int i = 0; i < 4 * kQtGroups; ++i) amn[i] = fminf(amn[i], amz);
 #pragma unroll
@@ -630,7 +649,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const uint32_t ia = c0 + gi + q * nq;
-              const float sc = acc[4 * gi + q] * inv_n_scale;
+              const float sc = (acc[4 * gi + q] - bsum) * inv_n_scale;
               if (amn[4 * gi + q] <= ptol) {
                 amb_mask |= 1ull << (16 * m + ia);
               } else {
@@ -801,7 +820,8 @@ __global__ void __launch_bounds__(NT, 1)
                       pk.cell_dims[0],
                       pk.cell_dims[0] * pk.cell_dims[1],
                       0x4B000000u * (1u + pk.cell_dims[0] + pk.cell_dims[0] * pk.cell_dims[1]),
-                      n_cells};
+                      n_cells,
+                      -pk.dz_bias};
   const uint32_t N = pr.n_restarts;
   const uint64_t total = uint64_t(b.n_lig) * N;
   const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
@@ -1380,7 +1400,7 @@ __global__ void __launch_bounds__(NT, 1)
               // most the moved atoms' error: 2 * eps_rel with eps_rel = |M'| eps_sample / n.
               const uint32_t nm = e0 - s0 - 1;
               const float eps_rel =
-                  (float(nm) * (eps_s + 1.3e-6f) + 6e-8f * (float(nm) * float(nm) + float(n))) / float(n) + 2e-7f;
+                  (float(nm) * (eps_s + 3e-6f) + 6e-8f * (float(nm) * float(nm) + float(n))) / float(n) + 2e-7f;
               // k = 0 in the same coarse terms: fixed part + the cached coarse values of M'
               float p0 = 0.f;
               bool samb0 = false;

@@ -40,6 +40,7 @@ struct DevPocket {
   float inv_spacing_f;
   float q_eps;           // quantisation bound of one coarse sample (inf: fast path off)
   float coarse_scale;    // scale of the decoded coarse values (1 with the current encoding)
+  float dz_bias;         // B: bias of the cells' dD field (3, or 6 for second differences beyond 1)
   float max_step;        // max |v(i+1) - v(i)| along any axis: slope bound per grid unit
 };
 
