@@ -1125,6 +1125,7 @@ int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
 // (earlier chunks' results are discarded with the error, as the reference's rethrow after join
 // discards them, pipeline.cpp:262-272).
 int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
+  const double t_entry = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
   if (!ctx || !lib || !out || !out->best_score || !out->best_restart) return GD_ERR_ARGUMENT;
   if (!ctx->have_pocket) return set_err(ctx, GD_ERR_NO_POCKET, "no pocket set");
   if (!ctx->have_params) return set_err(ctx, GD_ERR_CUDA, "parameters not uploaded");
@@ -1136,10 +1137,25 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
   int rc = check_contract(ctx, lib);
   if (rc != GD_OK) return rc;
   const gd_params P = ctx->params;
-  // chunk size: ~8 chunks for large libraries, at least 256 ligands, at most kMaxChunk
-  constexpr uint32_t kMaxChunk = 4096;
-  const uint32_t chunk = std::min<uint32_t>(kMaxChunk, std::max<uint32_t>(256, (L + 7) / 8));
-  const uint32_t n_chunks = L ? (L + chunk - 1) / chunk : 0;
+  // Chunk schedule: a small first chunk so the GPU starts early, then each chunk 4x the previous
+  // (the host packs ~7x faster than the GPU docks, so packing the next chunk stays hidden behind
+  // the current one) up to kMaxChunk. Few, large launches keep the kernels' tails small.
+  // GD_CHUNK=n forces uniform chunks of n ligands (experiments).
+  constexpr uint32_t kMaxChunk = 16384;
+  std::vector<uint32_t> bounds{0};
+  {
+    uint32_t fixed = 0;
+    if (const char* e = std::getenv("GD_CHUNK")) fixed = std::max<uint32_t>(1, uint32_t(std::atoi(e)));
+    uint32_t next = fixed ? fixed : std::min<uint32_t>(1024, std::max<uint32_t>(256, L / 16));
+    uint32_t growth = 4;
+    if (const char* e = std::getenv("GD_CHUNK0")) next = std::max<uint32_t>(1, uint32_t(std::atoi(e)));
+    if (const char* e = std::getenv("GD_CHUNK_GROWTH")) growth = std::max<uint32_t>(1, uint32_t(std::atoi(e)));
+    while (bounds.back() < L) {
+      bounds.push_back(bounds.back() + std::min(next, L - bounds.back()));
+      if (!fixed) next = std::min<uint32_t>(kMaxChunk, next * growth);
+    }
+  }
+  const uint32_t n_chunks = uint32_t(bounds.size() - 1);
   rc = reset_device_status(ctx, ctx->stream);
   if (rc != GD_OK) return rc;
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1155,12 +1171,16 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
   // GD_TRACE_EXECUTOR=1: per-chunk host timings (validate, pack, wait for the slot) to stderr
   const bool trace = std::getenv("GD_TRACE_EXECUTOR") != nullptr;
   auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t_start = t_entry;
+  cudaStream_t sb = std::getenv("GD_ONE_STREAM") ? ctx->sa : ctx->sb;
+  if (trace) std::fprintf(stderr, "executor: prologue (t=%.3f)\n", now() - t_start);
   auto drain = [&](int si) -> int {
     Pending& p = pend[si];
     if (!p.busy) return GD_OK;
     const double t0 = trace ? now() : 0.0;
     GD_CUDA(ctx, cudaEventSynchronize(ctx->slot[si].done));
     if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) wait %.3f ms\n", p.l0, p.l1, now() - t0);
+    const double t1 = trace ? now() : 0.0;
     // unpack: pinned output staging -> the caller's arrays (library order)
     const unsigned char* src = static_cast<const unsigned char*>(ctx->slot[si].h_out);
     size_t at = 0;
@@ -1169,6 +1189,7 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
       at += (c.bytes + 255) & ~size_t(255);
     }
     closed_form_counts(P, lib, p.l0, p.l1, out);
+    if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) unpack %.3f ms\n", p.l0, p.l1, now() - t1);
     p.busy = false;
     return GD_OK;
   };
@@ -1177,8 +1198,10 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     auto& slot = ctx->slot[si];
     rc = drain(si);
     if (rc != GD_OK) return rc;
-    const uint32_t l0 = c * chunk, l1 = std::min(L, l0 + chunk);
+    const uint32_t l0 = bounds[c], l1 = bounds[c + 1];
+    const double tv = trace ? now() : 0.0;
     rc = validate_range(ctx, lib, l0, l1);
+    if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) validate %.3f ms (t=%.3f)\n", l0, l1, now() - tv, tv - t_start);
     if (rc != GD_OK) {
       cudaDeviceSynchronize();
       return rc;
@@ -1203,9 +1226,9 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     GD_CUDA(ctx, cudaEventRecord(slot.in, slot.stream));
     h2d += p.y.host_bytes;
     GD_CUDA(ctx, cudaStreamWaitEvent(ctx->sa, slot.in, 0));
-    rc = launch_batch(ctx, bind_batch(ctx, p.y, D), ctx->sa, nullptr, ctx->sb, slot.mid);
+    rc = launch_batch(ctx, bind_batch(ctx, p.y, D), ctx->sa, nullptr, sb, slot.mid);
     if (rc != GD_OK) return rc;
-    GD_CUDA(ctx, cudaEventRecord(slot.k, ctx->sb));
+    GD_CUDA(ctx, cudaEventRecord(slot.k, sb));
     GD_CUDA(ctx, cudaStreamWaitEvent(slot.stream, slot.k, 0));
     size_t at = 0;
     for (const OutCopy& oc : p.copies) {
@@ -1222,7 +1245,9 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     rc = drain(si);
     if (rc != GD_OK) return rc;
   }
+  if (trace) std::fprintf(stderr, "executor: drained (t=%.3f)\n", now() - t_start);
   rc = read_device_status(ctx);
+  if (trace) std::fprintf(stderr, "executor: done (t=%.3f)\n", now() - t_start);
   ctx->last.h2d_bytes = h2d;
   ctx->last.d2h_bytes = d2h;
   return rc;
