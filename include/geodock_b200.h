@@ -157,6 +157,12 @@ int gd_last_stats(gd_ctx* ctx, gd_stats* out);
 /* Device time (ms) of the last gd_run's kernels: ms[0] K1a coarse alignment, ms[1] K1b exact
  * refinement + dihedral sweep, ms[2] K2 finalize (CUDA events on the context stream). */
 int gd_last_kernel_ms(gd_ctx* ctx, float* ms, uint32_t n);
+/* Device accounting of the last gd_dock_batch (seconds), the GPU fields of RunMetrics
+ * (pipeline.hpp:43-72, replaces the lane busy/idle bookkeeping of pipeline.cpp:32-183):
+ * out[0] busy span (first chunk's K1a start to last chunk's K2 end), out[1] alignment (K1a) and
+ * out[2] optimisation (K1b + K2) as per-chunk event intervals (chunks overlap, so these may sum to
+ * more than out[0]), out[3] host time spent waiting for the GPU. */
+int gd_last_run_times(gd_ctx* ctx, double* out, uint32_t n);
 
 /* Closed-form scoring-call count, count_score_calls (docking.cpp:44-50). */
 uint64_t gd_count_score_calls(const gd_params* params, uint64_t n_rotamers);

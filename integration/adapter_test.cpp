@@ -3,11 +3,13 @@
 // (MatchesReferenceOracleBitForBit), acceptance #1/#2 (acceptance_main.cpp:78-165) and the error
 // contract. Built by integration/Makefile here; runs on a GPU box. Exit code 0 = all pass.
 #include <cstdio>
+#include <sstream>
 #include <string>
 
 #include "geodock/docking.hpp"
 #include "geodock/errors.hpp"
 #include "geodock/generate.hpp"
+#include "geodock/io.hpp"
 #include "geodock/pipeline.hpp"
 #include "geodock_gpu.hpp"
 #include "testkit/testkit.hpp"
@@ -77,6 +79,14 @@ int main() {
       std::printf("run_screening C1 x24 clash %.2f: %d mismatches; cpu %.2f s, gpu %.3f s\n", clash, mism,
                   m0.wall_seconds, m1.wall_seconds);
       CHECK(mism == 0, "run_screening bit-for-bit");
+      // RunMetrics from the device accounting, written by the reference's own write_metrics
+      CHECK(m1.device_busy_seconds.size() == 1 && m1.device_busy_seconds[0] > 0.0 &&
+                m1.align_seconds_total > 0.0 && m1.optimize_seconds_total > 0.0 &&
+                m1.worker_wait_seconds.size() == 1 && m1.ligand_count == lib.size(),
+            "run_screening RunMetrics");
+      std::ostringstream csv;
+      write_metrics(csv, m1, gpu_cfg);
+      CHECK(csv.str().rfind("workers,devices,lane_width,mode,ligands,", 0) == 0, "write_metrics of GPU metrics");
     }
   }
   // 3. error contract (errors.hpp)

@@ -1,6 +1,7 @@
 // C++ adapter: reference value types <-> the flat C-ABI (include/geodock_b200.h).
 #include "geodock_gpu.hpp"
 
+#include <array>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -107,7 +108,7 @@ Device& device(int d) {
 }
 
 void dock_on(int d, const std::vector<const Ligand*>& ligs, const Pocket& pocket, const DockParams& params,
-             DockResult* out) {
+             DockResult* out, double* times = nullptr) {
   Flat flat(ligs);
   Device& dev = device(d);
   std::lock_guard<std::mutex> lk(dev.mu);
@@ -129,6 +130,7 @@ void dock_on(int d, const std::vector<const Ligand*>& ligs, const Pocket& pocket
   res.final_dihedrals = fdih.data();
   if (rc == GD_OK) rc = gd_dock_batch(dev.ctx, &flat.lib, &res);
   if (rc != GD_OK) raise(rc, dev.ctx, flat);
+  if (times) gd_last_run_times(dev.ctx, times, 4);  // busy, align, optimize, host wait
   for (std::size_t l = 0; l < L; ++l) {
     DockResult& r = out[l];
     r.ligand_name = ligs[l]->name;
@@ -168,6 +170,8 @@ std::pair<std::vector<DockResult>, RunMetrics> run_screening(const std::vector<L
   RunMetrics metrics;
   metrics.ligand_count = library.size();
   metrics.device_busy_seconds.assign(n_dev, 0.0);
+  metrics.worker_wait_seconds.assign(n_dev, 0.0);
+  std::vector<std::array<double, 4>> times(n_dev, std::array<double, 4>{0, 0, 0, 0});
   std::vector<std::exception_ptr> errors(n_dev);
   const auto t0 = std::chrono::steady_clock::now();
   {
@@ -178,13 +182,11 @@ std::pair<std::vector<DockResult>, RunMetrics> run_screening(const std::vector<L
         if (lo == hi) return;
         std::vector<const Ligand*> part;
         for (std::size_t i = lo; i < hi; ++i) part.push_back(&library[i]);
-        const auto s = std::chrono::steady_clock::now();
         try {
-          dock_on(int(d), part, pocket, params, results.data() + lo);
+          dock_on(int(d), part, pocket, params, results.data() + lo, times[d].data());
         } catch (...) {
           errors[d] = std::current_exception();
         }
-        metrics.device_busy_seconds[d] = std::chrono::duration<double>(std::chrono::steady_clock::now() - s).count();
       });
     }
     for (auto& t : threads) t.join();
@@ -193,7 +195,15 @@ std::pair<std::vector<DockResult>, RunMetrics> run_screening(const std::vector<L
     if (e) std::rethrow_exception(e);  // first failing shard, like pipeline.cpp:272
   metrics.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   metrics.throughput = metrics.wall_seconds > 0 ? double(library.size()) / metrics.wall_seconds : 0.0;
-  for (double b : metrics.device_busy_seconds) metrics.device_idle_seconds.push_back(metrics.wall_seconds - b);
+  // RunMetrics from the device accounting (gd_last_run_times): busy = device span, idle = wall -
+  // busy, wait = host time blocked on the GPU, align / optimize = K1a / K1b + K2 device time
+  for (unsigned d = 0; d < n_dev; ++d) {
+    metrics.device_busy_seconds[d] = times[d][0];
+    metrics.device_idle_seconds.push_back(metrics.wall_seconds - times[d][0]);
+    metrics.align_seconds_total += times[d][1];
+    metrics.optimize_seconds_total += times[d][2];
+    metrics.worker_wait_seconds[d] = times[d][3];
+  }
   return {std::move(results), std::move(metrics)};
 }
 

@@ -228,6 +228,24 @@ class Oracle:
         f(*args, buf, n)
         return buf.raw[:n]
 
+    def write_metrics(self, m, cfg) -> bytes:
+        """write_metrics (io.cpp:225-245) of a RunMetrics-like `m` and NodeConfig-like `cfg`."""
+        f = self._fn("write_metrics")
+        f.restype = C.c_uint64
+        f64 = C.POINTER(C.c_double)
+        arr = lambda v: np.ascontiguousarray(np.asarray(v, np.float64).reshape(-1))
+        b, i, w = arr(m.device_busy_seconds), arr(m.device_idle_seconds), arr(m.worker_wait_seconds)
+        args = [C.c_uint32(cfg.n_workers), C.c_uint32(cfg.n_devices), C.c_uint32(cfg.lane_width),
+                C.c_int(1 if cfg.mode == "synthetic" else 0), C.c_uint64(m.ligand_count),
+                C.c_double(m.wall_seconds), C.c_double(m.throughput), _ptr(b, f64), C.c_uint32(len(b)),
+                _ptr(i, f64), C.c_uint32(len(i)), _ptr(w, f64), C.c_uint32(len(w)),
+                C.c_double(m.align_seconds_total), C.c_double(m.optimize_seconds_total),
+                C.c_uint64(m.lane_failures), C.c_uint64(m.exclusivity_violations)]
+        n = f(*args, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        f(*args, buf, n)
+        return buf.raw[:n]
+
     def _check(self, rc):
         if rc != 0:
             raise OracleError(rc, self._fn("last_error")().decode(errors="replace"))

@@ -483,6 +483,36 @@ uint64_t ref_write_results(uint64_t n, const uint32_t* name_off, const char* nam
   return s.size();
 }
 
+// write_metrics (io.cpp:225-245) of a RunMetrics / NodeConfig given as flat numbers; returns the
+// length. busy/idle/wait: per-lane arrays of nb, ni, nw entries.
+uint64_t ref_write_metrics(uint32_t n_workers, uint32_t n_devices, uint32_t lane_width, int synthetic,
+                           uint64_t ligands, double wall, double throughput, const double* busy, uint32_t nb,
+                           const double* idle, uint32_t ni, const double* wait, uint32_t nw, double align_total,
+                           double optimize_total, uint64_t lane_failures, uint64_t violations, char* out,
+                           uint64_t cap) {
+  RunMetrics m;
+  m.wall_seconds = wall;
+  m.throughput = throughput;
+  m.ligand_count = ligands;
+  m.device_busy_seconds.assign(busy, busy + nb);
+  m.device_idle_seconds.assign(idle, idle + ni);
+  m.worker_wait_seconds.assign(wait, wait + nw);
+  m.align_seconds_total = align_total;
+  m.optimize_seconds_total = optimize_total;
+  m.lane_failures = lane_failures;
+  m.exclusivity_violations = violations;
+  NodeConfig c;
+  c.n_workers = n_workers;
+  c.n_devices = n_devices;
+  c.lane_width = lane_width;
+  c.mode = synthetic ? ExecMode::synthetic : ExecMode::real;
+  std::ostringstream os;
+  write_metrics(os, m, c);
+  const std::string s = os.str();
+  if (out && cap) std::memcpy(out, s.data(), std::min<uint64_t>(cap, s.size()));
+  return s.size();
+}
+
 // parse_pocket (io.cpp:162-206) of a text: 0 and the pocket (field_out gets min(cap, n) values),
 // or 8 with ref_last_error() (ParseError / RangeError text).
 int ref_parse_pocket(const char* text, uint64_t len, uint32_t dims[3], double origin[3], double* spacing,

@@ -24,7 +24,7 @@ import numpy as np
 
 __all__ = [
     "DockParams", "PocketSpec", "LibrarySpec", "Pocket", "Library", "DockResult", "DockResults",
-    "RunMetrics", "Context", "make_pocket", "make_library", "make_ligand", "dock_ligand",
+    "RunMetrics", "NodeConfig", "write_metrics", "Context", "make_pocket", "make_library", "make_ligand", "dock_ligand",
     "run_screening", "count_score_calls", "validate_ligand", "moving_set", "GeoDockError",
     "ValidationError", "ContractError", "DegenerateAxisError", "DeviceError", "ParseError", "lib_path",
     "parse_library", "load_library", "serialize_library", "format_double", "write_results",
@@ -145,6 +145,7 @@ def _load():
             "gd_stream": (vp, [vp]),
             "gd_last_stats": (C.c_int, [vp, C.POINTER(_Stats)]),
             "gd_last_kernel_ms": (C.c_int, [vp, C.POINTER(C.c_float), C.c_uint32]),
+            "gd_last_run_times": (C.c_int, [vp, C.POINTER(C.c_double), C.c_uint32]),
             "gd_count_score_calls": (C.c_uint64, [C.POINTER(_Params), C.c_uint64]),
             "gd_validate_ligand": (C.c_int, [C.POINTER(_Library), C.c_uint32, C.c_char_p, C.c_uint32]),
             "gd_moving_set": (C.c_int, [C.POINTER(_Library), C.c_uint32, C.c_uint32, _u32p, _u32p]),
@@ -360,13 +361,37 @@ class DockResults:
 
 
 @dataclass
+class NodeConfig:
+    """NodeConfig (pipeline.hpp:21-34) as a GPU run uses it: one host thread per GPU, no lanes
+    (lane_width kept for the metrics CSV), always real mode (the synthetic scheduler is out of scope)."""
+    n_workers: int = 1
+    n_devices: int = 1
+    lane_width: int = 8
+    mode: str = "real"
+
+
+@dataclass
 class RunMetrics:
-    """Subset of RunMetrics (pipeline.hpp:43-72) that a GPU run can report."""
+    """RunMetrics (pipeline.hpp:43-72) as a GPU run reports it. Per GPU: device_busy_seconds = the
+    device span of its gd_dock_batch (first K1a start to last K2 end, CUDA events),
+    device_idle_seconds = wall - busy, worker_wait_seconds = its host thread's time waiting on the
+    GPU. align/optimize_seconds_total = device time of K1a / K1b + K2 (per-chunk event intervals,
+    summed over GPUs). Offload records, claim/finish workers, lane failures and exclusivity
+    violations belong to the reference's CPU-lane scheduler (no CPU retry here): empty / 0."""
     wall_seconds: float = 0.0
     throughput: float = 0.0
     ligand_count: int = 0
     device_busy_seconds: List[float] = field(default_factory=list)
     device_idle_seconds: List[float] = field(default_factory=list)
+    worker_wait_seconds: List[float] = field(default_factory=list)
+    align_seconds_total: float = 0.0
+    optimize_seconds_total: float = 0.0
+    lane_failures: int = 0
+    exclusivity_violations: int = 0
+
+    def total_wait_seconds(self) -> float:
+        """RunMetrics::total_wait_seconds (pipeline.hpp:62-66)."""
+        return float(sum(self.worker_wait_seconds))
 
 
 # ----------------------------------------------------------------------------- host helpers
@@ -529,6 +554,20 @@ def write_results(lib: Library, res: "DockResults") -> str:
     return "".join(rows)
 
 
+def write_metrics(m: RunMetrics, config: NodeConfig) -> str:
+    """write_metrics (io.cpp:225-245): the one-row run metrics CSV."""
+    busy, idle, wait = sum(m.device_busy_seconds), sum(m.device_idle_seconds), sum(m.worker_wait_seconds)
+    mean_wait = wait / m.ligand_count if m.ligand_count > 0 else 0.0
+    return ("workers,devices,lane_width,mode,ligands,wall_seconds,throughput,"
+            "device_busy_seconds,device_idle_seconds,mean_lane_wait_seconds,"
+            "align_seconds_total,optimize_seconds_total,lane_failures,exclusivity_violations\n"
+            f"{config.n_workers},{config.n_devices},{config.lane_width},"
+            f"{'synthetic' if config.mode == 'synthetic' else 'real'},{m.ligand_count},"
+            f"{format_double(m.wall_seconds)},{format_double(m.throughput)},{format_double(busy)},"
+            f"{format_double(idle)},{format_double(mean_wait)},{format_double(m.align_seconds_total)},"
+            f"{format_double(m.optimize_seconds_total)},{m.lane_failures},{m.exclusivity_violations}\n")
+
+
 def moving_set(lib: Library, i: int, r: int) -> np.ndarray:
     """Rotamer r's moving set (finalize_ligand, molecule.cpp:88-98)."""
     L, keep = lib._c()
@@ -553,6 +592,9 @@ class Context:
                               "(there is no CPU fallback)")
         self._h = h
         self.device = device
+        # a context is externally synchronized (one batch in flight, like the reference's lane
+        # guard, pipeline.cpp:75,138); run_screening threads sharing a device take this lock
+        self.lock = threading.RLock()
         self.pocket = None
         self.params = DockParams()
         if mode is not None:
@@ -693,6 +735,12 @@ class Context:
         self._check(self._lib.gd_last_kernel_ms(self._h, ms, 3))
         return {"k1a_align": ms[0], "k1b_sweep": ms[1], "k2_finalize": ms[2]}
 
+    def run_times(self) -> dict:
+        """Device accounting of the last dock() (gd_last_run_times), seconds."""
+        t = (C.c_double * 4)()
+        self._check(self._lib.gd_last_run_times(self._h, t, 4))
+        return {"busy": t[0], "align": t[1], "optimize": t[2], "host_wait": t[3]}
+
     def sync(self):
         self._check(self._lib.gd_sync(self._h))
 
@@ -760,15 +808,17 @@ def run_screening(library: Library, pocket: Pocket, params: DockParams = DockPar
     devs = list(devices) if devices is not None else list(range(max(1, n_devices)))
     L = library.n_ligands
     bounds = [L * i // len(devs) for i in range(len(devs) + 1)]
-    parts, errors, busy = [None] * len(devs), [None] * len(devs), [0.0] * len(devs)
+    parts, errors = [None] * len(devs), [None] * len(devs)
+    times = [{"busy": 0.0, "align": 0.0, "optimize": 0.0, "host_wait": 0.0} for _ in devs]
 
     def work(i):
         try:
-            t0 = time.perf_counter()
             shard = library.slice(bounds[i], bounds[i + 1])
             if shard.n_ligands:
-                parts[i] = _ctx_for(devs[i]).dock(shard, pocket, params, trace=trace)
-            busy[i] = time.perf_counter() - t0
+                ctx = _ctx_for(devs[i])
+                with ctx.lock:
+                    parts[i] = ctx.dock(shard, pocket, params, trace=trace)
+                    times[i] = ctx.run_times()
         except BaseException as e:  # rethrown after join, like pipeline.cpp:262-272
             errors[i] = e
 
@@ -785,5 +835,8 @@ def run_screening(library: Library, pocket: Pocket, params: DockParams = DockPar
     got = [p for p in parts if p is not None]
     cat = lambda k: None if getattr(got[0], k) is None else np.concatenate([getattr(p, k) for p in got])
     res = DockResults(**{k: cat(k) for k in DockResults.__dataclass_fields__})
-    m = RunMetrics(wall, L / wall if wall > 0 else 0.0, L, busy, [wall - b for b in busy])
+    busy = [t["busy"] for t in times]
+    m = RunMetrics(wall, L / wall if wall > 0 else 0.0, L, busy, [wall - b for b in busy],
+                   [t["host_wait"] for t in times], sum(t["align"] for t in times),
+                   sum(t["optimize"] for t in times))
     return res, m

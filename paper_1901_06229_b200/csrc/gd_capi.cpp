@@ -79,10 +79,15 @@ struct gd_ctx {
     size_t d_cap = 0;
     cudaStream_t stream = nullptr;  // copies of this slot
     cudaEvent_t in = nullptr, mid = nullptr, k = nullptr, done = nullptr;  // H2D | K1a | K2 | D2H done
+    cudaEvent_t a0 = nullptr;                                             // before K1a (timing)
   } slot[kSlots];
   // executor compute streams: all chunks' K1a in order on sa, their K1b + K2 on sb (so chunk c+1's
   // alignment overlaps chunk c's sweep, and chunks complete in order)
   cudaStream_t sa = nullptr, sb = nullptr;
+  // last gd_dock_batch's device accounting (RunMetrics, pipeline.hpp:43-72): busy span (first K1a
+  // start to last K2 end), per-chunk K1a and K1b + K2 event intervals, host time waiting on the GPU
+  cudaEvent_t run0 = nullptr, run1 = nullptr;
+  double run_times[4] = {0, 0, 0, 0};
 };
 
 struct Layout {
@@ -374,9 +379,13 @@ int gd_create(int device, gd_ctx** out) {
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
   for (int i = 0; i < kSlots && e == cudaSuccess; ++i) {
     e = cudaStreamCreateWithFlags(&ctx->slot[i].stream, cudaStreamNonBlocking);
-    for (cudaEvent_t* ev : {&ctx->slot[i].in, &ctx->slot[i].mid, &ctx->slot[i].k, &ctx->slot[i].done})
+    for (cudaEvent_t* ev : {&ctx->slot[i].in, &ctx->slot[i].done})
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    for (cudaEvent_t* ev : {&ctx->slot[i].a0, &ctx->slot[i].mid, &ctx->slot[i].k})
+      if (e == cudaSuccess) e = cudaEventCreate(ev);
   }
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->run0);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->run1);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->sa, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->sb, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
@@ -409,10 +418,12 @@ void gd_destroy(gd_ctx* ctx) {
     if (sl.h_in) cudaFreeHost(sl.h_in);
     if (sl.h_out) cudaFreeHost(sl.h_out);
     cudaFree(sl.d_arena);
-    for (cudaEvent_t ev : {sl.in, sl.mid, sl.k, sl.done})
+    for (cudaEvent_t ev : {sl.in, sl.mid, sl.k, sl.done, sl.a0})
       if (ev) cudaEventDestroy(ev);
     if (sl.stream) cudaStreamDestroy(sl.stream);
   }
+  if (ctx->run0) cudaEventDestroy(ctx->run0);
+  if (ctx->run1) cudaEventDestroy(ctx->run1);
   if (ctx->sa) cudaStreamDestroy(ctx->sa);
   if (ctx->sb) cudaStreamDestroy(ctx->sb);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1032,6 +1043,12 @@ int gd_last_kernel_ms(gd_ctx* ctx, float* ms, uint32_t n) {
   return GD_OK;
 }
 
+int gd_last_run_times(gd_ctx* ctx, double* out, uint32_t n) {
+  if (!ctx || !out) return GD_ERR_ARGUMENT;
+  for (uint32_t i = 0; i < n && i < 4; ++i) out[i] = ctx->run_times[i];
+  return GD_OK;
+}
+
 int gd_sync(gd_ctx* ctx) {
   if (!ctx) return GD_ERR_ARGUMENT;
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1174,12 +1191,22 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
   const double t_start = t_entry;
   cudaStream_t sb = std::getenv("GD_ONE_STREAM") ? ctx->sa : ctx->sb;
   if (trace) std::fprintf(stderr, "executor: prologue (t=%.3f)\n", now() - t_start);
+  double host_wait_ms = 0.0, align_ms = 0.0, opt_ms = 0.0;
   auto drain = [&](int si) -> int {
     Pending& p = pend[si];
     if (!p.busy) return GD_OK;
-    const double t0 = trace ? now() : 0.0;
+    const double tw = now();
     GD_CUDA(ctx, cudaEventSynchronize(ctx->slot[si].done));
-    if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) wait %.3f ms\n", p.l0, p.l1, now() - t0);
+    const double waited = now() - tw;
+    host_wait_ms += waited;
+    {
+      float ka = 0.f, kb = 0.f;
+      GD_CUDA(ctx, cudaEventElapsedTime(&ka, ctx->slot[si].a0, ctx->slot[si].mid));
+      GD_CUDA(ctx, cudaEventElapsedTime(&kb, ctx->slot[si].mid, ctx->slot[si].k));
+      align_ms += ka;
+      opt_ms += kb;
+    }
+    if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) wait %.3f ms\n", p.l0, p.l1, waited);
     const double t1 = trace ? now() : 0.0;
     // unpack: pinned output staging -> the caller's arrays (library order)
     const unsigned char* src = static_cast<const unsigned char*>(ctx->slot[si].h_out);
@@ -1226,9 +1253,12 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     GD_CUDA(ctx, cudaEventRecord(slot.in, slot.stream));
     h2d += p.y.host_bytes;
     GD_CUDA(ctx, cudaStreamWaitEvent(ctx->sa, slot.in, 0));
+    if (c == 0) GD_CUDA(ctx, cudaEventRecord(ctx->run0, ctx->sa));
+    GD_CUDA(ctx, cudaEventRecord(slot.a0, ctx->sa));
     rc = launch_batch(ctx, bind_batch(ctx, p.y, D), ctx->sa, nullptr, sb, slot.mid);
     if (rc != GD_OK) return rc;
     GD_CUDA(ctx, cudaEventRecord(slot.k, sb));
+    if (c + 1 == n_chunks) GD_CUDA(ctx, cudaEventRecord(ctx->run1, sb));
     GD_CUDA(ctx, cudaStreamWaitEvent(slot.stream, slot.k, 0));
     size_t at = 0;
     for (const OutCopy& oc : p.copies) {
@@ -1246,6 +1276,14 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     if (rc != GD_OK) return rc;
   }
   if (trace) std::fprintf(stderr, "executor: drained (t=%.3f)\n", now() - t_start);
+  {
+    float busy = 0.f;
+    if (n_chunks) GD_CUDA(ctx, cudaEventElapsedTime(&busy, ctx->run0, ctx->run1));
+    ctx->run_times[0] = 1e-3 * busy;
+    ctx->run_times[1] = 1e-3 * align_ms;
+    ctx->run_times[2] = 1e-3 * opt_ms;
+    ctx->run_times[3] = 1e-3 * host_wait_ms;
+  }
   rc = read_device_status(ctx);
   if (trace) std::fprintf(stderr, "executor: done (t=%.3f)\n", now() - t_start);
   ctx->last.h2d_bytes = h2d;

@@ -204,3 +204,9 @@ def test_dock_ligand_and_run_screening_api():
     assert r.score_calls == 79360 and r.final_coordinates.shape == (32, 3)
     res, m = gd.run_screening(lib, pocket, p, devices=[0, 0])
     assert res.best_score[1] == r.best_score and m.ligand_count == 6
+    # RunMetrics (pipeline.hpp:43-72) from the device accounting, and its CSV (io.cpp:225-245)
+    assert len(m.device_busy_seconds) == 2 and all(b > 0 for b in m.device_busy_seconds)
+    assert all(abs(m.wall_seconds - b - i) < 1e-12 for b, i in zip(m.device_busy_seconds, m.device_idle_seconds))
+    assert m.align_seconds_total > 0 and m.optimize_seconds_total > 0 and len(m.worker_wait_seconds) == 2
+    csv = gd.write_metrics(m, gd.NodeConfig(2, 2)).splitlines()
+    assert csv[0].startswith("workers,devices,lane_width,mode,ligands") and csv[1].startswith("2,2,8,real,6,")

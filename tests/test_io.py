@@ -156,3 +156,20 @@ def test_pocket_roundtrip_matches_reference(reference):
     q = gd.parse_pocket(text)
     ref = reference.parse_pocket(text)
     assert q.dims == ref[0] and np.asarray(q.field).tobytes() == ref[3].tobytes()
+
+
+METRICS = [
+    gd.RunMetrics(0.05215, 191754.3, 10000, [0.04811], [0.00404], [0.04305], 0.0331, 0.0149),
+    gd.RunMetrics(1.5, 666.6666666666666, 1000, [1.2, 1.25, 1.1, 0.9], [0.3, 0.25, 0.4, 0.6],
+                  [0.1, 0.2, 0.3, 0.4], 3.0, 1.7),
+    gd.RunMetrics(0.0, 0.0, 0, [], [], [], 0.0, 0.0),                       # empty run: mean wait 0
+    gd.RunMetrics(1e-9, 1e12, 3, [1e-300], [-0.0], [5e-324], 1e308, 123456789.123, 2, 7),
+]
+
+
+@pytest.mark.parametrize("i", range(len(METRICS)))
+def test_metrics_csv_matches_reference(reference, i):
+    """write_metrics (io.cpp:225-245) byte for byte."""
+    m = METRICS[i]
+    for cfg in (gd.NodeConfig(), gd.NodeConfig(4, 4, 8, "real"), gd.NodeConfig(8, 2, 16, "synthetic")):
+        assert gd.write_metrics(m, cfg).encode() == reference.write_metrics(m, cfg)
