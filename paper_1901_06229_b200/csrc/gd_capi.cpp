@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <chrono>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -130,15 +132,91 @@ int cuda_err(gd_ctx* ctx, cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_err(ctx, e_, #call); \
   } while (0)
 
+// Host worker pool for the executor's per-chunk validation and packing: hardware_concurrency - 1
+// persistent threads (the caller works too), so a chunk's host work does not pay thread start-up
+// on the critical path. One job at a time; a concurrent caller (another device's host thread)
+// falls back to spawning its own threads. Never destroyed: the workers sleep until process exit.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();
+    return *p;
+  }
+  unsigned threads() const { return unsigned(th_.size()) + 1; }
+  // false if another job is running (the caller then runs its own threads)
+  bool run(size_t n, size_t grain, const std::function<void(size_t)>& f) {
+    std::unique_lock<std::mutex> s(submit_, std::try_to_lock);
+    if (!s.owns_lock()) return false;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      n_ = n;
+      grain_ = grain;
+      chunks_ = (n + grain - 1) / grain;
+      next_.store(0);
+      pending_ = unsigned(th_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+    return true;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    for (unsigned t = 0; t + 1 < hw; ++t) {
+      th_.emplace_back([this] { loop(); });
+      th_.back().detach();
+    }
+  }
+  void work() {
+    for (;;) {
+      const size_t c = next_.fetch_add(1);
+      if (c >= chunks_) return;
+      const size_t e = std::min(n_, (c + 1) * grain_);
+      for (size_t i = c * grain_; i < e; ++i) (*job_)(i);
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      lk.unlock();
+      work();
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex submit_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(size_t)>* job_ = nullptr;
+  size_t n_ = 0, grain_ = 1, chunks_ = 0;
+  std::atomic<size_t> next_{0};
+  unsigned pending_ = 0;
+  uint64_t gen_ = 0;
+};
+
+// f(i) for i < n on all host threads, in chunks of `grain` indices (0: about 8 chunks per thread)
 template <class F>
 void parallel_for(size_t n, size_t grain, F&& f) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  HostPool& pool = HostPool::get();
+  const unsigned hw = pool.threads();
+  if (grain == 0) grain = std::max<size_t>(1, n / (8 * size_t(hw)));
   const size_t chunks = (n + grain - 1) / grain;
-  const unsigned nt = unsigned(std::min<size_t>(hw, chunks));
-  if (nt <= 1) {
+  if (hw <= 1 || chunks <= 1) {
     for (size_t i = 0; i < n; ++i) f(i);
     return;
   }
+  const std::function<void(size_t)> fn = std::ref(f);
+  if (pool.run(n, grain, fn)) return;
+  const unsigned nt = unsigned(std::min<size_t>(hw, chunks));
   std::atomic<size_t> next{0};
   std::vector<std::thread> th;
   th.reserve(nt);
@@ -658,7 +736,7 @@ Layout plan_layout(const gd_library* lib, const gd_params& P) {
 // docking.cpp:239-240; run_screening reports the first failing task, pipeline.cpp:233).
 int validate_range(gd_ctx* ctx, const gd_library* lib, uint32_t l0, uint32_t l1) {
   std::vector<uint8_t> bad(l1 - l0, 0);
-  parallel_for(l1 - l0, 256, [&](size_t i) {
+  parallel_for(l1 - l0, 0, [&](size_t i) {
     const LigView v = view_of(lib, uint32_t(l0 + i));
     bad[i] = (!validate(v).empty() || v.n > GD_MAX_ATOMS) ? 1u : 0u;
   });
@@ -704,7 +782,7 @@ void pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, uns
                         ctx->origin[1] + ctx->spacing * static_cast<double>(ctx->dims[1] - 1),
                         ctx->origin[2] + ctx->spacing * static_cast<double>(ctx->dims[2] - 1)};
   const uint32_t a0 = L ? lib->atom_off[0] : 0, r0 = L ? lib->rot_off[0] : 0;
-  parallel_for(L, 64, [&](size_t li) {
+  parallel_for(L, 0, [&](size_t li) {
     const uint32_t l = uint32_t(li);
     const LigView v = view_of(lib, l);
     const uint32_t n = v.n, W = (n + 31) / 32;

@@ -1,1 +1,5 @@
-for cfg in "625 4" "1250 8" "625 16" "1000 3" "400 6" "2000 8"; do set -- $cfg; echo "== first $1 growth $2"; GD_CHUNK0=$1 GD_CHUNK_GROWTH=$2 python tools/e2e_trace.py | tail -2; done
+echo "== C2"; python tools/e2e_trace.py | tail -2
+echo "== C4"; python tools/e2e_trace.py --ligands 1000 --atoms 120 --rotamers 32 | tail -2
+echo "== C5"; python tools/e2e_trace.py --dims 47 --spacing 0.375 | tail -2
+GD_TRACE_EXECUTOR=1 python tools/e2e_trace.py 2>&1 | tail -12
+GD_TRACE_EXECUTOR=1 python tools/e2e_trace.py --ligands 1000 --atoms 120 --rotamers 32 2>&1 | tail -12
