@@ -93,7 +93,8 @@ struct gd_ctx {
 };
 
 struct Layout {
-  uint32_t L = 0, A = 0, Rt = 0, max_n = 1;
+  uint32_t L = 0, A = 0, Rt = 0, max_n = 1, fast_max_n = 0;
+  uint32_t class_max_n[3] = {0, 0, 0};  // per fast-kernel class (n <= 32, <= 64, <= 128)
   size_t n_items = 0;
   std::vector<uint32_t> mask_base, adj_base;
   size_t o_meta, o_atoms, o_start, o_rots, o_dih0, o_masks, o_adj, o_dfs, o_rdfs, o_adjd, host_bytes;
@@ -701,6 +702,11 @@ Layout plan_layout(const gd_library* lib, const gd_params& P) {
     const uint32_t n = lib->atom_off[l + 1] - lib->atom_off[l];
     const uint32_t W = (n + 31) / 32;
     y.max_n = std::max(y.max_n, n);
+    if (n <= gdk::kFastMaxAtoms) y.fast_max_n = std::max(y.fast_max_n, n);
+    if (n <= gdk::kFastMaxAtoms) {
+      const int c = n <= 32 ? 0 : (n <= 64 ? 1 : 2);
+      y.class_max_n[c] = std::max(y.class_max_n[c], n);
+    }
     y.mask_base[l + 1] = y.mask_base[l] + (lib->rot_off[l + 1] - lib->rot_off[l]) * W;
     y.adj_base[l + 1] = y.adj_base[l] + n * W;
   }
@@ -727,7 +733,7 @@ Layout plan_layout(const gd_library* lib, const gd_params& P) {
   y.o_brs = ar.take<uint32_t>(L);
   y.o_fxyz = ar.take<double>(size_t(y.A) * 3);
   y.o_fdih = ar.take<double>(y.Rt);
-  y.o_ctr = ar.take<unsigned int>(4);
+  y.o_ctr = ar.take<unsigned int>(16);  // work counters: [0..3] exact / one-class launch, [4 c ..] class c
   y.total = ar.off + 256;
   return y;
 }
@@ -903,6 +909,9 @@ DevBatch bind_batch(const gd_ctx* ctx, const Layout& y, unsigned char* D) {
   d.n_atoms = y.A;
   d.n_rots = y.Rt;
   d.max_n = y.max_n;
+  d.fast_max_n = y.fast_max_n;
+  d.fast_min_n = 0;
+  for (int c = 0; c < 3; ++c) d.class_max_n[c] = y.class_max_n[c];
   d.meta = reinterpret_cast<const LigMeta*>(D + y.o_meta);
   d.atoms = reinterpret_cast<const double4*>(D + y.o_atoms);
   d.start = reinterpret_cast<const double4*>(D + y.o_start);

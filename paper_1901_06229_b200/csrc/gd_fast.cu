@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t lig = item / N;
     const LigMeta meta = b.meta[lig];
     const uint32_t n = meta.n;
+    if (n > 32u * NS || n <= b.fast_min_n) continue;  // another launch's ligand (mixed batch)
     // start pose (docking.cpp:52-69): R(q) (p - c0) + t; only the part relative to its centroid
     // matters here, plus the centroid itself (t + mean of the rotated offsets, in FP64)
     float px[NS], py[NS], pz[NS];
@@ -839,13 +840,14 @@ __global__ void __launch_bounds__(NT, 1)
     item = __shfl_sync(FULL, item, 0);
     if (item >= total) break;
     if (*(volatile int*)b.error != 0) break;
-    ++st_items;
-    GD_T(0);
     Item it;
     it.lig = item / N;
     it.rs = item - it.lig * N;
     it.m = b.meta[it.lig];
     it.n = it.m.n;
+    if (it.n > 32u * NS || it.n <= b.fast_min_n) continue;  // another launch's ligand (mixed batch)
+    ++st_items;
+    GD_T(0);
     it.W = (it.n + 31) >> 5;
     const uint32_t n = it.n, R = it.m.nr;
 

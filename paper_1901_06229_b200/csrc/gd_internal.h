@@ -10,7 +10,8 @@
 
 namespace gdk {
 
-constexpr int kMaxAtoms = 256;      // GD_MAX_ATOMS
+constexpr int kMaxAtoms = 256;
+constexpr uint32_t kFastMaxAtoms = 128;  // the fast kernels keep <= 128 atoms per warp in registers      // GD_MAX_ATOMS
 constexpr int kMaxWords = kMaxAtoms / 32;
 constexpr int kAlignCand = 32;      // alignment candidates handed from K1a to K1b per restart
 
@@ -68,6 +69,9 @@ struct DevBatch {
   uint32_t n_atoms;
   uint32_t n_rots;
   uint32_t max_n;
+  uint32_t fast_max_n;     // largest n <= kFastMaxAtoms (the fast kernels' ligands; 0: none)
+  uint32_t fast_min_n;     // the fast kernels of one launch take kFastClass-ligands with n > this
+  uint32_t class_max_n[3]; // largest n per fast class (n <= 32, <= 64, <= 128; 0: class absent)
   const LigMeta* meta;
   const double4* atoms;    // (x, y, z, radius)
   const double4* start;    // per (ligand, restart): [q(w,x,y,z)], [t(x,y,z), 0]  -> 2 x double4

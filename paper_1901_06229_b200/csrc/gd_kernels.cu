@@ -52,7 +52,7 @@ __device__ __forceinline__ void st3(double* P, uint32_t a, V3d v) {
 // orders. Shared memory per warp: pose P[3n], candidate C[3n], samples S[n] (doubles).
 // --------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024, 1)
-    dock_exact_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t smem_stride) {
+    dock_exact_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t smem_stride, uint32_t min_n) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(1024, 1)
     const uint32_t rs = item - lig * N;
     const LigMeta m = b.meta[lig];
     const uint32_t n = m.n, R = m.nr, W = (n + 31) >> 5;
+    if (n < min_n) continue;  // mixed batch: the fast kernels' ligand
 
     // ---- starting pose (docking.cpp:52-69); q and target come from the host packer (libm).
     for (uint32_t a = lane; a < n; a += 32) {
@@ -306,31 +307,57 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
                         cudaEvent_t mid) {
   const bool split = stream_b && mid && stream_b != stream;
   *launches = 0;
-  cudaError_t e = cudaMemsetAsync(b.work_counter, 0, 2 * sizeof(unsigned int), stream);
+  cudaError_t e = cudaMemsetAsync(b.work_counter, 0, 16 * sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
   if (ev && (e = cudaEventRecord(ev[0], stream)) != cudaSuccess) return e;
+  // the FP64 kernel over the ligands with n >= min_n, on counter `ctr`
+  auto launch_exact = [&](cudaStream_t st, uint32_t min_n, unsigned int* ctr) -> cudaError_t {
+    const uint32_t stride = 7 * b.max_n;  // doubles per warp
+    const size_t per_warp = size_t(stride) * sizeof(double);
+    int warps = int((200 * 1024) / per_warp);
+    if (warps > 32) warps = 32;
+    if (warps < 1) warps = 1;
+    const size_t smem = per_warp * warps;
+    cudaError_t r = cudaFuncSetAttribute(dock_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (r != cudaSuccess) return r;
+    DevBatch bx = b;
+    bx.work_counter = ctr;
+    dock_exact_kernel<<<n_sms, 32 * warps, smem, st>>>(pk, pr, bx, stride, min_n);
+    ++*launches;
+    return cudaGetLastError();
+  };
   if (b.n_lig > 0) {
     const int mode = pr.mode & 0xff;
-    if (mode == GD_MODE_EXACT || b.max_n > 128) {  // the fast kernels keep <= 128 atoms in registers
-      const uint32_t stride = 7 * b.max_n;  // doubles per warp
-      const size_t per_warp = size_t(stride) * sizeof(double);
-      int warps = int((200 * 1024) / per_warp);
-      if (warps > 32) warps = 32;
-      if (warps < 1) warps = 1;
-      const size_t smem = per_warp * warps;
-      e = cudaFuncSetAttribute(dock_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e != cudaSuccess) return e;
-      dock_exact_kernel<<<n_sms, 32 * warps, smem, stream>>>(pk, pr, b, stride);
-      ++*launches;
+    if (mode == GD_MODE_EXACT || b.fast_max_n == 0) {  // everything in FP64
+      if ((e = launch_exact(stream, 0u, b.work_counter)) != cudaSuccess) return e;
       if (ev && (e = cudaEventRecord(ev[1], stream)) != cudaSuccess) return e;
       if (split) {
         if ((e = cudaEventRecord(mid, stream)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(stream_b, mid, 0)) != cudaSuccess) return e;
       }
     } else {
-      e = launch_fast(pk, pr, b, n_sms, stream, split ? mid : (ev ? ev[1] : nullptr), split ? stream_b : nullptr);
-      if (e != cudaSuccess) return e;
-      *launches += 2;
+      // the fast kernels for every ligand up to kFastMaxAtoms, one K1a + K1b pair per size class
+      // present (n <= 32, <= 64, <= 128: NS = 1, 2, 4 from that class's ligands only, so a few
+      // larger ligands do not put a whole batch on the NS = 4 kernels); a mixed batch's ligands
+      // beyond 128 atoms go through the FP64 kernel after K1b, on their own counter
+      int n_cls = 0;
+      for (int c = 0; c < 3; ++c) n_cls += b.class_max_n[c] ? 1 : 0;
+      for (int c = 0, k = 0; c < 3; ++c) {
+        if (!b.class_max_n[c]) continue;
+        DevBatch bf = b;
+        bf.max_n = b.class_max_n[c];
+        bf.fast_min_n = n_cls == 1 ? 0u : (c == 0 ? 0u : (c == 1 ? 32u : 64u));
+        if (n_cls > 1) bf.work_counter = b.work_counter + 4 * (c + 1);
+        const bool last = ++k == n_cls;
+        // timing (non-split): ev[1] after the last class's K1a is the K1a / K1b boundary
+        e = launch_fast(pk, pr, bf, n_sms, stream, split ? mid : (ev && last ? ev[1] : nullptr),
+                        split ? stream_b : nullptr);
+        if (e != cudaSuccess) return e;
+        *launches += 2;
+      }
+      if (b.max_n > kFastMaxAtoms &&
+          (e = launch_exact(split ? stream_b : stream, kFastMaxAtoms + 1, b.work_counter + 2)) != cudaSuccess)
+        return e;
     }
     if (split) stream = stream_b;  // K2 follows K1b
     e = cudaGetLastError();

@@ -90,3 +90,28 @@ def test_profile_table_matches_reference_counters(pair, reference=None):
     assert abs(prof["align_ligand"]["time_pct"] + prof["optimize_pose"]["time_pct"] - 100.0) < 1e-6
     text = gd.Context.format_profile(prof)
     assert text.splitlines()[0] == "function time_pct visits" and "expected_score_calls" in text
+
+
+def _interleaved(*libs):
+    """One library whose ligands alternate between the given libraries (through the .lgd text)."""
+    parts = []
+    for i in range(max(l.n_ligands for l in libs)):
+        parts += [l.slice(i, i + 1) for l in libs if i < l.n_ligands]
+    return gd.parse_library("".join(gd.serialize_library(p) for p in parts).encode())
+
+
+@pytest.mark.parametrize("clash", [0.75, 0.2])
+def test_mixed_sizes_route_per_ligand(pair, clash):
+    """A batch mixing every size class: one fast K1a + K1b pair per class (n <= 32, <= 64, <= 128,
+    NS from that class only) and the FP64 kernel for the ligands beyond 128 atoms, in one batch."""
+    fast, exact = pair
+    lib = _interleaved(gd.make_library(gd.LibrarySpec(40, 24, 4, 1)),    # NS = 1 class
+                       gd.make_library(gd.LibrarySpec(6, 150, 6, 2)),    # FP64 kernel
+                       gd.make_library(gd.LibrarySpec(20, 70, 10, 3)),   # NS = 4 class
+                       gd.make_library(gd.LibrarySpec(30, 40, 8, 4)))    # NS = 2 class
+    pocket = gd.make_pocket()
+    p = gd.DockParams(n_restarts=8, clash_factor=clash)
+    out = fast.dock(lib, pocket, p, trace=True)
+    st = fast.stats()
+    _same(out, exact.dock(lib, pocket, p, trace=True))
+    assert st["restarts"] == 8 * lib.n_ligands  # every item exactly once across the two kernels
