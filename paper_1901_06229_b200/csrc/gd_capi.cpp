@@ -1297,10 +1297,21 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     const double t1 = trace ? now() : 0.0;
     // unpack: pinned output staging -> the caller's arrays (library order)
     const unsigned char* src = static_cast<const unsigned char*>(ctx->slot[si].h_out);
-    size_t at = 0;
-    for (const OutCopy& c : p.copies) {
-      std::memcpy(c.dst, src + at, c.bytes);
-      at += (c.bytes + 255) & ~size_t(255);
+    {
+      // pieces of <= 256 KB over the host pool (the caller's arrays are pageable, first touch)
+      struct Piece {
+        unsigned char* dst;
+        const unsigned char* src;
+        size_t bytes;
+      };
+      std::vector<Piece> pieces;
+      size_t at = 0;
+      for (const OutCopy& c : p.copies) {
+        for (size_t o = 0; o < c.bytes; o += size_t(1) << 18)
+          pieces.push_back({static_cast<unsigned char*>(c.dst) + o, src + at + o, std::min(c.bytes - o, size_t(1) << 18)});
+        at += (c.bytes + 255) & ~size_t(255);
+      }
+      parallel_for(pieces.size(), 1, [&](size_t i) { std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].bytes); });
     }
     closed_form_counts(P, lib, p.l0, p.l1, out);
     if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) unpack %.3f ms\n", p.l0, p.l1, now() - t1);
