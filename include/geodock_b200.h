@@ -114,6 +114,8 @@ typedef struct {
   uint64_t d2h_bytes;          /* bytes downloaded by the last gd_fetch             */
   uint32_t launches;           /* kernels launched by the last gd_run               */
   uint32_t reserved;
+  uint64_t align_second_passes; /* restarts whose candidates K1a collected in a second
+                                   coarse pass (a lane's top-4 overflowed)              */
 } gd_stats;
 
 /* Kernel variants. FAST = two-stage (FP32 coarse screen + exact FP64 refinement, bit-identical

@@ -102,7 +102,8 @@ class _Stats(C.Structure):
                 ("align_fallbacks", C.c_uint64), ("step_exact_evals", C.c_uint64),
                 ("step_fallbacks", C.c_uint64), ("commits", C.c_uint64),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
-                ("launches", C.c_uint32), ("reserved", C.c_uint32)]
+                ("launches", C.c_uint32), ("reserved", C.c_uint32),
+                ("align_second_passes", C.c_uint64)]
 
 
 _lib = None

@@ -966,6 +966,7 @@ int read_device_status(gd_ctx* ctx) {
   ctx->last.step_exact_evals = st[3];
   ctx->last.step_fallbacks = st[4];
   ctx->last.commits = st[5];
+  ctx->last.align_second_passes = st[6];
   if (err[0] == GD_ERR_DEGENERATE_AXIS) {
     // The reference names the ligand (molecule.cpp:157).
     return set_err(ctx, GD_ERR_DEGENERATE_AXIS, "rotamer axis atoms coincide in ligand #" + std::to_string(err[1]));

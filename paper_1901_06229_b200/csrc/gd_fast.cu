@@ -547,7 +547,18 @@ __global__ void __launch_bounds__(NT, 1)
     unsigned long long amb_mask = 0ull;  // rotations j (g = lane + 32 j) with a face-ambiguous sample
     const uint32_t npad = meta.npad;
     const bool big_grid = pr.G > 64u * 32u;
+    // collect mode (second pass): every rotation whose upper key reaches thr_c goes straight to
+    // the restart's candidate list (rs_ncand counts them)
+    bool collect = false;
+    float thr_c = 0.f;
     auto insert = [&](float key_hi, uint32_t g) {
+      if (collect) {
+        if (key_hi >= thr_c) {
+          const int at = atomicAdd(b.rs_ncand + item, 1);
+          if (at < kAlignCand) b.rs_cand[size_t(item) * kAlignCand + at] = uint16_t(g);
+        }
+        return;
+      }
       if (key_hi > top_s[KTOP - 1]) {
         dropped = fmaxf(dropped, top_s[KTOP - 1]);
         float vs = key_hi;
@@ -575,200 +586,222 @@ __global__ void __launch_bounds__(NT, 1)
     auto amb_to_g = [&](uint32_t bit) -> uint32_t {
       return separable ? (bit & 15u) * n_frames + lane + 32u * (bit >> 4) : lane + 32u * bit;
     };
-    if (separable && pr.steps[0] % (4 * kQtGroups) == 0) {
-      // Quarter-turn symmetry: alpha_{c + q na/4} = alpha_c + q pi/2, so one 2D rotation
-      // (rx, ry) = Rz(alpha_c) (wx, wy) gives the four samples t + (rx, ry), t + (-ry, rx),
-      // t - (rx, ry), t + (ry, -rx): two FADDs per sample for x, y. kQtGroups consecutive c share
-      // one pass over the atoms (the frame transform and the z terms are per atom).
-      const uint32_t nq = pr.steps[0] / 4;
-      // byte offset of a cell from the three RZ-floor bit patterns: 16 bx + 16 cx by + zoff16
-      const uint32_t cx16 = cg.cx * 16u, cxy16 = cg.cxy * 16u;
-      // (shared: absolute 32-bit shared addresses; global: byte offsets from cg.cells)
-      const uint32_t base16 = (SC ? uint32_t(__cvta_generic_to_shared(cg.cells)) : 0u) - cg.koff * 16u;
-      const uint32_t dummy16 = (SC ? uint32_t(__cvta_generic_to_shared(cg.cells)) : 0u) + cg.dummy * 16u;
-      for (uint32_t f = lane, m = 0; f < n_frames; f += 32, ++m) {
-        const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
-#pragma unroll 1
-        for (uint32_t c0 = 0; c0 < nq; c0 += kQtGroups) {
-          float acc[4 * kQtGroups], amn[4 * kQtGroups];
-          float2 cs[kQtGroups];
-#pragma unroll
-          for (int i = 0; i < 4 * kQtGroups; ++i) {
-            acc[i] = 0.f;
-            amn[i] = 1e30f;
-          }
-#pragma unroll
-          for (int gi = 0; gi < kQtGroups; ++gi) cs[gi] = pr.acs[(c0 + gi) & 15];
-          // one atom of class CLS (see above): 0 skips the box test, the face tracking and the
-          // dummy select; 1 uses its frame's z term for all its samples (one face-tracking update
-          // per atom, a select per sample); 2 tests every sample
-          float amz = 1e30f, bsum = 0.f;
-          auto atom = [&](uint32_t a, auto cls_tag) {
-            constexpr int CLS = decltype(cls_tag)::value;
-            const float4 v = A[a];
-            const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
-            const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
-            const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
-            const float ez = CLS == 0 ? 0.f : fabsf(gz - cg.hz) - cg.hz;
-            if (CLS == 1) amz = fminf(amz, fabsf(ez));
-            const float rz = __fadd_rz(gz, kMagic);
-            const float fz = gz - (rz - kMagic);
-            const uint32_t zoff16 = __float_as_uint(rz) * cxy16 + base16;
-            const CellBias cb = cell_bias(fz, cg.nb);
-            bsum += cb.b0;  // every sample of this atom carries it
-#pragma unroll
-            for (int gi = 0; gi < kQtGroups; ++gi) {
-              const float rx = fmaf(cs[gi].x, wx, -cs[gi].y * wy), ry = fmaf(cs[gi].y, wx, cs[gi].x * wy);
-              const float px[4] = {tx + rx, tx - ry, tx - rx, tx + ry};
-              const float py[4] = {ty + ry, ty + rx, ty - ry, ty - rx};
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float gx = px[q], gy = py[q];
-                const float rxf = __fadd_rz(gx, kMagic), ryf = __fadd_rz(gy, kMagic);
-                const float fx = gx - (rxf - kMagic), fy = gy - (ryf - kMagic);
-                uint32_t addr = __float_as_uint(ryf) * cx16 + (__float_as_uint(rxf) * 16u + zoff16);
-                if (CLS == 1) addr = ez < 0.0f ? addr : dummy16;
-                if (CLS == 2) {
-                  const float e = fmaxf(fmaxf(fabsf(gx - cg.hx) - cg.hx, fabsf(gy - cg.hy) - cg.hy), ez);
-                  amn[4 * gi + q] = fminf(amn[4 * gi + q], fabsf(e));
-                  addr = e < 0.0f ? addr : dummy16;
+    for (int pass = 0; pass < 2; ++pass) {
+      if (separable && pr.steps[0] % (4 * kQtGroups) == 0) {
+        // Quarter-turn symmetry: alpha_{c + q na/4} = alpha_c + q pi/2, so one 2D rotation
+        // (rx, ry) = Rz(alpha_c) (wx, wy) gives the four samples t + (rx, ry), t + (-ry, rx),
+        // t - (rx, ry), t + (ry, -rx): two FADDs per sample for x, y. kQtGroups consecutive c share
+        // one pass over the atoms (the frame transform and the z terms are per atom).
+        const uint32_t nq = pr.steps[0] / 4;
+        // byte offset of a cell from the three RZ-floor bit patterns: 16 bx + 16 cx by + zoff16
+        const uint32_t cx16 = cg.cx * 16u, cxy16 = cg.cxy * 16u;
+        // (shared: absolute 32-bit shared addresses; global: byte offsets from cg.cells)
+        const uint32_t base16 = (SC ? uint32_t(__cvta_generic_to_shared(cg.cells)) : 0u) - cg.koff * 16u;
+        const uint32_t dummy16 = (SC ? uint32_t(__cvta_generic_to_shared(cg.cells)) : 0u) + cg.dummy * 16u;
+        for (uint32_t f = lane, m = 0; f < n_frames; f += 32, ++m) {
+          const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
+  #pragma unroll 1
+          for (uint32_t c0 = 0; c0 < nq; c0 += kQtGroups) {
+            float acc[4 * kQtGroups], amn[4 * kQtGroups];
+            float2 cs[kQtGroups];
+  #pragma unroll
+            for (int i = 0; i < 4 * kQtGroups; ++i) {
+              acc[i] = 0.f;
+              amn[i] = 1e30f;
+            }
+  #pragma unroll
+            for (int gi = 0; gi < kQtGroups; ++gi) cs[gi] = pr.acs[(c0 + gi) & 15];
+            // one atom of class CLS (see above): 0 skips the box test, the face tracking and the
+            // dummy select; 1 uses its frame's z term for all its samples (one face-tracking update
+            // per atom, a select per sample); 2 tests every sample
+            float amz = 1e30f, bsum = 0.f;
+            auto atom = [&](uint32_t a, auto cls_tag) {
+              constexpr int CLS = decltype(cls_tag)::value;
+              const float4 v = A[a];
+              const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
+              const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
+              const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
+              const float ez = CLS == 0 ? 0.f : fabsf(gz - cg.hz) - cg.hz;
+              if (CLS == 1) amz = fminf(amz, fabsf(ez));
+              const float rz = __fadd_rz(gz, kMagic);
+              const float fz = gz - (rz - kMagic);
+              const uint32_t zoff16 = __float_as_uint(rz) * cxy16 + base16;
+              const CellBias cb = cell_bias(fz, cg.nb);
+              bsum += cb.b0;  // every sample of this atom carries it
+  #pragma unroll
+              for (int gi = 0; gi < kQtGroups; ++gi) {
+                const float rx = fmaf(cs[gi].x, wx, -cs[gi].y * wy), ry = fmaf(cs[gi].y, wx, cs[gi].x * wy);
+                const float px[4] = {tx + rx, tx - ry, tx - rx, tx + ry};
+                const float py[4] = {ty + ry, ty + rx, ty - ry, ty - rx};
+  #pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float gx = px[q], gy = py[q];
+                  const float rxf = __fadd_rz(gx, kMagic), ryf = __fadd_rz(gy, kMagic);
+                  const float fx = gx - (rxf - kMagic), fy = gy - (ryf - kMagic);
+                  uint32_t addr = __float_as_uint(ryf) * cx16 + (__float_as_uint(rxf) * 16u + zoff16);
+                  if (CLS == 1) addr = ez < 0.0f ? addr : dummy16;
+                  if (CLS == 2) {
+                    const float e = fmaxf(fmaxf(fabsf(gx - cg.hx) - cg.hx, fabsf(gy - cg.hy) - cg.hy), ez);
+                    amn[4 * gi + q] = fminf(amn[4 * gi + q], fabsf(e));
+                    addr = e < 0.0f ? addr : dummy16;
+                  }
+                  acc[4 * gi + q] += cell_lerp_b(load_cell<SC>(cg, addr), fx, fy, fz, cb.k);
                 }
-                acc[4 * gi + q] += cell_lerp_b(load_cell<SC>(cg, addr), fx, fy, fz, cb.k);
+              }
+            };
+  #pragma unroll 1
+            for (uint32_t a = 0; a < nsafe; ++a) atom(a, std::integral_constant<int, 0>{});
+  #pragma unroll 1
+            for (uint32_t a = nsafe; a < nsafe + nxy; ++a) atom(a, std::integral_constant<int, 1>{});
+  #pragma unroll 1
+            for (uint32_t a = nsafe + nxy; a < n; ++a) atom(a, std::integral_constant<int, 2>{});
+  #pragma unroll
+            for (int i = 0; i < 4 * kQtGroups; ++i) amn[i] = fminf(amn[i], amz);
+  #pragma unroll
+            for (int gi = 0; gi < kQtGroups; ++gi)
+  #pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t ia = c0 + gi + q * nq;
+                const float sc = (acc[4 * gi + q] - bsum) * inv_n_scale;
+                if (amn[4 * gi + q] <= ptol) {
+                  amb_mask |= 1ull << (16 * m + ia);
+                } else {
+                  insert(sc, ia * n_frames + f);
+                  lkey = fmaxf(lkey, sc);
+                }
+              }
+          }
+        }
+      } else if (separable) {
+        const uint32_t na = pr.steps[0];
+        for (uint32_t f = lane, m = 0; f < n_frames; f += 32, ++m) {
+          const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
+          // alpha in chunks of kAlphaChunk (the frame transform is redone per chunk) so the unrolled
+          // body stays small enough for the instruction cache
+  #pragma unroll 1
+          for (uint32_t i0 = 0; i0 < na; i0 += kAlphaChunk) {
+            float acc[kAlphaChunk], amn[kAlphaChunk];
+            float2 cs[kAlphaChunk];
+  #pragma unroll
+            for (int i = 0; i < kAlphaChunk; ++i) {
+              acc[i] = 0.f;
+              amn[i] = 1e30f;
+              cs[i] = pr.acs[(i0 + i) & 15];
+            }
+  #pragma unroll 1
+            for (uint32_t a = 0; a < npad; ++a) {
+              const float4 v = A[a];
+              const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
+              const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
+              const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
+              const float ez = fabsf(gz - cg.hz) - cg.hz;
+              const float rz = __fadd_rz(gz, kMagic);
+              const float fz = gz - (rz - kMagic);
+              const uint32_t zoff = __float_as_uint(rz) * cg.cxy - cg.koff;
+  #pragma unroll
+              for (int i = 0; i < kAlphaChunk; ++i) {
+                const float gx = fmaf(cs[i].x, wx, fmaf(-cs[i].y, wy, tx));
+                const float gy = fmaf(cs[i].y, wx, fmaf(cs[i].x, wy, ty));
+                acc[i] += coarse_sample_z(cg, gx, gy, ez, fz, zoff, amn[i]);
               }
             }
-          };
-#pragma unroll 1
-          for (uint32_t a = 0; a < nsafe; ++a) atom(a, std::integral_constant<int, 0>{});
-#pragma unroll 1
-          for (uint32_t a = nsafe; a < nsafe + nxy; ++a) atom(a, std::integral_constant<int, 1>{});
-#pragma unroll 1
-          for (uint32_t a = nsafe + nxy; a < n; ++a) atom(a, std::integral_constant<int, 2>{});
-#pragma unroll
-          for (int i = 0; i < 4 * kQtGroups; ++i) amn[i] = fminf(amn[i], amz);
-#pragma unroll
-          for (int gi = 0; gi < kQtGroups; ++gi)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint32_t ia = c0 + gi + q * nq;
-              const float sc = (acc[4 * gi + q] - bsum) * inv_n_scale;
-              if (amn[4 * gi + q] <= ptol) {
+  #pragma unroll
+            for (int i = 0; i < kAlphaChunk; ++i) {
+              const uint32_t ia = i0 + i;
+              if (ia >= na) break;
+              const float sc = acc[i] * inv_n_scale;
+              if (amn[i] <= ptol) {
                 amb_mask |= 1ull << (16 * m + ia);
               } else {
                 insert(sc, ia * n_frames + f);
                 lkey = fmaxf(lkey, sc);
               }
             }
+          }
         }
-      }
-    } else if (separable) {
-      const uint32_t na = pr.steps[0];
-      for (uint32_t f = lane, m = 0; f < n_frames; f += 32, ++m) {
-        const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
-        // alpha in chunks of kAlphaChunk (the frame transform is redone per chunk) so the unrolled
-        // body stays small enough for the instruction cache
-#pragma unroll 1
-        for (uint32_t i0 = 0; i0 < na; i0 += kAlphaChunk) {
-          float acc[kAlphaChunk], amn[kAlphaChunk];
-          float2 cs[kAlphaChunk];
-#pragma unroll
-          for (int i = 0; i < kAlphaChunk; ++i) {
-            acc[i] = 0.f;
-            amn[i] = 1e30f;
-            cs[i] = pr.acs[(i0 + i) & 15];
+      } else {
+        for (uint32_t g = lane, j = 0; g < pr.G; g += 32, ++j) {
+          const float4 r0 = __ldg(pr.grid_f + 3 * g), r1 = __ldg(pr.grid_f + 3 * g + 1), r2 = __ldg(pr.grid_f + 3 * g + 2);
+          float acc0 = 0.f, acc1 = 0.f, amin = 1e30f;
+  #pragma unroll kAlignUnroll
+          for (uint32_t a = 0; a < npad; a += 4) {
+            const float4 v0 = A[a], v1 = A[a + 1], v2 = A[a + 2], v3 = A[a + 3];
+            acc0 += coarse_sample(cg, fmaf(r0.x, v0.x, fmaf(r0.y, v0.y, fmaf(r0.z, v0.z, tx))),
+                                  fmaf(r1.x, v0.x, fmaf(r1.y, v0.y, fmaf(r1.z, v0.z, ty))),
+                                  fmaf(r2.x, v0.x, fmaf(r2.y, v0.y, fmaf(r2.z, v0.z, tz))), amin);
+            acc1 += coarse_sample(cg, fmaf(r0.x, v1.x, fmaf(r0.y, v1.y, fmaf(r0.z, v1.z, tx))),
+                                  fmaf(r1.x, v1.x, fmaf(r1.y, v1.y, fmaf(r1.z, v1.z, ty))),
+                                  fmaf(r2.x, v1.x, fmaf(r2.y, v1.y, fmaf(r2.z, v1.z, tz))), amin);
+            acc0 += coarse_sample(cg, fmaf(r0.x, v2.x, fmaf(r0.y, v2.y, fmaf(r0.z, v2.z, tx))),
+                                  fmaf(r1.x, v2.x, fmaf(r1.y, v2.y, fmaf(r1.z, v2.z, ty))),
+                                  fmaf(r2.x, v2.x, fmaf(r2.y, v2.y, fmaf(r2.z, v2.z, tz))), amin);
+            acc1 += coarse_sample(cg, fmaf(r0.x, v3.x, fmaf(r0.y, v3.y, fmaf(r0.z, v3.z, tx))),
+                                  fmaf(r1.x, v3.x, fmaf(r1.y, v3.y, fmaf(r1.z, v3.z, ty))),
+                                  fmaf(r2.x, v3.x, fmaf(r2.y, v3.y, fmaf(r2.z, v3.z, tz))), amin);
           }
-#pragma unroll 1
-          for (uint32_t a = 0; a < npad; ++a) {
-            const float4 v = A[a];
-            const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
-            const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
-            const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
-            const float ez = fabsf(gz - cg.hz) - cg.hz;
-            const float rz = __fadd_rz(gz, kMagic);
-            const float fz = gz - (rz - kMagic);
-            const uint32_t zoff = __float_as_uint(rz) * cg.cxy - cg.koff;
-#pragma unroll
-            for (int i = 0; i < kAlphaChunk; ++i) {
-              const float gx = fmaf(cs[i].x, wx, fmaf(-cs[i].y, wy, tx));
-              const float gy = fmaf(cs[i].y, wx, fmaf(cs[i].x, wy, ty));
-              acc[i] += coarse_sample_z(cg, gx, gy, ez, fz, zoff, amn[i]);
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < kAlphaChunk; ++i) {
-            const uint32_t ia = i0 + i;
-            if (ia >= na) break;
-            const float sc = acc[i] * inv_n_scale;
-            if (amn[i] <= ptol) {
-              amb_mask |= 1ull << (16 * m + ia);
-            } else {
-              insert(sc, ia * n_frames + f);
-              lkey = fmaxf(lkey, sc);
-            }
+          const float sc = (acc0 + acc1) * inv_n_scale;
+          if (amin <= ptol) {
+            amb_mask |= (j < 64 ? 1ull << j : 0ull);
+            if (j >= 64) lkey = 1e30f;  // cannot track: forces the exact fallback below
+          } else {
+            insert(sc, g);
+            lkey = fmaxf(lkey, sc);
           }
         }
       }
-    } else {
-      for (uint32_t g = lane, j = 0; g < pr.G; g += 32, ++j) {
+      // second pass over face-ambiguous rotations: interval bounds (rare; z-face ambiguities come
+      // in groups of 16 rotations that share (beta, gamma) and therefore the z coordinate)
+      for (unsigned long long mk = amb_mask; mk; mk &= mk - 1) {
+        const uint32_t g = amb_to_g(uint32_t(__ffsll(static_cast<long long>(mk)) - 1));
         const float4 r0 = __ldg(pr.grid_f + 3 * g), r1 = __ldg(pr.grid_f + 3 * g + 1), r2 = __ldg(pr.grid_f + 3 * g + 2);
-        float acc0 = 0.f, acc1 = 0.f, amin = 1e30f;
-#pragma unroll kAlignUnroll
-        for (uint32_t a = 0; a < npad; a += 4) {
-          const float4 v0 = A[a], v1 = A[a + 1], v2 = A[a + 2], v3 = A[a + 3];
-          acc0 += coarse_sample(cg, fmaf(r0.x, v0.x, fmaf(r0.y, v0.y, fmaf(r0.z, v0.z, tx))),
-                                fmaf(r1.x, v0.x, fmaf(r1.y, v0.y, fmaf(r1.z, v0.z, ty))),
-                                fmaf(r2.x, v0.x, fmaf(r2.y, v0.y, fmaf(r2.z, v0.z, tz))), amin);
-          acc1 += coarse_sample(cg, fmaf(r0.x, v1.x, fmaf(r0.y, v1.y, fmaf(r0.z, v1.z, tx))),
-                                fmaf(r1.x, v1.x, fmaf(r1.y, v1.y, fmaf(r1.z, v1.z, ty))),
-                                fmaf(r2.x, v1.x, fmaf(r2.y, v1.y, fmaf(r2.z, v1.z, tz))), amin);
-          acc0 += coarse_sample(cg, fmaf(r0.x, v2.x, fmaf(r0.y, v2.y, fmaf(r0.z, v2.z, tx))),
-                                fmaf(r1.x, v2.x, fmaf(r1.y, v2.y, fmaf(r1.z, v2.z, ty))),
-                                fmaf(r2.x, v2.x, fmaf(r2.y, v2.y, fmaf(r2.z, v2.z, tz))), amin);
-          acc1 += coarse_sample(cg, fmaf(r0.x, v3.x, fmaf(r0.y, v3.y, fmaf(r0.z, v3.z, tx))),
-                                fmaf(r1.x, v3.x, fmaf(r1.y, v3.y, fmaf(r1.z, v3.z, ty))),
-                                fmaf(r2.x, v3.x, fmaf(r2.y, v3.y, fmaf(r2.z, v3.z, tz))), amin);
+        float lo = 0.f, hi = 0.f;
+  #pragma unroll 1
+        for (uint32_t a = 0; a < npad; ++a) {
+          const float4 v = A[a];
+          coarse_sample_iv(cg, fmaf(r0.x, v.x, fmaf(r0.y, v.y, fmaf(r0.z, v.z, tx))),
+                           fmaf(r1.x, v.x, fmaf(r1.y, v.y, fmaf(r1.z, v.z, ty))),
+                           fmaf(r2.x, v.x, fmaf(r2.y, v.y, fmaf(r2.z, v.z, tz))), ptol, lo, hi);
         }
-        const float sc = (acc0 + acc1) * inv_n_scale;
-        if (amin <= ptol) {
-          amb_mask |= (j < 64 ? 1ull << j : 0ull);
-          if (j >= 64) lkey = 1e30f;  // cannot track: forces the exact fallback below
-        } else {
-          insert(sc, g);
-          lkey = fmaxf(lkey, sc);
-        }
+        insert(hi * inv_n_scale + eps, g);  // one extra eps for the clamp
+        lkey = fmaxf(lkey, lo * inv_n_scale);
       }
-    }
-    // second pass over face-ambiguous rotations: interval bounds (rare; z-face ambiguities come
-    // in groups of 16 rotations that share (beta, gamma) and therefore the z coordinate)
-    for (unsigned long long mk = amb_mask; mk; mk &= mk - 1) {
-      const uint32_t g = amb_to_g(uint32_t(__ffsll(static_cast<long long>(mk)) - 1));
-      const float4 r0 = __ldg(pr.grid_f + 3 * g), r1 = __ldg(pr.grid_f + 3 * g + 1), r2 = __ldg(pr.grid_f + 3 * g + 2);
-      float lo = 0.f, hi = 0.f;
-#pragma unroll 1
-      for (uint32_t a = 0; a < npad; ++a) {
-        const float4 v = A[a];
-        coarse_sample_iv(cg, fmaf(r0.x, v.x, fmaf(r0.y, v.y, fmaf(r0.z, v.z, tx))),
-                         fmaf(r1.x, v.x, fmaf(r1.y, v.y, fmaf(r1.z, v.z, ty))),
-                         fmaf(r2.x, v.x, fmaf(r2.y, v.y, fmaf(r2.z, v.z, tz))), ptol, lo, hi);
+      if (collect) {
+        __syncwarp();
+        if (lane == 0 && atomicAdd(b.rs_ncand + item, 0) > kAlignCand) b.rs_ncand[item] = -1;
+        break;
       }
-      insert(hi * inv_n_scale + eps, g);  // one extra eps for the clamp
-      lkey = fmaxf(lkey, lo * inv_n_scale);
-    }
-    const float B = warp_max(lkey);
-    const float thr = B - 2.0f * eps;
-    const bool overflow = __any_sync(FULL, dropped >= thr) || B < -1e29f || B > 1e29f || big_grid;
-    // candidate list for K1b (order irrelevant: K1b takes max exact score, lowest index)
-    uint32_t cnt = 0;
-    if (!overflow) {
+      const float B = warp_max(lkey);
+      const float thr = B - 2.0f * eps;
+      const bool dropped_any = __any_sync(FULL, dropped >= thr);
+      const bool hard = B < -1e29f || B > 1e29f || big_grid;
+      // candidate list for K1b (order irrelevant: K1b takes max exact score, lowest index)
+      uint32_t cnt = 0;
+      if (!dropped_any && !hard) {
 #pragma unroll
-      for (int t = 0; t < KTOP; ++t) {
-        const bool c = top_s[t] >= thr;
-        const uint32_t pend = __ballot_sync(FULL, c);
-        const uint32_t at = cnt + __popc(pend & ((1u << lane) - 1u));
-        if (c && at < uint32_t(kAlignCand)) b.rs_cand[size_t(item) * kAlignCand + at] = uint16_t(top_g[t]);
-        cnt += __popc(pend);
+        for (int t = 0; t < KTOP; ++t) {
+          const bool c = top_s[t] >= thr;
+          const uint32_t pend = __ballot_sync(FULL, c);
+          const uint32_t at = cnt + __popc(pend & ((1u << lane) - 1u));
+          if (c && at < uint32_t(kAlignCand)) b.rs_cand[size_t(item) * kAlignCand + at] = uint16_t(top_g[t]);
+          cnt += __popc(pend);
+        }
       }
+      if (!dropped_any || hard) {
+        if (lane == 0) b.rs_ncand[item] = (dropped_any || hard || cnt > uint32_t(kAlignCand)) ? -1 : int32_t(cnt);
+        break;
+      }
+      // A lane kept only its KTOP best keys and dropped one that reaches thr (several near-equal
+      // alphas of one frame): a second pass with the threshold known collects every candidate
+      // (rare: ~1 restart in 8000 on C2; far cheaper than K1b's all-FP64 alignment).
+      collect = true;
+      thr_c = thr;
+      if (lane == 0) {
+        atomicExch(b.rs_ncand + item, 0);
+        atomicAdd(b.stats + 6, 1ull);
+      }
+      __syncwarp();
+      amb_mask = 0ull;
     }
-    if (lane == 0) b.rs_ncand[item] = (overflow || cnt > uint32_t(kAlignCand)) ? -1 : int32_t(cnt);
   }
 }
 
@@ -918,9 +951,12 @@ __global__ void __launch_bounds__(NT, 1)
     } else {
       // warp-cooperative exact scoring: candidates one at a time, lanes over atoms (P still holds
       // the start pose), index-order sum through shuffles; every lane ends with the same best
-      const uint32_t my_g = lane < uint32_t(ncand) ? b.rs_cand[size_t(item) * kAlignCand + lane] : 0u;
+      static_assert(kAlignCand <= 64, "two candidate words per lane");
+      const uint16_t* cl = b.rs_cand + size_t(item) * kAlignCand;
+      const uint32_t my_g0 = lane < uint32_t(ncand) ? cl[lane] : 0u;
+      const uint32_t my_g1 = lane + 32 < uint32_t(ncand) ? cl[lane + 32] : 0u;
       for (int32_t c = 0; c < ncand; ++c) {
-        const uint32_t g = __shfl_sync(FULL, my_g, c);
+        const uint32_t g = __shfl_sync(FULL, c < 32 ? my_g0 : my_g1, c & 31);
         ++st_aexact;
         const double4 gq = pr.grid[g];
         const Qd q{gq.x, gq.y, gq.z, gq.w};

@@ -13,7 +13,7 @@ namespace gdk {
 constexpr int kMaxAtoms = 256;
 constexpr uint32_t kFastMaxAtoms = 128;  // the fast kernels keep <= 128 atoms per warp in registers      // GD_MAX_ATOMS
 constexpr int kMaxWords = kMaxAtoms / 32;
-constexpr int kAlignCand = 32;      // alignment candidates handed from K1a to K1b per restart
+constexpr int kAlignCand = 64;      // alignment candidates handed from K1a to K1b per restart
 
 // Per-ligand metadata (32 B, one coalesced load per warp).
 struct LigMeta {

@@ -231,6 +231,9 @@ __global__ void finalize_kernel(DevParams pr, DevBatch b) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lig = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (lig >= b.n_lig) return;
+  // after a device-side error (DegenerateAxisError, ...) the K1 kernels stop early and the batch's
+  // results are discarded: the trace may be incomplete, so there is nothing to replay
+  if (*(volatile int*)b.error != 0) return;
   double* P = k2_smem + size_t(threadIdx.x >> 5) * 3 * b.max_n;
   const uint32_t N = pr.n_restarts;
   const LigMeta m = b.meta[lig];

@@ -41,7 +41,12 @@ def test_fast_equals_exact_at_scale(pair, count, atoms, rots, clash, grid):
     pocket = gd.make_pocket(gd.PocketSpec(dims=grid[0], spacing=grid[1]) if grid else gd.PocketSpec())
     lib = gd.make_library(gd.LibrarySpec(count, atoms, rots, 5))
     p = gd.DockParams(clash_factor=clash)
-    _same(fast.dock(lib, pocket, p, trace=True), exact.dock(lib, pocket, p, trace=True))
+    out = fast.dock(lib, pocket, p, trace=True)
+    st = fast.stats()
+    _same(out, exact.dock(lib, pocket, p, trace=True))
+    if (count, atoms, clash) == (1200, 40, 0.75):
+        # K1a's second coarse pass (a lane's top-4 overflowed) occurs at this size and is exact too
+        assert st["align_second_passes"] > 0, st
 
 
 def test_executor_chunks_match_staged_run(pair):
