@@ -15,3 +15,4 @@ for k in align_coarse dock_fast; do
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $O/ncu_${k}_c2 \
       python tools/prof_run.py --ligands 10000 --runs 1 > /dev/null 2>&1
 done
+python tools/stream_1m.py > gpurun_out/stream_1m_c5.json 2>> gpurun_out/bench_c2.err
