@@ -99,7 +99,7 @@ struct Layout {
   std::vector<uint32_t> mask_base, adj_base;
   size_t o_meta, o_atoms, o_start, o_rots, o_dih0, o_masks, o_adj, o_dfs, o_rdfs, o_adjd, host_bytes;
   size_t o_cand, o_ncand, o_rs_score, o_rs_ascore, o_rs_aidx, o_rs_stepk;
-  size_t o_best, o_brs, o_fxyz, o_fdih, o_ctr, total;
+  size_t o_best, o_brs, o_fxyz, o_fdih, o_ctr, o_order, o_ord_scr, o_ord_tmp, ord_tmp_bytes = 0, total;
 };
 
 struct gd_batch {
@@ -734,6 +734,10 @@ Layout plan_layout(const gd_library* lib, const gd_params& P) {
   y.o_fxyz = ar.take<double>(size_t(y.A) * 3);
   y.o_fdih = ar.take<double>(y.Rt);
   y.o_ctr = ar.take<unsigned int>(16);  // work counters: [0..3] exact / one-class launch, [4 c ..] class c
+  y.o_order = ar.take<uint32_t>(y.n_items);
+  y.o_ord_scr = ar.take<uint32_t>(3 * y.n_items);
+  y.ord_tmp_bytes = gdk::order_tmp_bytes(uint32_t(y.n_items));
+  y.o_ord_tmp = ar.take<unsigned char>(y.ord_tmp_bytes);
   y.total = ar.off + 256;
   return y;
 }
@@ -933,6 +937,11 @@ DevBatch bind_batch(const gd_ctx* ctx, const Layout& y, unsigned char* D) {
   d.final_xyz = reinterpret_cast<double*>(D + y.o_fxyz);
   d.final_dih = reinterpret_cast<double*>(D + y.o_fdih);
   d.work_counter = reinterpret_cast<unsigned int*>(D + y.o_ctr);
+  const bool ordered = y.n_items > 0 && !std::getenv("GD_NATURAL_ORDER");  // (A/B experiments)
+  d.order = ordered ? reinterpret_cast<uint32_t*>(D + y.o_order) : nullptr;
+  d.order_scratch = reinterpret_cast<uint32_t*>(D + y.o_ord_scr);
+  d.order_tmp = D + y.o_ord_tmp;
+  d.order_tmp_bytes = y.ord_tmp_bytes;
   d.error = ctx->d_error;
   d.stats = ctx->d_stats;
   return d;

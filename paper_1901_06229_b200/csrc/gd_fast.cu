@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (lane == 0) item = atomicAdd(b.work_counter + 1, 1u);
     item = __shfl_sync(FULL, item, 0);
     if (item >= total) break;
+    if (b.order) item = b.order[item];  // claims in start-target order (launch_dock)
     const uint32_t lig = item / N;
     const LigMeta meta = b.meta[lig];
     const uint32_t n = meta.n;
@@ -873,6 +874,7 @@ __global__ void __launch_bounds__(NT, 1)
     item = __shfl_sync(FULL, item, 0);
     if (item >= total) break;
     if (*(volatile int*)b.error != 0) break;
+    if (b.order) item = b.order[item];  // claims in start-target order (launch_dock)
     Item it;
     it.lig = item / N;
     it.rs = item - it.lig * N;

@@ -95,6 +95,12 @@ struct DevBatch {
   uint32_t* best_restart;
   double* final_xyz;
   double* final_dih;
+  // claim order of the fast kernels' items (sorted by start target, see launch_dock; nullptr:
+  // natural order) and its sort scratch: keys in / keys out / values in (3 x n_items u32) + cub temp
+  uint32_t* order;
+  uint32_t* order_scratch;
+  void* order_tmp;
+  size_t order_tmp_bytes;
   // control
   unsigned int* work_counter;  // [0] K1 / K1b items, [1] K1a items
   int* error;              // [0] = status, [1] = ligand index
@@ -105,6 +111,8 @@ struct DevBatch {
 // ev (nullable): 4 events recorded around K1a, K1b and K2 (per-kernel timing).
 // Pipelined form (stream_b and mid non-null): K1a on `stream`, then K1b and K2 on stream_b after
 // `mid` — the executor keeps the alignment of chunk c+1 and the sweep of chunk c in flight together.
+// cub temp bytes of the item-order sort for n items
+size_t order_tmp_bytes(uint32_t n);
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                         cudaStream_t stream, int* launches, cudaEvent_t* ev = nullptr,
                         cudaStream_t stream_b = nullptr, cudaEvent_t mid = nullptr);

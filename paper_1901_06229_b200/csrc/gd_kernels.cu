@@ -305,6 +305,8 @@ __global__ void finalize_kernel(DevParams pr, DevBatch b) {
   for (uint32_t a = lane; a < 3u * n; a += 32) dst[a] = P[a];
 }
 
+__global__ void order_keys_kernel(DevPocket pk, DevBatch b, uint32_t n_items, uint32_t* keys, uint32_t* vals);
+
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                         cudaStream_t stream, int* launches, cudaEvent_t* ev, cudaStream_t stream_b,
                         cudaEvent_t mid) {
@@ -313,6 +315,18 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
   cudaError_t e = cudaMemsetAsync(b.work_counter, 0, 16 * sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
   if (ev && (e = cudaEventRecord(ev[0], stream)) != cudaSuccess) return e;
+  const uint32_t n_items = b.n_lig * pr.n_restarts;
+  if (b.order && n_items > 0 && (pr.mode & 0xff) != GD_MODE_EXACT) {
+    uint32_t* keys_in = b.order_scratch;
+    uint32_t* keys_out = keys_in + n_items;
+    uint32_t* vals_in = keys_out + n_items;
+    order_keys_kernel<<<(n_items + 255) / 256, 256, 0, stream>>>(pk, b, n_items, keys_in, vals_in);
+    ++*launches;
+    size_t tb = b.order_tmp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(b.order_tmp, tb, keys_in, keys_out, vals_in, b.order, int(n_items), 0, 15,
+                                        stream);
+    if (e != cudaSuccess) return e;
+  }
   // the FP64 kernel over the ligands with n >= min_n, on counter `ctr`
   auto launch_exact = [&](cudaStream_t st, uint32_t min_n, unsigned int* ctr) -> cudaError_t {
     const uint32_t stride = 7 * b.max_n;  // doubles per warp
@@ -398,6 +412,42 @@ __global__ void topk_emit(const unsigned long long* keys, const uint32_t* vals, 
   out[i].best_score = __longlong_as_double(keys[i]);
   out[i].ligand = vals[i];
   out[i].restart = restart[vals[i]];
+}
+
+// --------------------------------------------------------------------------------------------
+// Item order: the fast kernels claim (ligand, restart) items sorted by the Morton code of the
+// start target (32 buckets per axis of the pocket box). Work in flight at any moment then sits in
+// a small region of the pocket, so the cells its samples gather stay in L1 (C5's 1.56 MB of cells
+// do not fit shared memory; K1b reads the cells through L1 on every grid).
+// --------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 5 bits -> every third bit
+  v &= 31u;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+__global__ void order_keys_kernel(DevPocket pk, DevBatch b, uint32_t n_items, uint32_t* keys, uint32_t* vals) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  const double4 t = b.start[2 * size_t(i) + 1];
+  uint32_t c[3];
+  const double tc[3] = {t.x, t.y, t.z};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double u = (tc[a] - pk.origin[a]) / (pk.spacing * double(pk.dims[a] - 1)) * 32.0;
+    c[a] = u <= 0.0 ? 0u : (u >= 31.0 ? 31u : uint32_t(u));
+  }
+  keys[i] = spread3(c[0]) | (spread3(c[1]) << 1) | (spread3(c[2]) << 2);
+  vals[i] = i;
+}
+
+size_t order_tmp_bytes(uint32_t n) {
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, int(n > 0 ? n : 1), 0, 15);
+  return temp + 256;
 }
 
 size_t topk_scratch_bytes(uint32_t n) {
