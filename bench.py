@@ -209,7 +209,8 @@ def run_ours(args):
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
-    launches_per_step = ctx.stats()["launches"] + 2  # K1a + K1b + K2 (gd_run) + topk_prepare + topk_emit
+    # our kernels per step: gd_run (order keys, K1a, K1b, K2) + topk_prepare + topk_emit (cub sorts not counted)
+    launches_per_step = ctx.stats()["launches"] + 2
     # per-kernel device times (CUDA events recorded by gd_run between K1a | K1b | K2 on the
     # context stream), separate pass, L2 flushed before each
     kt = []
