@@ -1,5 +1,3 @@
-for i in 1 2; do
-echo "== C2"; python tools/e2e_trace.py | tail -2
-echo "== C2 prio"; GD_SB_PRIORITY=1 python tools/e2e_trace.py | tail -2
-done
-GD_TRACE_EXECUTOR=1 python tools/e2e_trace.py 2>&1 | grep -E "unpack|drained|done|e2e" | tail -6
+python tools/e2e_trace.py
+for c0 in 1250 2500; do echo "== first $c0 x4"; GD_CHUNK0=$c0 python tools/e2e_trace.py | tail -1; done
+echo "== one chunk"; GD_CHUNK=10000 python tools/e2e_trace.py | tail -1
