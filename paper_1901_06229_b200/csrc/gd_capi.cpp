@@ -733,7 +733,7 @@ Layout plan_layout(const gd_library* lib, const gd_params& P) {
   y.o_brs = ar.take<uint32_t>(L);
   y.o_fxyz = ar.take<double>(size_t(y.A) * 3);
   y.o_fdih = ar.take<double>(y.Rt);
-  y.o_ctr = ar.take<unsigned int>(16);  // work counters: [0..3] exact / one-class launch, [4 c ..] class c
+  y.o_ctr = ar.take<unsigned int>(20);  // work counters: [0..3] exact / one-class, [4 c ..] class c, [16..] K1a NS = 8
   y.o_order = ar.take<uint32_t>(y.n_items);
   y.o_ord_scr = ar.take<uint32_t>(3 * y.n_items);
   y.ord_tmp_bytes = gdk::order_tmp_bytes(uint32_t(y.n_items));

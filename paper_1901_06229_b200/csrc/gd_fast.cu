@@ -1615,4 +1615,13 @@ cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch
   return cudaErrorNotSupported;  // launch_dock routes > 128 atoms to the exact kernel
 }
 
+cudaError_t launch_align_big(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
+                             cudaStream_t stream) {
+  const uint32_t slot_a = 4 * ((b.max_n + 3) & ~3u);
+  const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS / 32, 8);
+  return pa.cells_in_smem
+             ? launch_persistent(align_coarse_kernel<8, GD_ALIGN_THREADS, true>, pa, n_sms, stream, pk, pr, b, slot_a)
+             : launch_persistent(align_coarse_kernel<8, GD_ALIGN_THREADS, false>, pa, n_sms, stream, pk, pr, b, slot_a);
+}
+
 }  // namespace gdk

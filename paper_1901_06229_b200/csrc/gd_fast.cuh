@@ -10,4 +10,9 @@ namespace gdk {
 cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                         cudaStream_t stream, cudaEvent_t mid = nullptr, cudaStream_t stream_b = nullptr);
 
+// K1a alone for ligands of 129..256 atoms (NS = 8): their candidates feed the FP64 kernel, which
+// then skips its own all-FP64 alignment (the FP32 sweep does not fit registers at that size).
+cudaError_t launch_align_big(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
+                             cudaStream_t stream);
+
 }  // namespace gdk

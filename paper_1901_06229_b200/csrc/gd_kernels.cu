@@ -74,6 +74,9 @@ __global__ void __launch_bounds__(1024, 1)
     const LigMeta m = b.meta[lig];
     const uint32_t n = m.n, R = m.nr, W = (n + 31) >> 5;
     if (n < min_n) continue;  // mixed batch: the fast kernels' ligand
+    // min_n > 0: K1a (NS = 8) ran for these ligands; its candidate list (ncand >= 0) contains
+    // every rotation that can be the exact argmax
+    const int32_t ncand = min_n > 0 ? b.rs_ncand[item] : -1;
 
     // ---- starting pose (docking.cpp:52-69); q and target come from the host packer (libm).
     for (uint32_t a = lane; a < n; a += 32) {
@@ -94,13 +97,15 @@ __global__ void __launch_bounds__(1024, 1)
     const V3d c = centroid_smem(P, n);
     double best_s = -1.0;
     uint32_t best_g = 0xffffffffu;
-    for (uint32_t g = lane; g < pr.G; g += 32) {
+    const uint32_t n_eval = ncand >= 0 ? uint32_t(ncand) : pr.G;
+    for (uint32_t ci = lane; ci < n_eval; ci += 32) {
+      const uint32_t g = ncand >= 0 ? uint32_t(b.rs_cand[size_t(item) * kAlignCand + ci]) : ci;
       const double4 gq = pr.grid[g];
       const Qd q{gq.x, gq.y, gq.z, gq.w};
       double sum = 0.0;
       for (uint32_t a = 0; a < n; ++a) sum = __dadd_rn(sum, sample_exact(pk, rotated_about(ld3(P, a), c, q)));
       const double s = __ddiv_rn(sum, double(n));
-      if (s > best_s || best_g == 0xffffffffu) {
+      if (best_g == 0xffffffffu || s > best_s || (s == best_s && g < best_g)) {
         best_s = s;
         best_g = g;
       }
@@ -312,7 +317,7 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
                         cudaEvent_t mid) {
   const bool split = stream_b && mid && stream_b != stream;
   *launches = 0;
-  cudaError_t e = cudaMemsetAsync(b.work_counter, 0, 16 * sizeof(unsigned int), stream);
+  cudaError_t e = cudaMemsetAsync(b.work_counter, 0, 20 * sizeof(unsigned int), stream);
   if (e != cudaSuccess) return e;
   if (ev && (e = cudaEventRecord(ev[0], stream)) != cudaSuccess) return e;
   const uint32_t n_items = b.n_lig * pr.n_restarts;
@@ -345,7 +350,7 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
   };
   if (b.n_lig > 0) {
     const int mode = pr.mode & 0xff;
-    if (mode == GD_MODE_EXACT || b.fast_max_n == 0) {  // everything in FP64
+    if (mode == GD_MODE_EXACT) {  // everything in FP64 (the reference's arithmetic throughout)
       if ((e = launch_exact(stream, 0u, b.work_counter)) != cudaSuccess) return e;
       if (ev && (e = cudaEventRecord(ev[1], stream)) != cudaSuccess) return e;
       if (split) {
@@ -356,7 +361,7 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
       // the fast kernels for every ligand up to kFastMaxAtoms, one K1a + K1b pair per size class
       // present (n <= 32, <= 64, <= 128: NS = 1, 2, 4 from that class's ligands only, so a few
       // larger ligands do not put a whole batch on the NS = 4 kernels); a mixed batch's ligands
-      // beyond 128 atoms go through the FP64 kernel after K1b, on their own counter
+      // beyond 128 atoms get K1a (NS = 8) and then the FP64 kernel on their own counters
       int n_cls = 0;
       for (int c = 0; c < 3; ++c) n_cls += b.class_max_n[c] ? 1 : 0;
       for (int c = 0, k = 0; c < 3; ++c) {
@@ -372,9 +377,20 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
         if (e != cudaSuccess) return e;
         *launches += 2;
       }
-      if (b.max_n > kFastMaxAtoms &&
-          (e = launch_exact(split ? stream_b : stream, kFastMaxAtoms + 1, b.work_counter + 2)) != cudaSuccess)
-        return e;
+      if (b.max_n > kFastMaxAtoms) {
+        // ligands beyond 128 atoms: K1a (NS = 8) for their candidates, then the FP64 kernel
+        DevBatch bb = b;
+        bb.fast_min_n = kFastMaxAtoms;
+        bb.work_counter = b.work_counter + 16;
+        if ((e = launch_align_big(pk, pr, bb, n_sms, stream)) != cudaSuccess) return e;
+        ++*launches;
+        if (split) {
+          if ((e = cudaEventRecord(mid, stream)) != cudaSuccess) return e;
+          if ((e = cudaStreamWaitEvent(stream_b, mid, 0)) != cudaSuccess) return e;
+        }
+        if ((e = launch_exact(split ? stream_b : stream, kFastMaxAtoms + 1, b.work_counter + 2)) != cudaSuccess)
+          return e;
+      }
     }
     if (split) stream = stream_b;  // K2 follows K1b
     e = cudaGetLastError();

@@ -120,3 +120,14 @@ def test_mixed_sizes_route_per_ligand(pair, clash):
     st = fast.stats()
     _same(out, exact.dock(lib, pocket, p, trace=True))
     assert st["restarts"] == 8 * lib.n_ligands  # every item exactly once across the two kernels
+
+
+def test_only_large_ligands(pair):
+    """Every ligand beyond 128 atoms: K1a (NS = 8) hands its candidates to the FP64 kernel."""
+    fast, exact = pair
+    lib = gd.make_library(gd.LibrarySpec(3, 200, 5, 8))
+    pocket = gd.make_pocket()
+    p = gd.DockParams(n_restarts=6, clash_factor=0.3)
+    out = fast.dock(lib, pocket, p, trace=True)
+    assert fast.stats()["align_exact_evals"] == 0  # (the FP64 kernel does not count candidates)
+    _same(out, exact.dock(lib, pocket, p, trace=True))
