@@ -89,6 +89,25 @@ int main() {
       CHECK(csv.str().rfind("workers,devices,lane_width,mode,ligands,", 0) == 0, "write_metrics of GPU metrics");
     }
   }
+  // 2b. degenerate parameters: no restart (default-constructed result: no pose), no repetition
+  {
+    const Pocket pocket = make_pocket(PocketSpec{});
+    LibrarySpec ls;
+    ls.count = 3;
+    ls.atoms = 12;
+    ls.rotamers = 3;
+    const std::vector<Ligand> lib = make_library(ls);
+    int mism = 0;
+    for (unsigned restarts : {0u, 2u}) {
+      DockParams params;
+      params.n_restarts = restarts;
+      params.num_repetitions = restarts ? 0u : 3u;
+      for (const Ligand& lig : lib)
+        if (!same_result(dock_ligand(lig, pocket, params), gpu::dock_ligand(lig, pocket, params))) ++mism;
+    }
+    std::printf("degenerate parameters: %d mismatches / 6\n", mism);
+    CHECK(mism == 0, "n_restarts = 0 and num_repetitions = 0 bit-for-bit");
+  }
   // 3. error contract (errors.hpp)
   {
     SplitMix64 rng(51);

@@ -140,6 +140,10 @@ void dock_on(int d, const std::vector<const Ligand*>& ligs, const Pocket& pocket
     r.phase_times.align_seconds = phase[2 * l];
     r.phase_times.optimize_seconds = phase[2 * l + 1];
     r.final_coordinates.clear();
+    r.final_dihedrals.clear();
+    // no restart: finish_dock keeps its default-constructed best pose, i.e. no coordinates and
+    // no dihedrals (docking.cpp:200-230)
+    if (params.n_restarts == 0) continue;
     for (uint32_t a = flat.atom_off[l]; a < flat.atom_off[l + 1]; ++a) {
       r.final_coordinates.push_back({fxyz[3 * a], fxyz[3 * a + 1], fxyz[3 * a + 2]});
     }

@@ -256,7 +256,11 @@ __global__ void finalize_kernel(DevParams pr, DevBatch b) {
     b.best_score[lig] = best;
     b.best_restart[lig] = id;
   }
-  if (N == 0) return;
+  if (N == 0) {  // no restart: no pose (the flat outputs are zeros; the adapter returns empty)
+    for (uint32_t a = lane; a < 3u * n; a += 32) b.final_xyz[size_t(m.atom_base) * 3 + a] = 0.0;
+    for (uint32_t r = lane; r < R; r += 32) b.final_dih[m.rot_base + r] = 0.0;
+    return;
+  }
   const size_t item = size_t(lig) * N + id;
   for (uint32_t a = lane; a < n; a += 32) {
     const double4 at = b.atoms[m.atom_base + a];
