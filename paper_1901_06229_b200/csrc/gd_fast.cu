@@ -816,7 +816,12 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
-  DevPocket pk = pk_in;
+  // One DevPocket per CTA in shared memory (with the field pointer redirected below): the exact
+  // samplers take it by reference, and a per-thread copy would live in local memory
+  __shared__ DevPocket spk;
+  if (threadIdx.x == 0) spk = pk_in;
+  __syncthreads();
+  DevPocket& pk = spk;
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
   // SC: the pocket cells are staged once per CTA into shared memory (every warp of every work item
   // reads them; a compile-time flag so the gather is an LDS.128, not a generic load)
@@ -833,8 +838,8 @@ __global__ void __launch_bounds__(NT, 1)
     double* sf = reinterpret_cast<double*>(slots + size_t(blockDim.x >> 5) * slot_floats);
     const uint32_t nv = pk.dims[0] * pk.dims[1] * pk.dims[2];
     for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) sf[v] = pk_in.field[v];
+    if (threadIdx.x == 0) pk.field = sf;
     __syncthreads();
-    pk.field = sf;
   }
   float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
   // Behind the atom slot, one double per atom: the FP64 scratch of the index-order sums (SCR1, n
@@ -1643,12 +1648,15 @@ struct SmemPlan {
 // min_warps_sc: the cells go to shared memory only if at least this many warp slots still fit
 // beside them (K1a: 8, its gathers are the hot path; K1b: 12, its few samples can come from L1/L2
 // while more resident warps hide the sweep's latency).
-static SmemPlan plan_smem(const DevPocket& pk, size_t slot_bytes, int max_warps, int min_warps_sc) {
+// `reserve`: the kernel's static shared memory (K1b's DevPocket copy)
+static SmemPlan plan_smem(const DevPocket& pk, size_t slot_bytes, int max_warps, int min_warps_sc,
+                          size_t reserve = 0) {
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
   const size_t cell_bytes = size_t(n_cells + 1) * sizeof(uint4);  // + the dummy cell
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  optin -= int(reserve);
   SmemPlan p{};
   p.cells_in_smem = cell_bytes + size_t(min_warps_sc) * slot_bytes <= size_t(optin);
   const size_t avail = size_t(optin) - (p.cells_in_smem ? cell_bytes : 0);
@@ -1686,14 +1694,15 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
     if ((e = cudaStreamWaitEvent(stream_b, mid, 0)) != cudaSuccess) return e;
     stream = stream_b;
   }
-  SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC);
+  constexpr size_t kK1bStatic = 256;  // the kernel's __shared__ DevPocket, rounded up
+  SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC, kK1bStatic);
   if (pb.warps < 1) return cudaErrorInvalidConfiguration;
   // the FP64 field goes to shared memory too when it fits beside the slots (24^3: 110 KB)
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t field_bytes = size_t(pk.dims[0]) * pk.dims[1] * pk.dims[2] * sizeof(double);
-  const uint32_t fs = pb.smem + field_bytes <= size_t(optin) ? 1u : 0u;
+  const uint32_t fs = pb.smem + field_bytes + kK1bStatic <= size_t(optin) ? 1u : 0u;
   if (fs) pb.smem += field_bytes;
   auto kb = pb.cells_in_smem ? dock_fast_kernel<NS, NTB, true> : dock_fast_kernel<NS, NTB, false>;
   e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pb.smem));
