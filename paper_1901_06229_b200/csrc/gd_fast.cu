@@ -851,6 +851,7 @@ __global__ void __launch_bounds__(NT, 1)
   float4* PL = reinterpret_cast<float4*>(SURV + 2 * ((b.max_n + 3) & ~3u));
   double* X = reinterpret_cast<double*>(PL + kPairCap);
   double* ES = X + 3 * ((b.max_n + 3) & ~3u);
+  float* CF = reinterpret_cast<float*>(ES + ((b.max_n + 3) & ~3u));  // step cache: fixed-side sums
   double* SCR1 = reinterpret_cast<double*>(SURV);
   double* SCR3 = reinterpret_cast<double*>(A);
   const CoarseGrid cg{cells,
@@ -1231,6 +1232,7 @@ __global__ void __launch_bounds__(NT, 1)
         refresh(true, none);
       }
 
+      uint32_t vmask = 0u;  // step cache (rotamers r < 32): valid entries of CF
       for (uint32_t rep = 0; rep < pr.reps; ++rep) {
         for (uint32_t r = 0; r < R; ++r) {
           GD_T(4);
@@ -1251,62 +1253,13 @@ __global__ void __launch_bounds__(NT, 1)
           }
           // M' = moving set minus atom_j (molecule.cpp:166-169), original (mo) and DFS (md) bit
           // spaces. Fast layout: M' is the DFS range (s0, e0), so both follow from the range.
+          // Step cache: a rotamer whose last visit saw an invariant clash (fast layout, no razor
+          // pairs) sees it again while the pose is unchanged (no k != 0 commit since), with the
+          // same fixed-side sum (CF): its head is one shared load.
           uint32_t mo[NS], md[NS];
           bool inm[NS];
-          if (it.m.fast_ok) {
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-              inm[s] = lane + 32 * s < n && pos[s] > s0 && pos[s] < e0;
-              mo[s] = __ballot_sync(FULL, inm[s]);  // slot s holds atoms 32 s + lane
-              md[s] = range_word(uint32_t(s), s0 + 1, e0);
-            }
-          } else {
-#pragma unroll
-            for (int w = 0; w < NS; ++w) {
-              mo[w] = uint32_t(w) < it.W ? __ldg(b.masks + it.m.mask_base + r * it.W + w) : 0u;
-              md[w] = 0u;
-            }
-#pragma unroll
-            for (int w = 0; w < NS; ++w)
-              if ((ij.y >> 5) == uint32_t(w)) mo[w] &= ~(1u << (ij.y & 31));
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-              const uint32_t a = lane + 32 * s;
-              inm[s] = a < n && bit4(mo, a);
-#pragma unroll
-              for (int w = 0; w < NS; ++w)
-                if (inm[s] && (pos[s] >> 5) == uint32_t(w)) md[w] |= 1u << (pos[s] & 31);
-            }
-#pragma unroll
-            for (int w = 0; w < NS; ++w)
-              for (int o = 16; o > 0; o >>= 1) md[w] |= __shfl_xor_sync(FULL, md[w], o);
-          }
-          // invariant pairs (both in M' or both outside) of the current pose: exact from crow
-          bool inv_l = false, frag_l = false, cne_l = false;
+          bool inv, frag, elig0;
           float fsum = 0.f;
-#pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            if (lane + 32 * s >= n) continue;
-            // Invariant pairs: both in M', both outside M', and (m, atom_j) — j lies on the axis,
-            // so |m - j| does not change with the angle either. Their exact verdicts (crow) hold
-            // for every candidate unless the exact margin is razor-thin (arow after refresh).
-            const bool isj = pos[s] == s0;
-#pragma unroll
-            for (int w = 0; w < NS; ++w) {
-              const uint32_t lo = 32u * w;
-              const uint32_t valid = lo + 32u <= n ? FULL : (lo >= n ? 0u : ((1u << (n - lo)) - 1u));
-              const uint32_t mdj = md[w] | ((s0 >> 5) == uint32_t(w) ? 1u << (s0 & 31) : 0u);
-              inv_l |= (crow[s][w] & (inm[s] ? mdj : isj ? valid : (~md[w] & valid))) != 0u;
-              if (inm[s]) frag_l |= (arow[s][w] & mdj) != 0u;
-              if (isj) frag_l |= (arow[s][w] & md[w]) != 0u;
-              cne_l |= crow[s][w] != 0u;
-            }
-            if (!inm[s]) fsum += cs[s];
-          }
-          const bool inv = __any_sync(FULL, inv_l);
-          const bool frag = __any_sync(FULL, frag_l);
-          const bool elig0 = !__any_sync(FULL, cne_l);  // k = 0: the current pose passes bump_check
-          fsum = warp_sum(fsum);
           // FP64 axis (rotate_fragment, molecule.cpp:150-160), computed when first needed; the
           // DegenerateAxisError check (len < 1e-12) only needs FP64 when the FP32 bond is tiny
           V3d pi{0, 0, 0}, axis{0, 0, 0};
@@ -1318,16 +1271,87 @@ __global__ void __launch_bounds__(NT, 1)
             axis = vscale(__ddiv_rn(1.0, __dsqrt_rn(vdot(delta, delta))), delta);
             have_axis = true;
           };
-          if (pr.S > 1) {
-            const float4 fi = A[it.m.fast_ok ? ipos : 0u], fj = A[it.m.fast_ok ? s0 : 0u];
-            const float dx = fj.x - fi.x, dy = fj.y - fi.y, dz = fj.z - fi.z;
-            if (!it.m.fast_ok || dx * dx + dy * dy + dz * dz < 1e-6f) {
-              const V3d qi{X[3 * ij.x], X[3 * ij.x + 1], X[3 * ij.x + 2]};
-              const V3d delta = vsub(V3d{X[3 * ij.y], X[3 * ij.y + 1], X[3 * ij.y + 2]}, qi);
-              if (__dsqrt_rn(vdot(delta, delta)) < 1e-12) {
-                if (lane == 0 && atomicCAS(b.error, 0, GD_ERR_DEGENERATE_AXIS) == 0) b.error[1] = int(it.lig);
-                break;
+          const bool cached = r < 32 && ((vmask >> r) & 1u);
+          if (cached) {
+            fsum = CF[r];
+            inv = true;
+            frag = elig0 = false;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+              mo[s] = md[s] = 0u;
+              inm[s] = false;
+            }
+          } else {
+          // M' = moving set minus atom_j (molecule.cpp:166-169), original (mo) and DFS (md) bit
+            // spaces. Fast layout: M' is the DFS range (s0, e0), so both follow from the range.
+              if (it.m.fast_ok) {
+#pragma unroll
+              for (int s = 0; s < NS; ++s) {
+                inm[s] = lane + 32 * s < n && pos[s] > s0 && pos[s] < e0;
+                mo[s] = __ballot_sync(FULL, inm[s]);  // slot s holds atoms 32 s + lane
+                md[s] = range_word(uint32_t(s), s0 + 1, e0);
               }
+            } else {
+#pragma unroll
+              for (int w = 0; w < NS; ++w) {
+                mo[w] = uint32_t(w) < it.W ? __ldg(b.masks + it.m.mask_base + r * it.W + w) : 0u;
+                md[w] = 0u;
+              }
+#pragma unroll
+              for (int w = 0; w < NS; ++w)
+                if ((ij.y >> 5) == uint32_t(w)) mo[w] &= ~(1u << (ij.y & 31));
+#pragma unroll
+              for (int s = 0; s < NS; ++s) {
+                const uint32_t a = lane + 32 * s;
+                inm[s] = a < n && bit4(mo, a);
+#pragma unroll
+                for (int w = 0; w < NS; ++w)
+                  if (inm[s] && (pos[s] >> 5) == uint32_t(w)) md[w] |= 1u << (pos[s] & 31);
+              }
+#pragma unroll
+              for (int w = 0; w < NS; ++w)
+                for (int o = 16; o > 0; o >>= 1) md[w] |= __shfl_xor_sync(FULL, md[w], o);
+            }
+            // invariant pairs (both in M' or both outside) of the current pose: exact from crow
+            bool inv_l = false, frag_l = false, cne_l = false;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+              if (lane + 32 * s >= n) continue;
+              // Invariant pairs: both in M', both outside M', and (m, atom_j) — j lies on the axis,
+              // so |m - j| does not change with the angle either. Their exact verdicts (crow) hold
+              // for every candidate unless the exact margin is razor-thin (arow after refresh).
+              const bool isj = pos[s] == s0;
+#pragma unroll
+              for (int w = 0; w < NS; ++w) {
+                const uint32_t lo = 32u * w;
+                const uint32_t valid = lo + 32u <= n ? FULL : (lo >= n ? 0u : ((1u << (n - lo)) - 1u));
+                const uint32_t mdj = md[w] | ((s0 >> 5) == uint32_t(w) ? 1u << (s0 & 31) : 0u);
+                inv_l |= (crow[s][w] & (inm[s] ? mdj : isj ? valid : (~md[w] & valid))) != 0u;
+                if (inm[s]) frag_l |= (arow[s][w] & mdj) != 0u;
+                if (isj) frag_l |= (arow[s][w] & md[w]) != 0u;
+                cne_l |= crow[s][w] != 0u;
+              }
+              if (!inm[s]) fsum += cs[s];
+            }
+            inv = __any_sync(FULL, inv_l);
+            frag = __any_sync(FULL, frag_l);
+            elig0 = !__any_sync(FULL, cne_l);  // k = 0: the current pose passes bump_check
+            fsum = warp_sum(fsum);
+            if (pr.S > 1) {
+              const float4 fi = A[it.m.fast_ok ? ipos : 0u], fj = A[it.m.fast_ok ? s0 : 0u];
+              const float dx = fj.x - fi.x, dy = fj.y - fi.y, dz = fj.z - fi.z;
+              if (!it.m.fast_ok || dx * dx + dy * dy + dz * dz < 1e-6f) {
+                const V3d qi{X[3 * ij.x], X[3 * ij.x + 1], X[3 * ij.x + 2]};
+                const V3d delta = vsub(V3d{X[3 * ij.y], X[3 * ij.y + 1], X[3 * ij.y + 2]}, qi);
+                if (__dsqrt_rn(vdot(delta, delta)) < 1e-12) {
+                  if (lane == 0 && atomicCAS(b.error, 0, GD_ERR_DEGENERATE_AXIS) == 0) b.error[1] = int(it.lig);
+                  break;
+                }
+              }
+            }
+            if (r < 32 && inv && !frag && it.m.fast_ok && pr.S >= 2 && pr.S <= 64) {
+              if (lane == 0) CF[r] = fsum;
+              vmask |= 1u << r;
             }
           }
           int32_t step_k = -1;
@@ -1610,6 +1634,7 @@ __global__ void __launch_bounds__(NT, 1)
               // NS <= 2 the full row pass is cheaper than the per-atom votes (C2 at clash 0.1 -5 %)
               if (NS >= 4 && it.m.fast_ok) refresh_cross(mo, md, s0, e0);
               else refresh(false, mo);
+              vmask = 0u;  // the pose changed: every cached step head is stale
             }
           }
           if (lane == 0) b.rs_step_k[trace_at] = step_k;
@@ -1683,7 +1708,7 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   const uint32_t npad_max = (b.max_n + 3) & ~3u;
   const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
   // A (4 floats/atom) + SCR1 (1 double/atom) + PL + X (3 doubles/atom) + ES (1 double/atom)
-  const uint32_t slot_b = 6 * npad_max + 4 * kPairCap + 8 * npad_max;
+  const uint32_t slot_b = 6 * npad_max + 4 * kPairCap + 8 * npad_max + 32;
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
   cudaError_t e = pa.cells_in_smem
                       ? launch_persistent(align_coarse_kernel<NS, NTA, true>, pa, n_sms, stream, pk, pr, b, slot_a)
