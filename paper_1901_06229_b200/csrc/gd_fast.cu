@@ -59,6 +59,9 @@ constexpr uint32_t kPairCap = 64;        // cross-pair list entries per warp (fo
 #ifndef GD_ALIGN_THREADS
 #define GD_ALIGN_THREADS 512
 #endif
+#ifndef GD_ALIGN_THREADS_L1
+#define GD_ALIGN_THREADS_L1 384  // K1a when the cells do not fit shared memory (read through L1)
+#endif
 #ifndef GD_FAST_THREADS_NS4
 #define GD_FAST_THREADS_NS4 256  // NS = 4: 255 registers (no spills) beat 16 warps at 128 (C4 clash 0.1 +15 %)
 #endif
@@ -1710,9 +1713,13 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   // A (4 floats/atom) + SCR1 (1 double/atom) + PL + X (3 doubles/atom) + ES (1 double/atom)
   const uint32_t slot_b = 6 * npad_max + 4 * kPairCap + 8 * npad_max + 32;
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
-  cudaError_t e = pa.cells_in_smem
-                      ? launch_persistent(align_coarse_kernel<NS, NTA, true>, pa, n_sms, stream, pk, pr, b, slot_a)
-                      : launch_persistent(align_coarse_kernel<NS, NTA, false>, pa, n_sms, stream, pk, pr, b, slot_a);
+  // cells in shared memory: issue-bound, 16 warps x 128 registers; cells through L1 (large grids):
+  // 12 warps x 151 registers (C5 +4 %)
+  const SmemPlan pg = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS_L1 / 32, 8);
+  cudaError_t e =
+      pa.cells_in_smem
+          ? launch_persistent(align_coarse_kernel<NS, NTA, true>, pa, n_sms, stream, pk, pr, b, slot_a)
+          : launch_persistent(align_coarse_kernel<NS, GD_ALIGN_THREADS_L1, false>, pg, n_sms, stream, pk, pr, b, slot_a);
   if (e != cudaSuccess) return e;
   if (mid && (e = cudaEventRecord(mid, stream)) != cudaSuccess) return e;
   if (stream_b && stream_b != stream) {  // K1b on its own stream, after this batch's K1a
@@ -1749,9 +1756,11 @@ cudaError_t launch_align_big(const DevPocket& pk, const DevParams& pr, const Dev
                              cudaStream_t stream) {
   const uint32_t slot_a = 4 * ((b.max_n + 3) & ~3u);
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS / 32, 8);
+  const SmemPlan pg = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS_L1 / 32, 8);
   return pa.cells_in_smem
              ? launch_persistent(align_coarse_kernel<8, GD_ALIGN_THREADS, true>, pa, n_sms, stream, pk, pr, b, slot_a)
-             : launch_persistent(align_coarse_kernel<8, GD_ALIGN_THREADS, false>, pa, n_sms, stream, pk, pr, b, slot_a);
+             : launch_persistent(align_coarse_kernel<8, GD_ALIGN_THREADS_L1, false>, pg, n_sms, stream, pk, pr, b,
+                                 slot_a);
 }
 
 }  // namespace gdk
