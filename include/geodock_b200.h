@@ -113,9 +113,17 @@ typedef struct {
   uint64_t h2d_bytes;          /* bytes uploaded by the last gd_stage               */
   uint64_t d2h_bytes;          /* bytes downloaded by the last gd_fetch             */
   uint32_t launches;           /* kernels launched by the last gd_run               */
-  uint32_t reserved;
+  uint32_t exact_fallback;     /* 1: the pocket field lies outside [0,1] (outside the
+                                  Pocket contract, scoring.hpp:15), so the batch ran the
+                                  all-FP64 kernel instead of the two-stage fast path   */
   uint64_t align_second_passes; /* restarts whose candidates K1a collected in a second
                                    coarse pass (a lane's top-4 overflowed)              */
+  /* executed dihedral-sweep work of the fast kernel (the roofline numerator) */
+  uint64_t sweep_steps;           /* dihedral steps (restart x rep x rotamer)              */
+  uint64_t sweep_invariant_steps; /* steps with an invariant clash (no candidate eligible) */
+  uint64_t sweep_scored_steps;    /* steps whose S-1 candidates were scored                */
+  uint64_t sweep_samples;         /* moved-atom samples of the scored candidates           */
+  uint64_t cross_pairs;           /* bump cross pairs (moved x fixed x candidate) evaluated */
 } gd_stats;
 
 /* Kernel variants. FAST = two-stage (FP32 coarse screen + exact FP64 refinement, bit-identical
@@ -128,6 +136,8 @@ typedef struct {
 
 gd_params gd_default_params(void);
 
+/* Number of visible CUDA devices (-1 if the runtime cannot be queried). */
+int gd_device_count(void);
 int gd_create(int device, gd_ctx** out);
 void gd_destroy(gd_ctx* ctx);
 const char* gd_last_error(const gd_ctx* ctx);

@@ -107,8 +107,19 @@ Device& device(int d) {
   throw std::runtime_error("geodock::gpu: " + msg);
 }
 
+// validate_ligand (molecule.cpp:176-238) before anything is flattened, exactly as dock_ligand
+// (docking.cpp:239-240) and run_screening's workers (pipeline.cpp:233-234) do: the flat C-ABI
+// carries neither the dihedral count nor a cached moving set, so those checks happen here.
+void validate_all(const std::vector<const Ligand*>& ligs) {
+  for (const Ligand* l : ligs) {
+    const std::vector<std::string> v = validate_ligand(*l);
+    if (!v.empty()) throw ValidationError(l->name, v);
+  }
+}
+
 void dock_on(int d, const std::vector<const Ligand*>& ligs, const Pocket& pocket, const DockParams& params,
              DockResult* out, double* times = nullptr) {
+  validate_all(ligs);
   Flat flat(ligs);
   Device& dev = device(d);
   std::lock_guard<std::mutex> lk(dev.mu);
@@ -155,12 +166,21 @@ void dock_on(int d, const std::vector<const Ligand*>& ligs, const Pocket& pocket
 
 DockResult dock_ligand(const Ligand& ligand, const Pocket& pocket, const DockParams& params, DockStats* stats) {
   DockResult r;
-  dock_on(0, {&ligand}, pocket, params, &r);
-  if (stats) {  // DockStats counters are the closed form (docking.cpp:44-50); wall times unmeasured
+  double times[4] = {0, 0, 0, 0};
+  dock_on(0, {&ligand}, pocket, params, &r, times);
+  if (stats) {
+    // DockStats counters (docking.cpp:131-142, 188-190) are the closed form the reference records:
+    // N G alignment calls, N reps R S optimise calls and bump checks, N reps R (S - 1) fragment
+    // rotations; wall times are the device time of the alignment (K1a) and the sweep (K1b + K2)
     const uint64_t grid = uint64_t(params.rotation_steps[0]) * params.rotation_steps[1] * params.rotation_steps[2];
+    const uint64_t opt = r.score_calls - uint64_t(params.n_restarts) * grid;
+    const uint64_t steps = uint64_t(params.n_restarts) * params.num_repetitions * ligand.rotamers.size();
     stats->align_score_calls += uint64_t(params.n_restarts) * grid;
-    stats->optimize_score_calls += r.score_calls - uint64_t(params.n_restarts) * grid;
-    stats->bump_checks += r.score_calls - uint64_t(params.n_restarts) * grid;
+    stats->optimize_score_calls += opt;
+    stats->bump_checks += opt;
+    stats->fragment_rotations += params.dihedral_steps > 0 ? steps * (params.dihedral_steps - 1) : 0;
+    stats->align_wall_seconds += times[1];
+    stats->optimize_wall_seconds += times[2];
   }
   return r;
 }
@@ -168,8 +188,20 @@ DockResult dock_ligand(const Ligand& ligand, const Pocket& pocket, const DockPar
 std::pair<std::vector<DockResult>, RunMetrics> run_screening(const std::vector<Ligand>& library, const Pocket& pocket,
                                                              const DockParams& params, const NodeConfig& config,
                                                              const PipelineHooks& /*hooks*/) {
-  if (library.empty()) throw ContractError("ligand library is empty");  // pipeline.cpp:192
+  if (library.empty()) throw ContractError("ligand library is empty");  // pipeline.cpp:192-194
+  if (config.n_workers < 1) throw ContractError("n_workers must be >= 1");
+  if (config.lane_width < 1) throw ContractError("lane_width must be >= 1");
+  {  // every task is validated before its docking (pipeline.cpp:233-234): first invalid ligand
+    std::vector<const Ligand*> all;
+    all.reserve(library.size());
+    for (const Ligand& l : library) all.push_back(&l);
+    validate_all(all);
+  }
+  // n_devices lanes (at least one), each on CUDA device lane % (visible devices): the reference's
+  // lanes are logical (pipeline.cpp:199-202), so more lanes than GPUs share the GPUs
   const unsigned n_dev = config.n_devices > 0 ? config.n_devices : 1;
+  const int n_cuda = gd_device_count();
+  if (n_cuda < 1) throw std::runtime_error("geodock::gpu: no CUDA device visible (there is no CPU fallback)");
   std::vector<DockResult> results(library.size());
   RunMetrics metrics;
   metrics.ligand_count = library.size();
@@ -187,7 +219,7 @@ std::pair<std::vector<DockResult>, RunMetrics> run_screening(const std::vector<L
         std::vector<const Ligand*> part;
         for (std::size_t i = lo; i < hi; ++i) part.push_back(&library[i]);
         try {
-          dock_on(int(d), part, pocket, params, results.data() + lo, times[d].data());
+          dock_on(int(d % unsigned(n_cuda)), part, pocket, params, results.data() + lo, times[d].data());
         } catch (...) {
           errors[d] = std::current_exception();
         }

@@ -19,9 +19,11 @@ DockResult dock_ligand(const Ligand& ligand, const Pocket& pocket, const DockPar
                        DockStats* stats = nullptr);
 
 /// run_screening (pipeline.hpp:85-89): the library is cut into config.n_devices contiguous
-/// shards (at least one), one host thread and one gd_ctx per GPU; results in library order,
-/// bit-identical for any device count. n_workers / lane_width / hooks have no GPU meaning and
-/// are ignored (the CPU retry path of pipeline.cpp:247-251 does not exist: errors propagate).
+/// shards (at least one), one host thread per shard, shard d on CUDA device d % (visible devices)
+/// (the reference's lanes are logical); results in library order, bit-identical for any device
+/// count. n_workers and lane_width keep their ContractErrors (< 1) but otherwise have no GPU
+/// meaning; hooks are ignored (the CPU retry path of pipeline.cpp:247-251 does not exist: errors
+/// propagate). Every ligand is validated (validate_ligand) before any docking.
 std::pair<std::vector<DockResult>, RunMetrics> run_screening(const std::vector<Ligand>& library,
                                                              const Pocket& pocket,
                                                              const DockParams& params,

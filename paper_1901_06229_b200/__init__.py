@@ -17,6 +17,7 @@ import ctypes as C
 import os
 import threading
 import time
+import warnings
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
@@ -102,8 +103,10 @@ class _Stats(C.Structure):
                 ("align_fallbacks", C.c_uint64), ("step_exact_evals", C.c_uint64),
                 ("step_fallbacks", C.c_uint64), ("commits", C.c_uint64),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
-                ("launches", C.c_uint32), ("reserved", C.c_uint32),
-                ("align_second_passes", C.c_uint64)]
+                ("launches", C.c_uint32), ("exact_fallback", C.c_uint32),
+                ("align_second_passes", C.c_uint64), ("sweep_steps", C.c_uint64),
+                ("sweep_invariant_steps", C.c_uint64), ("sweep_scored_steps", C.c_uint64),
+                ("sweep_samples", C.c_uint64), ("cross_pairs", C.c_uint64)]
 
 
 _lib = None
@@ -130,6 +133,7 @@ def _load():
         sig = {
             "gd_default_params": (_Params, []),
             "gd_version": (C.c_char_p, []),
+            "gd_device_count": (C.c_int, []),
             "gd_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
             "gd_destroy": (None, [vp]),
             "gd_last_error": (C.c_char_p, [vp]),
@@ -636,6 +640,10 @@ class Context:
         d = np.asarray(pocket.dims, np.uint32)
         o = np.asarray(pocket.origin, np.float64)
         f = np.ascontiguousarray(pocket.field, np.float64)
+        if f.size and not (f.min() >= 0.0 and f.max() <= 1.0):
+            warnings.warn("pocket field lies outside [0, 1] (the Pocket contract, scoring.hpp:15): "
+                          "batches on this pocket run the all-FP64 kernel, not the fast path "
+                          "(stats()['exact_fallback'] == 1)", RuntimeWarning, stacklevel=2)
         self._check(self._lib.gd_set_pocket(self._h, _p(d, _u32p), _p(o, _f64p), pocket.spacing, _p(f, _f64p)))
         self.pocket = pocket
 
@@ -684,7 +692,7 @@ class Context:
     def stats(self) -> dict:
         s = _Stats()
         self._check(self._lib.gd_last_stats(self._h, C.byref(s)))
-        return {k: getattr(s, k) for k, _ in s._fields_ if k != "reserved"}
+        return {k: getattr(s, k) for k, _ in s._fields_}
 
     def profile(self, lib: Library, pocket: Pocket = None, params: DockParams = None) -> dict:
         """The reference's `profile` subcommand (geodock_main.cpp:189-232) for the GPU path: the
@@ -780,20 +788,28 @@ class Batch:
 
 # ----------------------------------------------------------------------------- reference-shaped API
 _default_ctx = {}
+_default_ctx_lock = threading.Lock()
 
 
 def _ctx_for(device: int) -> Context:
-    c = _default_ctx.get(device)
-    if c is None:
-        c = _default_ctx[device] = Context(device)
-    return c
+    """The shared per-device context (created once, under a module lock)."""
+    with _default_ctx_lock:
+        c = _default_ctx.get(device)
+        if c is None:
+            c = _default_ctx[device] = Context(device)
+        return c
 
 
 def dock_ligand(ligand: Library, pocket: Pocket, params: DockParams = DockParams(), device: int = 0) -> DockResult:
-    """dock_ligand (docking.hpp:140-141) for a one-ligand Library (see make_ligand)."""
+    """dock_ligand (docking.hpp:140-141) for a one-ligand Library (see make_ligand).
+
+    Thread-safe like the reference's pure function: the shared per-device context is externally
+    synchronized, so the pocket/params upload and the batch run under its lock."""
     if ligand.n_ligands != 1:
         raise ContractError("dock_ligand takes exactly one ligand")
-    res = _ctx_for(device).dock(ligand, pocket, params)
+    ctx = _ctx_for(device)
+    with ctx.lock:
+        res = ctx.dock(ligand, pocket, params)
     return res.result(ligand, 0)
 
 

@@ -110,7 +110,8 @@ struct gd_batch {
   void* topk_scratch = nullptr;
   size_t topk_bytes = 0;
   gd_hit* d_hits = nullptr;
-  std::vector<uint32_t> atom_off, rot_off;
+  std::vector<uint32_t> atom_off, rot_off, name_off;
+  std::string names;  // ligand names (error messages)
   uint32_t n_restarts = 0, reps = 0, S = 0;
   gd_params params{};
   Layout layout;
@@ -443,6 +444,15 @@ uint64_t gd_count_score_calls(const gd_params* p, uint64_t n_rotamers) {  // doc
   return uint64_t(p->n_restarts) * (grid + uint64_t(p->num_repetitions) * n_rotamers * p->dihedral_steps);
 }
 
+int gd_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return n;
+}
+
 int gd_create(int device, gd_ctx** out) {
   if (!out) return GD_ERR_ARGUMENT;
   *out = nullptr;
@@ -452,7 +462,7 @@ int gd_create(int device, gd_ctx** out) {
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->n_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_stats, sizeof(unsigned long long) * 16);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_stats, sizeof(unsigned long long) * 32);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_error, sizeof(int) * 2);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_counter, sizeof(unsigned int) * 4);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
@@ -468,9 +478,7 @@ int gd_create(int device, gd_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->sa, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->sb, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
-    static thread_local std::string msg;
-    msg = std::string("gd_create: ") + cudaGetErrorString(e);
-    delete ctx;
+    gd_destroy(ctx);  // releases whatever was created before the failure (streams, events, buffers)
     return GD_ERR_CUDA;
   }
   ctx->have_params = upload_params(ctx) == GD_OK;
@@ -761,12 +769,20 @@ int validate_range(gd_ctx* ctx, const gd_library* lib, uint32_t l0, uint32_t l1)
   return GD_OK;
 }
 
-// bump_check's clash-factor contract fires on the first dihedral candidate (scoring.cpp:48-50).
+// bump_check's clash-factor contract (scoring.cpp:48-50) fires at the first bump_check, i.e. in the
+// first dihedral step of the first ligand that has rotamers (and only when restarts, repetitions
+// and dihedral steps are all non-zero). dock_ligand validates that ligand before (docking.cpp:239-240)
+// and run_screening validates every task before docking it (pipeline.cpp:233): an invalid ligand
+// up to and including that one is reported first.
 int check_contract(gd_ctx* ctx, const gd_library* lib) {
   const gd_params& P = ctx->params;
+  if (!(P.n_restarts && P.num_repetitions && P.dihedral_steps)) return GD_OK;
+  if (P.clash_factor > 0.0 && P.clash_factor <= 1.0) return GD_OK;
   const uint32_t L = lib->n_ligands;
-  const bool any_rot = L && lib->rot_off[L] != lib->rot_off[0];
-  if (any_rot && P.num_repetitions && P.dihedral_steps && (!(P.clash_factor > 0.0) || P.clash_factor > 1.0)) {
+  for (uint32_t l = 0; l < L; ++l) {
+    if (lib->rot_off[l + 1] == lib->rot_off[l]) continue;
+    const int rc = validate_range(ctx, lib, 0, l + 1);
+    if (rc != GD_OK) return rc;
     return set_err(ctx, GD_ERR_CONTRACT, "clash_factor must lie in (0, 1]");
   }
   return GD_OK;
@@ -907,9 +923,10 @@ void pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, uns
 }
 
 // Device view of a packed batch in arena D (ctx-level stats / error flag, per-batch counters).
-DevBatch bind_batch(const gd_ctx* ctx, const Layout& y, unsigned char* D) {
+DevBatch bind_batch(const gd_ctx* ctx, const Layout& y, unsigned char* D, uint32_t lig_base = 0) {
   DevBatch d{};
   d.n_lig = y.L;
+  d.lig_base = lig_base;
   d.n_atoms = y.A;
   d.n_rots = y.Rt;
   d.max_n = y.max_n;
@@ -949,7 +966,7 @@ DevBatch bind_batch(const gd_ctx* ctx, const Layout& y, unsigned char* D) {
 
 int reset_device_status(gd_ctx* ctx, cudaStream_t s) {
   GD_CUDA(ctx, cudaMemsetAsync(ctx->d_error, 0, 2 * sizeof(int), s));
-  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, 16 * sizeof(unsigned long long), s));
+  GD_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, 32 * sizeof(unsigned long long), s));
   return GD_OK;
 }
 
@@ -957,16 +974,22 @@ int launch_batch(gd_ctx* ctx, const DevBatch& d, cudaStream_t s, cudaEvent_t* ev
                  cudaEvent_t mid = nullptr) {
   int launches = 0;
   DevParams pr = dev_params(ctx);
-  if (!(ctx->q_eps < 1.0f)) pr.mode = (pr.mode & ~0xff) | GD_MODE_EXACT;
+  // a field outside [0, 1] (out of the Pocket contract, scoring.hpp:15) cannot be quantised into
+  // the coarse cells: the batch runs the all-FP64 kernel, reported in gd_stats.exact_fallback
+  const bool field_exact = !(ctx->q_eps < 1.0f);
+  if (field_exact) pr.mode = (pr.mode & ~0xff) | GD_MODE_EXACT;
+  ctx->last.exact_fallback = field_exact ? 1u : 0u;
   const cudaError_t e = gdk::launch_dock(dev_pocket(ctx), pr, d, ctx->n_sms, s, &launches, ev, s_b, mid);
   ctx->last.launches = uint32_t(launches);
   if (e != cudaSuccess) return cuda_err(ctx, e, "launch_dock");
   return GD_OK;
 }
 
-int read_device_status(gd_ctx* ctx) {
+// name_of(l): the name of library ligand l (DegenerateAxisError names the ligand like the
+// reference, molecule.cpp:156-158)
+int read_device_status(gd_ctx* ctx, const std::function<std::string(uint32_t)>& name_of) {
   int err[2] = {0, 0};
-  unsigned long long st[8];
+  unsigned long long st[32];
   GD_CUDA(ctx, cudaMemcpy(err, ctx->d_error, sizeof err, cudaMemcpyDeviceToHost));
   GD_CUDA(ctx, cudaMemcpy(st, ctx->d_stats, sizeof st, cudaMemcpyDeviceToHost));
   ctx->last.restarts = st[0];
@@ -976,9 +999,13 @@ int read_device_status(gd_ctx* ctx) {
   ctx->last.step_fallbacks = st[4];
   ctx->last.commits = st[5];
   ctx->last.align_second_passes = st[6];
+  ctx->last.sweep_steps = st[16];
+  ctx->last.sweep_invariant_steps = st[17];
+  ctx->last.sweep_scored_steps = st[18];
+  ctx->last.sweep_samples = st[19];
+  ctx->last.cross_pairs = st[20];
   if (err[0] == GD_ERR_DEGENERATE_AXIS) {
-    // The reference names the ligand (molecule.cpp:157).
-    return set_err(ctx, GD_ERR_DEGENERATE_AXIS, "rotamer axis atoms coincide in ligand #" + std::to_string(err[1]));
+    return set_err(ctx, GD_ERR_DEGENERATE_AXIS, "rotamer axis atoms coincide in ligand '" + name_of(uint32_t(err[1])) + "'");
   }
   if (err[0] != 0) return set_err(ctx, err[0], "device error " + std::to_string(err[0]));
   return GD_OK;
@@ -1101,6 +1128,8 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
   b->S = ctx->params.dihedral_steps;
   b->atom_off.assign(lib->atom_off, lib->atom_off + L + 1);
   b->rot_off.assign(lib->rot_off, lib->rot_off + L + 1);
+  b->name_off.assign(lib->name_off, lib->name_off + L + 1);
+  if (L) b->names.assign(lib->names + lib->name_off[0], lib->name_off[L] - lib->name_off[0]);
   b->layout = plan_layout(&sl.v, ctx->params);
   const Layout& y = b->layout;
   b->arena_bytes = y.total;
@@ -1157,7 +1186,11 @@ int gd_fetch(gd_batch* b, gd_results* out) {
   gd_ctx* ctx = b->ctx;
   cudaSetDevice(ctx->device);
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  int rc = read_device_status(ctx);
+  int rc = read_device_status(ctx, [b](uint32_t l) {
+    return l + 1 < b->name_off.size()
+               ? b->names.substr(b->name_off[l] - b->name_off[0], b->name_off[l + 1] - b->name_off[l])
+               : std::string();
+  });
   if (rc != GD_OK) return rc;
   const Layout& y = b->layout;
   gd_library shim{};
@@ -1207,7 +1240,7 @@ void gd_batch_free(gd_batch* b) {
 int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
   if (!ctx || !out) return GD_ERR_ARGUMENT;
   // device counters of the last gd_run (synchronises the context stream)
-  unsigned long long st[16];
+  unsigned long long st[32];
   GD_CUDA(ctx, cudaMemcpyAsync(st, ctx->d_stats, sizeof st, cudaMemcpyDeviceToHost, ctx->stream));
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   if (const char* env = std::getenv("GD_PRINT_PHASES")) {
@@ -1225,6 +1258,12 @@ int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
   ctx->last.step_exact_evals = st[3];
   ctx->last.step_fallbacks = st[4];
   ctx->last.commits = st[5];
+  ctx->last.align_second_passes = st[6];
+  ctx->last.sweep_steps = st[16];
+  ctx->last.sweep_invariant_steps = st[17];
+  ctx->last.sweep_scored_steps = st[18];
+  ctx->last.sweep_samples = st[19];
+  ctx->last.cross_pairs = st[20];
   *out = ctx->last;
   return GD_OK;
 }
@@ -1363,7 +1402,7 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     GD_CUDA(ctx, cudaStreamWaitEvent(ctx->sa, slot.in, 0));
     if (c == 0) GD_CUDA(ctx, cudaEventRecord(ctx->run0, ctx->sa));
     GD_CUDA(ctx, cudaEventRecord(slot.a0, ctx->sa));
-    rc = launch_batch(ctx, bind_batch(ctx, p.y, D), ctx->sa, nullptr, sb, slot.mid);
+    rc = launch_batch(ctx, bind_batch(ctx, p.y, D, l0), ctx->sa, nullptr, sb, slot.mid);
     if (rc != GD_OK) return rc;
     GD_CUDA(ctx, cudaEventRecord(slot.k, sb));
     if (c + 1 == n_chunks) GD_CUDA(ctx, cudaEventRecord(ctx->run1, sb));
@@ -1392,7 +1431,10 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     ctx->run_times[2] = 1e-3 * opt_ms;
     ctx->run_times[3] = 1e-3 * host_wait_ms;
   }
-  rc = read_device_status(ctx);
+  rc = read_device_status(ctx, [lib](uint32_t l) {
+    return l < lib->n_ligands ? std::string(lib->names + lib->name_off[l], lib->name_off[l + 1] - lib->name_off[l])
+                              : std::string();
+  });
   if (trace) std::fprintf(stderr, "executor: done (t=%.3f)\n", now() - t_start);
   ctx->last.h2d_bytes = h2d;
   ctx->last.d2h_bytes = d2h;

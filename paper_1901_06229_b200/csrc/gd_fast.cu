@@ -871,6 +871,13 @@ __global__ void __launch_bounds__(NT, 1)
   const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
   // per-warp counters (32-bit: a warp's share of one launch stays far below 2^32)
   uint32_t st_aexact = 0, st_afall = 0, st_sexact = 0, st_sfall = 0, st_commit = 0, st_items = 0;
+  // executed sweep work (the roofline's numerator counts only what ran): steps,
+  // steps with an invariant clash, steps whose candidates were scored, moved-atom samples of the
+  // scored candidates, and bump cross pairs (moved x fixed x candidates) of the steps that
+  // evaluated them (none under an invariant clash: the reference's bump_check stops at its first
+  // clashing pair, scoring.cpp:47-60)
+  uint32_t st_steps = 0, st_inv = 0, st_scored = 0;
+  unsigned long long st_samples = 0, st_cross = 0;
 #ifdef GD_PHASE_TIMERS
   long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_ph = clock64();
@@ -1347,7 +1354,7 @@ __global__ void __launch_bounds__(NT, 1)
                 const V3d qi{X[3 * ij.x], X[3 * ij.x + 1], X[3 * ij.x + 2]};
                 const V3d delta = vsub(V3d{X[3 * ij.y], X[3 * ij.y + 1], X[3 * ij.y + 2]}, qi);
                 if (__dsqrt_rn(vdot(delta, delta)) < 1e-12) {
-                  if (lane == 0 && atomicCAS(b.error, 0, GD_ERR_DEGENERATE_AXIS) == 0) b.error[1] = int(it.lig);
+                  if (lane == 0 && atomicCAS(b.error, 0, GD_ERR_DEGENERATE_AXIS) == 0) b.error[1] = int(b.lig_base + it.lig);
                   break;
                 }
               }
@@ -1355,6 +1362,23 @@ __global__ void __launch_bounds__(NT, 1)
             if (r < 32 && inv && !frag && it.m.fast_ok && pr.S >= 2 && pr.S <= 64) {
               if (lane == 0) CF[r] = fsum;
               vmask |= 1u << r;
+            }
+          }
+          {
+            uint32_t nm_c = e0 - s0 - 1;
+            if (!it.m.fast_ok) {
+              nm_c = 0;
+#pragma unroll
+              for (int w = 0; w < NS; ++w) nm_c += __popc(mo[w]);
+            }
+            const uint32_t n_k = pr.S > 0 ? pr.S - 1 : 0;
+            const bool slow = !it.m.fast_ok || frag || pr.S > 64 || pr.S < 2;
+            ++st_steps;
+            st_inv += inv ? 1u : 0u;
+            if (slow || !(skip_inv && inv)) {
+              ++st_scored;
+              st_samples += (unsigned long long)nm_c * n_k;
+              if (!inv || frag) st_cross += (unsigned long long)nm_c * (n - nm_c - 1) * n_k;
             }
           }
           int32_t step_k = -1;
@@ -1658,6 +1682,11 @@ __global__ void __launch_bounds__(NT, 1)
     atomicAdd(b.stats + 3, (unsigned long long)st_sexact);
     atomicAdd(b.stats + 4, (unsigned long long)st_sfall);
     atomicAdd(b.stats + 5, (unsigned long long)st_commit);
+    atomicAdd(b.stats + 16, (unsigned long long)st_steps);
+    atomicAdd(b.stats + 17, (unsigned long long)st_inv);
+    atomicAdd(b.stats + 18, (unsigned long long)st_scored);
+    atomicAdd(b.stats + 19, st_samples);
+    atomicAdd(b.stats + 20, st_cross);
 #ifdef GD_PHASE_TIMERS
     GD_T(7);
     for (int i = 0; i < 8; ++i) atomicAdd(b.stats + 8 + i, (unsigned long long)ph[i]);

@@ -66,6 +66,7 @@ struct DevParams {
 // Device-resident batch.
 struct DevBatch {
   uint32_t n_lig;
+  uint32_t lig_base;       // library index of this batch's ligand 0 (executor chunks; error reports)
   uint32_t n_atoms;
   uint32_t n_rots;
   uint32_t max_n;

@@ -21,7 +21,7 @@ namespace gdk {
 namespace {
 
 __device__ __forceinline__ void raise_error(const DevBatch& b, int code, uint32_t lig) {
-  if (atomicCAS(b.error, 0, code) == 0) b.error[1] = int(lig);
+  if (atomicCAS(b.error, 0, code) == 0) b.error[1] = int(b.lig_base + lig);  // library index
 }
 
 __device__ __forceinline__ bool bit_of(const uint32_t* words, uint32_t a) {
