@@ -201,6 +201,12 @@ int gd_pocketbuf_view(const gd_pocketbuf* buf, uint32_t dims[3], double origin[3
                       const double** field);
 void gd_pocketbuf_free(gd_pocketbuf* buf);
 
+/* Host-side half of gd_stage without a GPU (diagnostics): validation + SoA packing of the whole
+ * library into the device layout, on `threads` host threads (0: the context default, see
+ * GD_HOST_THREADS). *seconds = wall time. Status as gd_stage's validation. */
+int gd_host_pack(const gd_library* lib, const gd_params* params, const uint32_t dims[3], const double origin[3],
+                 double spacing, uint32_t threads, double* seconds);
+
 /* Synthetic inputs (generate.hpp:12-31), host-side and deterministic in the seed. */
 int gd_make_pocket(const uint32_t dims[3], double spacing, const double origin[3], uint32_t blobs,
                    uint64_t seed, double* field_out);
@@ -208,6 +214,10 @@ int gd_make_pocket(const uint32_t dims[3], double spacing, const double origin[3
  * outputs are sized accordingly (names are "lig_%06zu" and are not written here). */
 int gd_make_library(uint64_t count, uint64_t atoms, uint64_t rotamers, uint64_t seed,
                     double* xyz, double* radius, uint32_t* bonds, uint32_t* rots);
+/* Ligands [first, first + count) of the same library (each ligand has its own random stream,
+ * generate.cpp:76), e.g. one rank's shard of a 1M-ligand screen; outputs sized for count ligands. */
+int gd_make_library_range(uint64_t first, uint64_t count, uint64_t atoms, uint64_t rotamers, uint64_t seed,
+                          double* xyz, double* radius, uint32_t* bonds, uint32_t* rots);
 
 #ifdef __cplusplus
 }

@@ -134,6 +134,8 @@ def _load():
             "gd_default_params": (_Params, []),
             "gd_version": (C.c_char_p, []),
             "gd_device_count": (C.c_int, []),
+            "gd_host_pack": (C.c_int, [C.POINTER(_Library), C.POINTER(_Params), _u32p, _f64p, C.c_double,
+                                       C.c_uint32, C.POINTER(C.c_double)]),
             "gd_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
             "gd_destroy": (None, [vp]),
             "gd_last_error": (C.c_char_p, [vp]),
@@ -164,6 +166,8 @@ def _load():
             "gd_pocketbuf_free": (None, [vp]),
             "gd_make_library": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _f64p,
                                           _f64p, _u32p, _u32p]),
+            "gd_make_library_range": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                _f64p, _f64p, _u32p, _u32p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -282,6 +286,26 @@ class Library:
             rots=self.rots[r0:int(self.rot_off[hi])], dihedrals=self.dihedrals[r0:int(self.rot_off[hi])],
             name_off=(self.name_off[lo:hi + 1] - n0).astype(np.uint32),
             names=self.names[n0:int(self.name_off[hi])])
+
+    def take(self, idx) -> "Library":
+        """The ligands idx (any order, repeats allowed) as a new library (vectorised gather)."""
+        idx = np.asarray(idx, np.int64)
+
+        def gather(off, arr):
+            lo, hi = off[idx].astype(np.int64), off[idx + 1].astype(np.int64)
+            lens = hi - lo
+            o = np.zeros(len(idx) + 1, np.uint32)
+            o[1:] = np.cumsum(lens)
+            src = np.repeat(lo - o[:-1].astype(np.int64), lens) + np.arange(int(o[-1]), dtype=np.int64)
+            return o, arr[src]
+
+        ao, xyz = gather(self.atom_off, self.xyz)
+        _, rad = gather(self.atom_off, self.radius)
+        bo, bonds = gather(self.bond_off, self.bonds)
+        ro, rots = gather(self.rot_off, self.rots)
+        _, dih = gather(self.rot_off, self.dihedrals)
+        no, names = gather(self.name_off, np.frombuffer(self.names, np.uint8))
+        return Library(ao, xyz, rad, bo, bonds, ro, rots, dih, no, names.tobytes())
 
     @staticmethod
     def from_ligands(ligs: Sequence[dict]) -> "Library":
@@ -416,26 +440,27 @@ def make_pocket(spec: PocketSpec = PocketSpec()) -> Pocket:
     return Pocket(tuple(int(x) for x in spec.dims), tuple(float(x) for x in spec.origin), float(spec.spacing), f)
 
 
-def make_library(spec: LibrarySpec = LibrarySpec()) -> Library:
-    """generate.cpp:68-109 (host, deterministic)."""
-    count, n = spec.count, max(1, spec.atoms)
+def make_library(spec: LibrarySpec = LibrarySpec(), first: int = 0, count: Optional[int] = None) -> Library:
+    """generate.cpp:68-109 (host, deterministic, multi-threaded). ``first``/``count`` select ligands
+    [first, first + count) of the spec's library (default: all of it), e.g. one rank's shard;
+    every ligand has its own random stream, so a range equals the same slice of the whole."""
+    count = spec.count - first if count is None else count
+    n = max(1, spec.atoms)
     nr = min(spec.rotamers, n - 1)
     xyz = np.zeros((count * n, 3))
     rad = np.zeros(count * n)
     bonds = np.zeros((count * (n - 1), 2), np.uint32)
     rots = np.zeros((count * nr, 2), np.uint32)
-    rc = _load().gd_make_library(count, spec.atoms, spec.rotamers, spec.seed, _p(xyz, _f64p), _p(rad, _f64p),
-                                 _p(bonds, _u32p), _p(rots, _u32p))
+    rc = _load().gd_make_library_range(first, count, spec.atoms, spec.rotamers, spec.seed, _p(xyz, _f64p),
+                                       _p(rad, _f64p), _p(bonds, _u32p), _p(rots, _u32p))
     if rc:
-        raise GeoDockError(f"gd_make_library failed ({rc})")
-    names = b"".join(b"lig_%06d" % i for i in range(count))
-    name_off = np.arange(count + 1, dtype=np.uint32) * 10 if count < 1000000 else None
-    if name_off is None:  # lig_%06zu grows past 6 digits
-        lens = [len(b"lig_%06d" % i) for i in range(count)]
-        name_off = np.zeros(count + 1, np.uint32)
-        name_off[1:] = np.cumsum(lens)
+        raise GeoDockError(f"gd_make_library_range failed ({rc})")
+    names = [b"lig_%06d" % i for i in range(first, first + count)]  # lig_%06zu (generate.cpp:78)
+    name_off = np.zeros(count + 1, np.uint32)
+    if count:
+        name_off[1:] = np.cumsum([len(x) for x in names])
     ar = lambda k: (np.arange(count + 1, dtype=np.uint32) * k).astype(np.uint32)
-    return Library(ar(n), xyz, rad, ar(n - 1), bonds, ar(nr), rots, np.zeros(count * nr), name_off, names)
+    return Library(ar(n), xyz, rad, ar(n - 1), bonds, ar(nr), rots, np.zeros(count * nr), name_off, b"".join(names))
 
 
 def make_ligand(name: str, atoms: Sequence[Tuple[Sequence[float], float]], bonds=(), rotamer_bonds=()) -> Library:
@@ -447,6 +472,19 @@ def make_ligand(name: str, atoms: Sequence[Tuple[Sequence[float], float]], bonds
     if v:
         raise ValidationError(f"ligand '{name}' is invalid:" + "".join(f" [{s}]" for s in v))
     return lib
+
+
+def host_pack_seconds(lib: Library, pocket: Pocket, params: DockParams = DockParams(), threads: int = 0) -> float:
+    """Wall time of the executor's host half (validate + SoA pack) for `lib`, no GPU needed."""
+    L, keep = lib._c()
+    d = np.asarray(pocket.dims, np.uint32)
+    o = np.asarray(pocket.origin, np.float64)
+    t = C.c_double()
+    rc = _load().gd_host_pack(C.byref(L), C.byref(params._c()), _p(d, _u32p), _p(o, _f64p), pocket.spacing,
+                              threads, C.byref(t))
+    if rc:
+        raise _ERRORS.get(rc, GeoDockError)(f"gd_host_pack failed ({rc})")
+    return t.value
 
 
 def validate_ligand(lib: Library, i: int = 0) -> List[str]:

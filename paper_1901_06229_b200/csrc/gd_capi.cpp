@@ -36,6 +36,95 @@ using gdk::LigMeta;
 // next and unpacks the previous
 constexpr int kSlots = 3;
 
+// Host worker pool for the executor's per-chunk validation, packing and unpacking: persistent
+// threads (the caller works too), so a chunk's host work does not pay thread start-up on the
+// critical path. One pool per context (a context is externally synchronized, so one job runs at a
+// time); its width is the host's share of this GPU: GD_HOST_THREADS if set, else the hardware
+// threads divided by max(visible GPUs, LOCAL_WORLD_SIZE) — one context per GPU, whether the GPUs
+// are driven by threads of one process (run_screening) or by one process each (torchrun), share
+// the cores instead of oversubscribing them.
+class HostPool {
+ public:
+  explicit HostPool(unsigned threads) {
+    for (unsigned t = 0; t + 1 < threads; ++t) th_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  unsigned threads() const { return unsigned(th_.size()) + 1; }
+  void run(size_t n, size_t grain, const std::function<void(size_t)>& f) {
+    std::lock_guard<std::mutex> s(submit_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      n_ = n;
+      grain_ = grain;
+      chunks_ = (n + grain - 1) / grain;
+      next_.store(0);
+      pending_ = unsigned(th_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+  static unsigned default_threads() {
+    if (const char* e = std::getenv("GD_HOST_THREADS")) {
+      const int v = std::atoi(e);
+      if (v > 0) return unsigned(v);
+    }
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    int devs = 1;
+    if (cudaGetDeviceCount(&devs) != cudaSuccess || devs < 1) {
+      cudaGetLastError();
+      devs = 1;
+    }
+    unsigned share = unsigned(devs);
+    if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) share = std::max(share, unsigned(std::max(1, std::atoi(e))));
+    return std::max(1u, hw / share);
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      const size_t c = next_.fetch_add(1);
+      if (c >= chunks_) return;
+      const size_t e = std::min(n_, (c + 1) * grain_);
+      for (size_t i = c * grain_; i < e; ++i) (*job_)(i);
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (stop_) return;
+      lk.unlock();
+      work();
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex submit_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(size_t)>* job_ = nullptr;
+  size_t n_ = 0, grain_ = 1, chunks_ = 0;
+  std::atomic<size_t> next_{0};
+  unsigned pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 struct gd_ctx {
   int device = 0;
   int n_sms = 0;
@@ -90,6 +179,7 @@ struct gd_ctx {
   // start to last K2 end), per-chunk K1a and K1b + K2 event intervals, host time waiting on the GPU
   cudaEvent_t run0 = nullptr, run1 = nullptr;
   double run_times[4] = {0, 0, 0, 0};
+  HostPool* pool = nullptr;  // host threads of this context (validation, packing, unpacking)
 };
 
 struct Layout {
@@ -134,81 +224,16 @@ int cuda_err(gd_ctx* ctx, cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_err(ctx, e_, #call); \
   } while (0)
 
-// Host worker pool for the executor's per-chunk validation and packing: hardware_concurrency - 1
-// persistent threads (the caller works too), so a chunk's host work does not pay thread start-up
-// on the critical path. One job at a time; a concurrent caller (another device's host thread)
-// falls back to spawning its own threads. Never destroyed: the workers sleep until process exit.
-class HostPool {
- public:
-  static HostPool& get() {
-    static HostPool* p = new HostPool();
-    return *p;
-  }
-  unsigned threads() const { return unsigned(th_.size()) + 1; }
-  // false if another job is running (the caller then runs its own threads)
-  bool run(size_t n, size_t grain, const std::function<void(size_t)>& f) {
-    std::unique_lock<std::mutex> s(submit_, std::try_to_lock);
-    if (!s.owns_lock()) return false;
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      job_ = &f;
-      n_ = n;
-      grain_ = grain;
-      chunks_ = (n + grain - 1) / grain;
-      next_.store(0);
-      pending_ = unsigned(th_.size());
-      ++gen_;
-    }
-    cv_.notify_all();
-    work();
-    std::unique_lock<std::mutex> lk(mu_);
-    done_.wait(lk, [&] { return pending_ == 0; });
-    job_ = nullptr;
-    return true;
-  }
+HostPool& pool_of(gd_ctx* ctx) {
+  if (!ctx->pool) ctx->pool = new HostPool(HostPool::default_threads());
+  return *ctx->pool;
+}
 
- private:
-  HostPool() {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    for (unsigned t = 0; t + 1 < hw; ++t) {
-      th_.emplace_back([this] { loop(); });
-      th_.back().detach();
-    }
-  }
-  void work() {
-    for (;;) {
-      const size_t c = next_.fetch_add(1);
-      if (c >= chunks_) return;
-      const size_t e = std::min(n_, (c + 1) * grain_);
-      for (size_t i = c * grain_; i < e; ++i) (*job_)(i);
-    }
-  }
-  void loop() {
-    uint64_t seen = 0;
-    for (;;) {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return gen_ != seen; });
-      seen = gen_;
-      lk.unlock();
-      work();
-      lk.lock();
-      if (--pending_ == 0) done_.notify_one();
-    }
-  }
-  std::vector<std::thread> th_;
-  std::mutex submit_, mu_;
-  std::condition_variable cv_, done_;
-  const std::function<void(size_t)>* job_ = nullptr;
-  size_t n_ = 0, grain_ = 1, chunks_ = 0;
-  std::atomic<size_t> next_{0};
-  unsigned pending_ = 0;
-  uint64_t gen_ = 0;
-};
-
-// f(i) for i < n on all host threads, in chunks of `grain` indices (0: about 8 chunks per thread)
+// f(i) for i < n on the context's host threads, in chunks of `grain` indices (0: about 8 chunks
+// per thread)
 template <class F>
-void parallel_for(size_t n, size_t grain, F&& f) {
-  HostPool& pool = HostPool::get();
+void parallel_for(gd_ctx* ctx, size_t n, size_t grain, F&& f) {
+  HostPool& pool = pool_of(ctx);
   const unsigned hw = pool.threads();
   if (grain == 0) grain = std::max<size_t>(1, n / (8 * size_t(hw)));
   const size_t chunks = (n + grain - 1) / grain;
@@ -217,22 +242,7 @@ void parallel_for(size_t n, size_t grain, F&& f) {
     return;
   }
   const std::function<void(size_t)> fn = std::ref(f);
-  if (pool.run(n, grain, fn)) return;
-  const unsigned nt = unsigned(std::min<size_t>(hw, chunks));
-  std::atomic<size_t> next{0};
-  std::vector<std::thread> th;
-  th.reserve(nt);
-  for (unsigned t = 0; t < nt; ++t) {
-    th.emplace_back([&] {
-      for (;;) {
-        const size_t c = next.fetch_add(1);
-        if (c >= chunks) return;
-        const size_t e = std::min(n, (c + 1) * grain);
-        for (size_t i = c * grain; i < e; ++i) f(i);
-      }
-    });
-  }
-  for (auto& t : th) t.join();
+  pool.run(n, grain, fn);
 }
 
 using gdl::Adj;
@@ -514,6 +524,7 @@ void gd_destroy(gd_ctx* ctx) {
   if (ctx->sa) cudaStreamDestroy(ctx->sa);
   if (ctx->sb) cudaStreamDestroy(ctx->sb);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx->pool;
   delete ctx;
 }
 
@@ -754,7 +765,7 @@ Layout plan_layout(const gd_library* lib, const gd_params& P) {
 // docking.cpp:239-240; run_screening reports the first failing task, pipeline.cpp:233).
 int validate_range(gd_ctx* ctx, const gd_library* lib, uint32_t l0, uint32_t l1) {
   std::vector<uint8_t> bad(l1 - l0, 0);
-  parallel_for(l1 - l0, 0, [&](size_t i) {
+  parallel_for(ctx, l1 - l0, 0, [&](size_t i) {
     const LigView v = view_of(lib, uint32_t(l0 + i));
     bad[i] = (!validate(v).empty() || v.n > GD_MAX_ATOMS) ? 1u : 0u;
   });
@@ -788,8 +799,43 @@ int check_contract(gd_ctx* ctx, const gd_library* lib) {
   return GD_OK;
 }
 
-// Host SoA packing of a (rebased, atom_off[0] == 0) library into H[0, host_bytes).
-void pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, unsigned char* H) {
+// Per-thread scratch of the packer (no heap traffic per ligand once warm).
+struct PackScratch {
+  std::vector<uint32_t> start, nbr, fill, stack, order, msize;
+  std::vector<char> seen, in_any, vis;
+  std::vector<uint16_t> pos;
+  std::vector<std::pair<uint32_t, uint32_t>> st;
+};
+
+// DFS from `from` over the CSR graph with the edge (skip_a, skip_b) removed (reachable,
+// molecule.cpp:22-41); seen[] marks the component.
+inline void dfs_mark(const PackScratch& g, uint32_t n, uint32_t from, uint32_t skip_a, uint32_t skip_b,
+                     std::vector<char>& seen, std::vector<uint32_t>& stack) {
+  seen.assign(n, 0);
+  stack.clear();
+  stack.push_back(from);
+  seen[from] = 1;
+  while (!stack.empty()) {
+    const uint32_t u = stack.back();
+    stack.pop_back();
+    for (uint32_t e = g.start[u]; e < g.start[u + 1]; ++e) {
+      const uint32_t w = g.nbr[e];
+      if ((u == skip_a && w == skip_b) || (u == skip_b && w == skip_a)) continue;
+      if (!seen[w]) {
+        seen[w] = 1;
+        stack.push_back(w);
+      }
+    }
+  }
+}
+
+// Host SoA packing of a (rebased, atom_off[0] == 0) library into H[0, host_bytes), fused with
+// validate_ligand (molecule.cpp:176-238): one pass over each ligand's graph builds its adjacency,
+// checks it and derives the moving sets from the same DFS (the component of atom_j with the bond
+// (i, j) removed is both the ring check and the moving set, molecule.cpp:88-98). Returns the index
+// of the first ligand that fails validation (or exceeds GD_MAX_ATOMS) in library order, or -1;
+// invalid ligands are not packed.
+int64_t pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, unsigned char* H) {
   const gd_params& P = ctx->params;
   const uint32_t L = y.L, N = P.n_restarts;
   auto* meta = reinterpret_cast<LigMeta*>(H + y.o_meta);
@@ -808,10 +854,46 @@ void pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, uns
                         ctx->origin[1] + ctx->spacing * static_cast<double>(ctx->dims[1] - 1),
                         ctx->origin[2] + ctx->spacing * static_cast<double>(ctx->dims[2] - 1)};
   const uint32_t a0 = L ? lib->atom_off[0] : 0, r0 = L ? lib->rot_off[0] : 0;
-  parallel_for(L, 0, [&](size_t li) {
+  std::atomic<int64_t> first_bad{int64_t(L)};
+  parallel_for(const_cast<gd_ctx*>(ctx), L, 0, [&](size_t li) {
+    thread_local PackScratch tls;
+    PackScratch& g = tls;  // one TLS lookup per ligand (-fPIC: every thread_local access is a call)
     const uint32_t l = uint32_t(li);
     const LigView v = view_of(lib, l);
     const uint32_t n = v.n, W = (n + 31) / 32;
+    auto bad = [&] {
+      int64_t cur = first_bad.load();
+      while (int64_t(l) < cur && !first_bad.compare_exchange_weak(cur, int64_t(l))) {
+      }
+    };
+    // ---- validate_ligand's checks (the message is rebuilt by validate() for the reported ligand)
+    if (n == 0 || n > GD_MAX_ATOMS || v.nr > GD_MAX_ROTAMERS) return bad();
+    for (uint32_t a = 0; a < n; ++a) {
+      if (!(v.radius[a] > 0.0) || !std::isfinite(v.xyz[3 * a]) || !std::isfinite(v.xyz[3 * a + 1]) ||
+          !std::isfinite(v.xyz[3 * a + 2]))
+        return bad();
+    }
+    for (uint32_t e = 0; e < v.nb; ++e) {
+      const uint32_t x = v.bonds[2 * e], z = v.bonds[2 * e + 1];
+      if (x >= n || z >= n || x == z) return bad();
+    }
+    // adjacency lists (adjacency_lists, molecule.cpp:12-20), CSR in scratch
+    g.start.assign(n + 1, 0);
+    for (uint32_t e = 0; e < v.nb; ++e) {
+      g.start[v.bonds[2 * e] + 1]++;
+      g.start[v.bonds[2 * e + 1] + 1]++;
+    }
+    for (uint32_t i = 0; i < n; ++i) g.start[i + 1] += g.start[i];
+    g.nbr.resize(g.start[n]);
+    g.fill.assign(g.start.begin(), g.start.end() - 1);
+    for (uint32_t e = 0; e < v.nb; ++e) {
+      const uint32_t x = v.bonds[2 * e], z = v.bonds[2 * e + 1];
+      g.nbr[g.fill[x]++] = z;
+      g.nbr[g.fill[z]++] = x;
+    }
+    dfs_mark(g, n, 0, ~0u, ~0u, g.seen, g.stack);
+    for (uint32_t a = 0; a < n; ++a)
+      if (!g.seen[a]) return bad();  // bond graph is not connected
     LigMeta m{};
     m.atom_base = lib->atom_off[l] - a0;
     m.rot_base = lib->rot_off[l] - r0;
@@ -819,6 +901,28 @@ void pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, uns
     m.adj_base = y.adj_base[l];
     m.n = uint16_t(n);
     m.nr = uint16_t(v.nr);
+    // moving sets (finalize_ligand, molecule.cpp:88-98) as bitmasks, from the ring-check DFS
+    g.in_any.assign(n, 0);
+    g.msize.assign(v.nr, 0);
+    for (uint32_t r = 0; r < v.nr; ++r) {
+      const uint32_t i = v.rots[2 * r], j = v.rots[2 * r + 1];
+      if (i >= n || j >= n) return bad();
+      bool bonded = false;
+      for (uint32_t e = g.start[i]; e < g.start[i + 1]; ++e) bonded |= g.nbr[e] == j;
+      if (!bonded) return bad();
+      dfs_mark(g, n, j, i, j, g.seen, g.stack);
+      if (g.seen[i]) return bad();  // the rotamer bond does not disconnect the graph
+      rots[m.rot_base + r] = make_uint2(i, j);
+      dih0[m.rot_base + r] = lib->dihedrals ? lib->dihedrals[lib->rot_off[l] + r] : 0.0;
+      uint32_t* mk = masks + m.mask_base + r * W;
+      std::fill(mk, mk + W, 0u);
+      for (uint32_t a = 0; a < n; ++a)
+        if (g.seen[a]) {
+          mk[a >> 5] |= 1u << (a & 31);
+          g.in_any[a] = 1;
+          ++g.msize[r];
+        }
+    }
     meta[l] = m;
     for (uint32_t a = 0; a < n; ++a) {
       atoms[m.atom_base + a] = make_double4(v.xyz[3 * a], v.xyz[3 * a + 1], v.xyz[3 * a + 2], v.radius[a]);
@@ -827,81 +931,56 @@ void pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, uns
     uint32_t* adj_l = adjm + m.adj_base;
     std::fill(adj_l, adj_l + size_t(n) * W, 0u);
     for (uint32_t e = 0; e < v.nb; ++e) {
-      const uint32_t x = v.bonds[2 * e], y = v.bonds[2 * e + 1];
-      adj_l[x * W + (y >> 5)] |= 1u << (y & 31);
-      adj_l[y * W + (x >> 5)] |= 1u << (x & 31);
-    }
-    // moving sets (finalize_ligand, molecule.cpp:88-98) as bitmasks
-    const Adj adj = adjacency(v);
-    std::vector<char> seen;
-    std::vector<uint32_t> stack;
-    for (uint32_t r = 0; r < v.nr; ++r) {
-      const uint32_t i = v.rots[2 * r], j = v.rots[2 * r + 1];
-      rots[m.rot_base + r] = make_uint2(i, j);
-      dih0[m.rot_base + r] = lib->dihedrals ? lib->dihedrals[lib->rot_off[l] + r] : 0.0;
-      reachable(adj, n, j, i, j, seen, stack);
-      uint32_t* mk = masks + m.mask_base + r * W;
-      std::fill(mk, mk + W, 0u);
-      for (uint32_t a = 0; a < n; ++a)
-        if (seen[a]) mk[a >> 5] |= 1u << (a & 31);
+      const uint32_t x = v.bonds[2 * e], z = v.bonds[2 * e + 1];
+      adj_l[x * W + (z >> 5)] |= 1u << (z & 31);
+      adj_l[z * W + (x >> 5)] |= 1u << (x & 31);
     }
     // DFS preorder from an atom outside every moving set: each moving set (the component of atom_j
     // behind the bridge (i,j)) is then entered only through j and occupies one contiguous range
     // [pos(j), pos(j) + |M|) — the layout the fast sweep's range loops need.
     {
-      std::vector<char> in_any(n, 0);
-      std::vector<uint32_t> msize(v.nr, 0);
-      for (uint32_t r = 0; r < v.nr; ++r) {
-        const uint32_t* mk = masks + m.mask_base + r * W;
-        for (uint32_t a = 0; a < n; ++a)
-          if ((mk[a >> 5] >> (a & 31)) & 1u) {
-            in_any[a] = 1;
-            ++msize[r];
-          }
-      }
       uint32_t root = 0;
-      while (root < n && in_any[root]) ++root;
+      while (root < n && g.in_any[root]) ++root;
       bool ok = root < n && n <= 128;
       if (root >= n) root = 0;
-      std::vector<uint32_t> order;
-      order.reserve(n);
-      std::vector<char> vis(n, 0);
-      std::vector<std::pair<uint32_t, uint32_t>> st;  // (atom, next neighbour slot)
-      st.push_back({root, adj.start[root]});
-      vis[root] = 1;
-      order.push_back(root);
-      while (!st.empty()) {
-        auto& top = st.back();
-        if (top.second == adj.start[top.first + 1]) {
-          st.pop_back();
+      g.order.clear();
+      g.vis.assign(n, 0);
+      g.st.clear();
+      g.st.push_back({root, g.start[root]});
+      g.vis[root] = 1;
+      g.order.push_back(root);
+      while (!g.st.empty()) {
+        auto& top = g.st.back();
+        if (top.second == g.start[top.first + 1]) {
+          g.st.pop_back();
           continue;
         }
-        const uint32_t w = adj.nbr[top.second++];
-        if (!vis[w]) {
-          vis[w] = 1;
-          order.push_back(w);
-          st.push_back({w, adj.start[w]});
+        const uint32_t w = g.nbr[top.second++];
+        if (!g.vis[w]) {
+          g.vis[w] = 1;
+          g.order.push_back(w);
+          g.st.push_back({w, g.start[w]});
         }
       }
-      std::vector<uint16_t> pos(n, 0);
-      for (uint32_t p = 0; p < order.size(); ++p) pos[order[p]] = uint16_t(p);
-      for (uint32_t a = 0; a < n; ++a) dfs[m.atom_base + a] = pos[a];
+      g.pos.assign(n, 0);
+      for (uint32_t p = 0; p < g.order.size(); ++p) g.pos[g.order[p]] = uint16_t(p);
+      for (uint32_t a = 0; a < n; ++a) dfs[m.atom_base + a] = g.pos[a];
       for (uint32_t r = 0; r < v.nr; ++r) {
         const uint32_t i = v.rots[2 * r], j = v.rots[2 * r + 1];
-        const uint32_t s0 = pos[j], e0 = pos[j] + msize[r];
+        const uint32_t s0 = g.pos[j], e0 = g.pos[j] + g.msize[r];
         const uint32_t* mk = masks + m.mask_base + r * W;
         for (uint32_t a = 0; a < n && ok; ++a) {
           const bool mv = (mk[a >> 5] >> (a & 31)) & 1u;
-          ok = mv == (pos[a] >= s0 && pos[a] < e0);
+          ok = mv == (g.pos[a] >= s0 && g.pos[a] < e0);
         }
-        rdfs[m.rot_base + r] = make_ushort4(uint16_t(s0), uint16_t(e0), uint16_t(pos[i]), 0);
+        rdfs[m.rot_base + r] = make_ushort4(uint16_t(s0), uint16_t(e0), uint16_t(g.pos[i]), 0);
       }
       uint32_t* ad = adjd + m.adj_base;
       std::fill(ad, ad + size_t(n) * W, 0u);
       for (uint32_t e = 0; e < v.nb; ++e) {
-        const uint32_t x = pos[v.bonds[2 * e]], y = pos[v.bonds[2 * e + 1]];
-        ad[x * W + (y >> 5)] |= 1u << (y & 31);
-        ad[y * W + (x >> 5)] |= 1u << (x & 31);
+        const uint32_t x = g.pos[v.bonds[2 * e]], z = g.pos[v.bonds[2 * e + 1]];
+        ad[x * W + (z >> 5)] |= 1u << (z & 31);
+        ad[z * W + (x >> 5)] |= 1u << (x & 31);
       }
       meta[l].fast_ok = ok ? 1u : 0u;
       meta[l].npad = (n + 3) & ~3u;
@@ -919,7 +998,18 @@ void pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, uns
       start[2 * it + 1] = make_double4(tx, ty, tz, 0.0);
     }
   });
+  const int64_t fb = first_bad.load();
+  return fb < int64_t(L) ? fb : -1;
+}
 
+// The reference's error for ligand l (known to be invalid or too large): ValidationError with
+// validate_ligand's messages, else GD_ERR_UNSUPPORTED.
+int report_invalid(gd_ctx* ctx, const gd_library* lib, uint32_t l) {
+  const LigView v = view_of(lib, l);
+  const auto viol = validate(v);
+  if (!viol.empty()) return set_err(ctx, GD_ERR_INVALID_LIGAND, validation_message(v.name, viol));
+  return set_err(ctx, GD_ERR_UNSUPPORTED, "ligand '" + std::string(v.name) + "' has " + std::to_string(v.n) +
+                                              " atoms; this build supports up to " + std::to_string(GD_MAX_ATOMS));
 }
 
 // Device view of a packed batch in arena D (ctx-level stats / error flag, per-batch counters).
@@ -1105,6 +1195,34 @@ int ensure_device(gd_ctx* ctx, void*& p, size_t& cap, size_t need) {
 
 extern "C" {
 
+int gd_host_pack(const gd_library* lib, const gd_params* params, const uint32_t dims[3], const double origin[3],
+                 double spacing, uint32_t threads, double* seconds) {
+  if (!lib || !params || !dims || !origin) return GD_ERR_ARGUMENT;
+  gd_ctx tmp;  // host-only: no device state is created or touched
+  tmp.params = *params;
+  for (int i = 0; i < 3; ++i) {
+    tmp.dims[i] = dims[i];
+    tmp.origin[i] = origin[i];
+  }
+  tmp.spacing = spacing;
+  tmp.pool = new HostPool(threads ? threads : HostPool::default_threads());
+  int rc = GD_OK;
+  {
+    SubLib sl;
+    sub_library(lib, 0, lib->n_ligands, sl);
+    const Layout y = plan_layout(&sl.v, tmp.params);
+    // the staging buffer is resident before the clock starts, as the executor's reused pinned
+    // slots are (first-touch page faults are not packing work)
+    std::vector<unsigned char> host(y.host_bytes + 256, 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    const int64_t bad = pack_library(&tmp, &sl.v, y, host.data());
+    if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (bad >= 0) rc = report_invalid(&tmp, lib, uint32_t(bad));
+  }
+  delete tmp.pool;
+  return rc;
+}
+
 int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
   if (!ctx || !lib || !out) return GD_ERR_ARGUMENT;
   *out = nullptr;
@@ -1115,8 +1233,7 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
   if (L > 0 && (!lib->atom_off || !lib->bond_off || !lib->rot_off || !lib->name_off || !lib->names)) {
     return set_err(ctx, GD_ERR_ARGUMENT, "null library array");
   }
-  int rc = validate_range(ctx, lib, 0, L);
-  if (rc == GD_OK) rc = check_contract(ctx, lib);
+  int rc = check_contract(ctx, lib);
   if (rc != GD_OK) return rc;
   SubLib sl;
   sub_library(lib, 0, L, sl);
@@ -1134,7 +1251,11 @@ int gd_stage(gd_ctx* ctx, const gd_library* lib, gd_batch** out) {
   const Layout& y = b->layout;
   b->arena_bytes = y.total;
   std::vector<unsigned char> host(y.host_bytes + 256);
-  pack_library(ctx, &sl.v, y, host.data());
+  const int64_t bad = pack_library(ctx, &sl.v, y, host.data());  // validates every ligand first-in-order
+  if (bad >= 0) {
+    delete b;
+    return report_invalid(ctx, lib, uint32_t(bad));
+  }
   cudaError_t e = cudaMalloc(&b->arena, b->arena_bytes);
   if (e != cudaSuccess) {
     delete b;
@@ -1360,7 +1481,7 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
           pieces.push_back({static_cast<unsigned char*>(c.dst) + o, src + at + o, std::min(c.bytes - o, size_t(1) << 18)});
         at += (c.bytes + 255) & ~size_t(255);
       }
-      parallel_for(pieces.size(), 1, [&](size_t i) { std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].bytes); });
+      parallel_for(ctx, pieces.size(), 1, [&](size_t i) { std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].bytes); });
     }
     closed_form_counts(P, lib, p.l0, p.l1, out);
     if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) unpack %.3f ms\n", p.l0, p.l1, now() - t1);
@@ -1373,13 +1494,6 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     rc = drain(si);
     if (rc != GD_OK) return rc;
     const uint32_t l0 = bounds[c], l1 = bounds[c + 1];
-    const double tv = trace ? now() : 0.0;
-    rc = validate_range(ctx, lib, l0, l1);
-    if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) validate %.3f ms (t=%.3f)\n", l0, l1, now() - tv, tv - t_start);
-    if (rc != GD_OK) {
-      cudaDeviceSynchronize();
-      return rc;
-    }
     SubLib sl;
     sub_library(lib, l0, l1, sl);
     Pending& p = pend[si];
@@ -1393,8 +1507,14 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
     if ((rc = ensure_pinned(ctx, slot.h_out, slot.h_out_cap, out_bytes + 256)) != GD_OK) return rc;
     if ((rc = ensure_device(ctx, slot.d_arena, slot.d_cap, p.y.total)) != GD_OK) return rc;
     const double tp = trace ? now() : 0.0;
-    pack_library(ctx, &sl.v, p.y, static_cast<unsigned char*>(slot.h_in));
-    if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) pack %.3f ms\n", l0, l1, now() - tp);
+    // validation + packing in one pass; the first invalid ligand in library order is reported
+    // before any of its chunk's work (earlier chunks' results are discarded with the error)
+    const int64_t bad = pack_library(ctx, &sl.v, p.y, static_cast<unsigned char*>(slot.h_in));
+    if (trace) std::fprintf(stderr, "executor: chunk [%u,%u) validate+pack %.3f ms (t=%.3f)\n", l0, l1, now() - tp, tp - t_start);
+    if (bad >= 0) {
+      cudaDeviceSynchronize();
+      return report_invalid(ctx, lib, l0 + uint32_t(bad));
+    }
     unsigned char* D = static_cast<unsigned char*>(slot.d_arena);
     GD_CUDA(ctx, cudaMemcpyAsync(D, slot.h_in, p.y.host_bytes, cudaMemcpyHostToDevice, slot.stream));
     GD_CUDA(ctx, cudaEventRecord(slot.in, slot.stream));

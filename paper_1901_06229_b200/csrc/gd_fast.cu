@@ -822,7 +822,9 @@ __global__ void __launch_bounds__(NT, 1)
   // One DevPocket per CTA in shared memory (with the field pointer redirected below): the exact
   // samplers take it by reference, and a per-thread copy would live in local memory
   __shared__ DevPocket spk;
+  __shared__ unsigned long long sweep_ctr[5];  // executed sweep work, see st_* below
   if (threadIdx.x == 0) spk = pk_in;
+  if (threadIdx.x < 5) sweep_ctr[threadIdx.x] = 0ull;
   __syncthreads();
   DevPocket& pk = spk;
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
@@ -875,9 +877,8 @@ __global__ void __launch_bounds__(NT, 1)
   // steps with an invariant clash, steps whose candidates were scored, moved-atom samples of the
   // scored candidates, and bump cross pairs (moved x fixed x candidates) of the steps that
   // evaluated them (none under an invariant clash: the reference's bump_check stops at its first
-  // clashing pair, scoring.cpp:47-60)
-  uint32_t st_steps = 0, st_inv = 0, st_scored = 0;
-  unsigned long long st_samples = 0, st_cross = 0;
+  // clashing pair, scoring.cpp:47-60). CTA counters in shared memory (sweep_ctr): per-warp
+  // registers here cost K1b spills.
 #ifdef GD_PHASE_TIMERS
   long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_ph = clock64();
@@ -1373,12 +1374,14 @@ __global__ void __launch_bounds__(NT, 1)
             }
             const uint32_t n_k = pr.S > 0 ? pr.S - 1 : 0;
             const bool slow = !it.m.fast_ok || frag || pr.S > 64 || pr.S < 2;
-            ++st_steps;
-            st_inv += inv ? 1u : 0u;
-            if (slow || !(skip_inv && inv)) {
-              ++st_scored;
-              st_samples += (unsigned long long)nm_c * n_k;
-              if (!inv || frag) st_cross += (unsigned long long)nm_c * (n - nm_c - 1) * n_k;
+            if (lane == 0) {
+              atomicAdd(&sweep_ctr[0], 1ull);
+              if (inv) atomicAdd(&sweep_ctr[1], 1ull);
+              if (slow || !(skip_inv && inv)) {
+                atomicAdd(&sweep_ctr[2], 1ull);
+                atomicAdd(&sweep_ctr[3], (unsigned long long)(nm_c * n_k));
+                if (!inv || frag) atomicAdd(&sweep_ctr[4], (unsigned long long)(nm_c * (n - nm_c - 1) * n_k));
+              }
             }
           }
           int32_t step_k = -1;
@@ -1682,16 +1685,13 @@ __global__ void __launch_bounds__(NT, 1)
     atomicAdd(b.stats + 3, (unsigned long long)st_sexact);
     atomicAdd(b.stats + 4, (unsigned long long)st_sfall);
     atomicAdd(b.stats + 5, (unsigned long long)st_commit);
-    atomicAdd(b.stats + 16, (unsigned long long)st_steps);
-    atomicAdd(b.stats + 17, (unsigned long long)st_inv);
-    atomicAdd(b.stats + 18, (unsigned long long)st_scored);
-    atomicAdd(b.stats + 19, st_samples);
-    atomicAdd(b.stats + 20, st_cross);
 #ifdef GD_PHASE_TIMERS
     GD_T(7);
     for (int i = 0; i < 8; ++i) atomicAdd(b.stats + 8 + i, (unsigned long long)ph[i]);
 #endif
   }
+  __syncthreads();
+  if (threadIdx.x < 5) atomicAdd(b.stats + 16 + threadIdx.x, sweep_ctr[threadIdx.x]);
 }
 
 // Shared-memory plan of one persistent kernel: the pocket cells (when they fit next to 8 warp

@@ -50,3 +50,32 @@ def test_gather_topk_gloo_world2(n, k):
         p.join(timeout=60)
     for rank, merged in got:
         assert merged == want, rank
+
+
+def test_library_ranges_equal_slices_of_the_library():
+    """A rank generates its shard directly (make_library(first=, count=)): every ligand draws from
+    its own stream (generate.cpp:76), so ranges are slices of the whole library."""
+    import numpy as np
+    import paper_1901_06229_b200 as gd
+    spec = gd.LibrarySpec(3001, 40, 8, 0)
+    full = gd.make_library(spec)
+    for world in (1, 2, 3, 8):
+        for r in range(world):
+            lo, hi = shard_bounds(spec.count, world, r)
+            part, want = gd.make_library(spec, first=lo, count=hi - lo), full.slice(lo, hi)
+            for k in ("atom_off", "xyz", "radius", "bond_off", "bonds", "rot_off", "rots", "name_off"):
+                assert np.array_equal(getattr(part, k), getattr(want, k)), (world, r, k)
+            assert part.names == want.names
+
+
+def test_bench_shards_strong_and_weak():
+    import argparse
+    import bench
+    for scaling, base in (("strong", 10000), ("weak", 10000)):
+        for world in (1, 2, 4, 8):
+            args = argparse.Namespace(ligands=0, config="c2", scaling=scaling)
+            parts = [bench.shard(args, world, r) for r in range(world)]
+            total = parts[0][0]
+            assert total == (base if scaling == "strong" else base * world)
+            assert sum(c for _, _, c in parts) == total
+            assert [f for _, f, _ in parts] == [sum(c for _, _, c in parts[:r]) for r in range(world)]

@@ -28,6 +28,7 @@ for i in range(a.runs):
     b.run()
     ctx.sync()
     dt = time.perf_counter() - t0
-    print(f"run {i}: {dt*1e3:.2f} ms  {a.ligands/dt:.0f} lig/s")
+    km = ctx.kernel_ms()
+    print(f"run {i}: {dt*1e3:.2f} ms  {a.ligands/dt:.0f} lig/s  K1a {km['k1a_align']:.2f} K1b {km['k1b_sweep']:.2f} K2 {km['k2_finalize']:.2f} ms")
 res = b.fetch()
 print("mean best", float(res.best_score.mean()), ctx.stats())
