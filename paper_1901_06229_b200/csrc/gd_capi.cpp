@@ -399,6 +399,7 @@ DevPocket dev_pocket(const gd_ctx* ctx) {
     pk.maxc[i] = static_cast<double>(ctx->dims[i] - 1);
   }
   pk.spacing = ctx->spacing;
+  pk.inv_spacing = 1.0 / ctx->spacing;
   pk.inv_spacing_f = float(1.0 / ctx->spacing);
   pk.q_eps = ctx->q_eps;
   pk.max_step = ctx->max_step;

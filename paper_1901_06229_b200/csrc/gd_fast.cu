@@ -40,11 +40,16 @@ constexpr int kAlignUnroll = GD_ALIGN_UNROLL;
 #define GD_ALPHA_CHUNK 4
 #endif
 constexpr int kAlphaChunk = GD_ALPHA_CHUNK;
+#ifndef GD_K1A_X2
+#define GD_K1A_X2 1  // K1a samples in f32x2 pairs (bit-identical to the scalar form)
+#endif
 #ifndef GD_QT_GROUPS
 #define GD_QT_GROUPS 2
 #endif
 constexpr int kQtGroups = GD_QT_GROUPS;  // quarter-turn groups per pass over the atoms
-constexpr uint32_t kPairCap = 64;        // cross-pair list entries per warp (folded when full)
+// cross-pair list entries per warp (folded when the next moved atom's <= 32 NS pairs might not fit)
+template <int NS>
+__host__ __device__ constexpr uint32_t pair_cap() { return 32u * NS + 32u; }
 // Optional device-side phase timers (build with -DGD_PHASE_TIMERS): per-warp clock64 deltas summed
 // into gd_stats-adjacent counters 8..15 (setup, align coarse, align refine, refresh, step head,
 // step coarse candidates, step decisions+commit, tail).
@@ -255,6 +260,31 @@ __device__ __forceinline__ V3d centroid_smem(const Pose<NS>& P, uint32_t n, doub
   return vscale(__ddiv_rn(1.0, double(n)), tot);
 }
 
+// Element i of a small register array without a dynamic index (a dynamic index would put the
+// array in local memory): a select chain over the NS slots.
+template <int NS, class T>
+__device__ __forceinline__ T pick(const T (&v)[NS], int i) {
+  T r = v[0];
+#pragma unroll
+  for (int k = 1; k < NS; ++k)
+    if (i == k) r = v[k];
+  return r;
+}
+template <int NS, class T>
+__device__ __forceinline__ void put(T (&v)[NS], int i, T x) {
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+    if (i == k) v[k] = x;
+}
+template <int NS>
+__device__ __forceinline__ void put2(uint32_t (&v)[NS][NS], int i, int j, uint32_t x) {
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int l = 0; l < NS; ++l)
+      if (i == k && j == l) v[k][l] = x;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -367,19 +397,25 @@ __device__ __forceinline__ double exact_candidate_score_g(const DevPocket& pk, u
                                                        const double* ES, uint32_t mo0, uint32_t mo1, uint32_t mo2,
                                                        uint32_t mo3, bool rotate, V3d pi, Qd q, uint32_t lane,
                                                        double* scr) {
-  const uint32_t mo[4] = {mo0, mo1, mo2, mo3};
-  double ns[NS];
-#pragma unroll
+  // lanes deposit their atoms' values straight into the index-order scratch (one copy of the
+  // rotate + sample code: the slot loop is not unrolled, instruction-cache footprint)
+#pragma unroll 1
   for (int t = 0; t < NS; ++t) {
     const uint32_t a = lane + 32 * t;
-    ns[t] = 0.0;
+    const uint32_t mw = t == 0 ? mo0 : t == 1 ? mo1 : t == 2 ? mo2 : mo3;  // no dynamic array index
     if (a < n) {
-      ns[t] = ES[a];
-      if (rotate && bit4<4>(mo, a))
-        ns[t] = sample_exact(pk, rotated_about(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, pi, q));
+      double v = ES[a];
+      if (rotate && ((mw >> lane) & 1u))
+        v = sample_exact_ni(pk, rotated_about(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, pi, q));
+      scr[a] = v;
     }
   }
-  return __ddiv_rn(ordered_sum_smem<NS>(ns, n, scr, lane), double(n));
+  __syncwarp();
+  double sum = 0.0;
+  if (lane == 0) sum = serial_sum(scr, n);
+  sum = __shfl_sync(FULL, sum, 0);
+  __syncwarp();
+  return __ddiv_rn(sum, double(n));
 }
 
 }  // namespace
@@ -653,12 +689,98 @@ __global__ void __launch_bounds__(NT, 1)
                 }
               }
             };
+#if GD_K1A_X2
+            // The same samples, in pairs (quarter-turns q = 2h, 2h + 1 of one group) through the
+            // f32x2 pipe: every FP32 operation of the pair is one FADD2 / FMUL2 / FFMA2 (two
+            // lane-ops per issue slot), each element rounded exactly as the scalar form above, so
+            // the coarse values (and everything downstream) are bit-identical. Only the address
+            // arithmetic, the LDS and the byte-permute decodes stay per sample.
+            float2 acc2[2 * kQtGroups];
+  #pragma unroll
+            for (int i = 0; i < 2 * kQtGroups; ++i) acc2[i] = make_float2(0.f, 0.f);
+            float2 cs_a[kQtGroups], cs_b[kQtGroups], cs_c[kQtGroups];  // (c, -s), (-s, -c), (s, c)
+  #pragma unroll
+            for (int gi = 0; gi < kQtGroups; ++gi) {
+              cs_a[gi] = make_float2(cs[gi].x, -cs[gi].y);
+              cs_b[gi] = make_float2(-cs[gi].y, -cs[gi].x);
+              cs_c[gi] = make_float2(cs[gi].y, cs[gi].x);
+            }
+            const float2 T2x = make_float2(tx, tx), T2y = make_float2(ty, ty);
+            const float2 M2 = make_float2(kMagic, kMagic), NM2 = make_float2(-kMagic, -kMagic);
+            auto atom2 = [&](uint32_t a, auto cls_tag) {
+              constexpr int CLS = decltype(cls_tag)::value;
+              const float4 v = A[a];
+              const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
+              const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
+              const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
+              const float ez = CLS == 0 ? 0.f : fabsf(gz - cg.hz) - cg.hz;
+              if (CLS == 1) amz = fminf(amz, fabsf(ez));
+              const float rz = __fadd_rz(gz, kMagic);
+              const float fz = gz - (rz - kMagic);
+              const uint32_t zoff16 = __float_as_uint(rz) * cxy16 + base16;
+              const CellBias cb = cell_bias(fz, cg.nb);
+              bsum += cb.b0;
+              const float2 FZ = make_float2(fz, fz), NK = make_float2(-cb.k, -cb.k);
+              const float2 WX = make_float2(wx, wx), WY = make_float2(wy, wy);
+  #pragma unroll
+              for (int gi = 0; gi < kQtGroups; ++gi) {
+                // (rx, -ry) and (ry, rx): rx = c wx - s wy, ry = s wx + c wy (as the scalar form)
+                const float2 X01 = __ffma2_rn(WX, cs_a[gi], __fmul2_rn(WY, cs_b[gi]));
+                const float2 Y01 = __ffma2_rn(WX, cs_c[gi], __fmul2_rn(WY, cs_a[gi]));
+  #pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  // samples q = 2h, 2h + 1: t + (rx, ry), t + (-ry, rx) | t - (rx, ry), t + (ry, -rx)
+                  const float2 gx = h == 0 ? __fadd2_rn(T2x, X01) : __fadd2_rn(T2x, make_float2(-X01.x, -X01.y));
+                  const float2 gy = h == 0 ? __fadd2_rn(T2y, Y01) : __fadd2_rn(T2y, make_float2(-Y01.x, -Y01.y));
+                  const float2 rX = __fadd2_rz(gx, M2), rY = __fadd2_rz(gy, M2);
+                  const float2 tX = __fadd2_rn(rX, NM2), tY = __fadd2_rn(rY, NM2);  // floor(g), exact
+                  const float2 fX = __fadd2_rn(gx, make_float2(-tX.x, -tX.y));
+                  const float2 fY = __fadd2_rn(gy, make_float2(-tY.x, -tY.y));
+                  uint32_t ad0 = __float_as_uint(rY.x) * cx16 + (__float_as_uint(rX.x) * 16u + zoff16);
+                  uint32_t ad1 = __float_as_uint(rY.y) * cx16 + (__float_as_uint(rX.y) * 16u + zoff16);
+                  if (CLS == 1) {
+                    ad0 = ez < 0.0f ? ad0 : dummy16;
+                    ad1 = ez < 0.0f ? ad1 : dummy16;
+                  }
+                  if (CLS == 2) {
+                    const float e0 = fmaxf(fmaxf(fabsf(gx.x - cg.hx) - cg.hx, fabsf(gy.x - cg.hy) - cg.hy), ez);
+                    const float e1 = fmaxf(fmaxf(fabsf(gx.y - cg.hx) - cg.hx, fabsf(gy.y - cg.hy) - cg.hy), ez);
+                    amn[4 * gi + 2 * h] = fminf(amn[4 * gi + 2 * h], fabsf(e0));
+                    amn[4 * gi + 2 * h + 1] = fminf(amn[4 * gi + 2 * h + 1], fabsf(e1));
+                    ad0 = e0 < 0.0f ? ad0 : dummy16;
+                    ad1 = e1 < 0.0f ? ad1 : dummy16;
+                  }
+                  const uint4 wA = load_cell<SC>(cg, ad0), wB = load_cell<SC>(cg, ad1);
+                  const float2 c0 = __ffma2_rn(FZ, make_float2(dec_dz(wA.x), dec_dz(wB.x)), make_float2(dec_c0(wA.x), dec_c0(wB.x)));
+                  const float2 d0 = __ffma2_rn(FZ, make_float2(dec_dz(wA.y), dec_dz(wB.y)), make_float2(dec_d0(wA.y), dec_d0(wB.y)));
+                  const float2 c1 = __ffma2_rn(FZ, make_float2(dec_dz(wA.z), dec_dz(wB.z)), make_float2(dec_c0(wA.z), dec_c0(wB.z)));
+                  const float2 d1 = __ffma2_rn(FZ, make_float2(dec_dz(wA.w), dec_dz(wB.w)), make_float2(dec_d0(wA.w), dec_d0(wB.w)));
+                  const float2 x0 = __ffma2_rn(fX, d0, c0), x1 = __ffma2_rn(fX, d1, c1);
+                  const float2 dx = __fadd2_rn(x1, make_float2(-x0.x, -x0.y));
+                  const float2 r = __ffma2_rn(fY, dx, __ffma2_rn(fX, NK, x0));
+                  acc2[2 * gi + h] = __fadd2_rn(acc2[2 * gi + h], r);
+                }
+              }
+            };
+  #pragma unroll 1
+            for (uint32_t a = 0; a < nsafe; ++a) atom2(a, std::integral_constant<int, 0>{});
+  #pragma unroll 1
+            for (uint32_t a = nsafe; a < nsafe + nxy; ++a) atom2(a, std::integral_constant<int, 1>{});
+  #pragma unroll 1
+            for (uint32_t a = nsafe + nxy; a < n; ++a) atom2(a, std::integral_constant<int, 2>{});
+  #pragma unroll
+            for (int i = 0; i < 2 * kQtGroups; ++i) {
+              acc[2 * i] = acc2[i].x;
+              acc[2 * i + 1] = acc2[i].y;
+            }
+#else
   #pragma unroll 1
             for (uint32_t a = 0; a < nsafe; ++a) atom(a, std::integral_constant<int, 0>{});
   #pragma unroll 1
             for (uint32_t a = nsafe; a < nsafe + nxy; ++a) atom(a, std::integral_constant<int, 1>{});
   #pragma unroll 1
             for (uint32_t a = nsafe + nxy; a < n; ++a) atom(a, std::integral_constant<int, 2>{});
+#endif
   #pragma unroll
             for (int i = 0; i < 4 * kQtGroups; ++i) amn[i] = fminf(amn[i], amz);
   #pragma unroll
@@ -822,9 +944,9 @@ __global__ void __launch_bounds__(NT, 1)
   // One DevPocket per CTA in shared memory (with the field pointer redirected below): the exact
   // samplers take it by reference, and a per-thread copy would live in local memory
   __shared__ DevPocket spk;
-  __shared__ unsigned long long sweep_ctr[5];  // executed sweep work, see st_* below
+  __shared__ uint32_t sweep_ctr[32][5];  // per warp: executed sweep work, see st_* below
   if (threadIdx.x == 0) spk = pk_in;
-  if (threadIdx.x < 5) sweep_ctr[threadIdx.x] = 0ull;
+  if (threadIdx.x < 32 * 5) sweep_ctr[threadIdx.x / 5][threadIdx.x % 5] = 0u;
   __syncthreads();
   DevPocket& pk = spk;
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
@@ -854,7 +976,7 @@ __global__ void __launch_bounds__(NT, 1)
   // per-step cross-pair list (alpha, beta, gamma) behind SCR1, then the sweep's FP64 pose X (3 per
   // atom, atom order) and exact per-atom samples ES
   float4* PL = reinterpret_cast<float4*>(SURV + 2 * ((b.max_n + 3) & ~3u));
-  double* X = reinterpret_cast<double*>(PL + kPairCap);
+  double* X = reinterpret_cast<double*>(PL + pair_cap<NS>());
   double* ES = X + 3 * ((b.max_n + 3) & ~3u);
   float* CF = reinterpret_cast<float*>(ES + ((b.max_n + 3) & ~3u));  // step cache: fixed-side sums
   double* SCR1 = reinterpret_cast<double*>(SURV);
@@ -877,8 +999,8 @@ __global__ void __launch_bounds__(NT, 1)
   // steps with an invariant clash, steps whose candidates were scored, moved-atom samples of the
   // scored candidates, and bump cross pairs (moved x fixed x candidates) of the steps that
   // evaluated them (none under an invariant clash: the reference's bump_check stops at its first
-  // clashing pair, scoring.cpp:47-60). CTA counters in shared memory (sweep_ctr): per-warp
-  // registers here cost K1b spills.
+  // clashing pair, scoring.cpp:47-60). per-warp counters in shared memory (sweep_ctr,
+  // plain adds by lane 0; registers here cost K1b spills, shared 64-bit atomics are CAS loops).
 #ifdef GD_PHASE_TIMERS
   long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t_ph = clock64();
@@ -1063,40 +1185,44 @@ __global__ void __launch_bounds__(NT, 1)
       // 2 d |dd| with |dd| <= 2 sqrt(3) ptol, plus FP32 rounding of t^2 and the chain.
       const float tau = 16.0f * rmax * ptol + 4e-6f * rmax * rmax + 1e-6f;
 
+      // (loops over the NS atom slots are not unrolled here: one copy of each body in the code,
+      // register arrays indexed through pick/put selects)
       auto refresh = [&](bool all, const uint32_t (&mo)[NS]) {
-#pragma unroll
+#pragma unroll 1
         for (int s = 0; s < NS; ++s) {
           const uint32_t a = lane + 32 * s;
-          if (a < n && (all || bit4(mo, a))) {
+          if (a < n && (all || ((pick<NS>(mo, s) >> lane) & 1u))) {
             const V3d pa{X[3 * a], X[3 * a + 1], X[3 * a + 2]};
-            const float gx = float(__ddiv_rn(__dsub_rn(pa.x, pk.origin[0]), pk.spacing));
-            const float gy = float(__ddiv_rn(__dsub_rn(pa.y, pk.origin[1]), pk.spacing));
-            const float gz = float(__ddiv_rn(__dsub_rn(pa.z, pk.origin[2]), pk.spacing));
-            A[pos[s]] = make_float4(gx, gy, gz, rho[s]);
+            // FP32 grid coordinates (coarse path only: FP64 multiply by 1/spacing, error far
+            // below the FP32 rounding that ptol covers)
+            const float gx = float(__dmul_rn(__dsub_rn(pa.x, pk.origin[0]), pk.inv_spacing));
+            const float gy = float(__dmul_rn(__dsub_rn(pa.y, pk.origin[1]), pk.inv_spacing));
+            const float gz = float(__dmul_rn(__dsub_rn(pa.z, pk.origin[2]), pk.inv_spacing));
+            A[pick<NS>(pos, s)] = make_float4(gx, gy, gz, pick<NS>(rho, s));
             ES[a] = sample_exact_ni(pk, pa);
             float am = 1e30f;
-            cs[s] = coarse_sample(cg, gx, gy, gz, am);
-            samb[s] = am <= ptol;
+            put<NS>(cs, s, coarse_sample(cg, gx, gy, gz, am));
+            put<NS>(samb, s, am <= ptol);
           }
         }
         __syncwarp();
         bool any_amb = false;
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
+        for (int s = 0; s < NS; ++s)
 #pragma unroll
-          for (int w = 0; w < NS; ++w) {
-            crow[s][w] = 0u;
-            arow[s][w] = 0u;
-          }
+          for (int w = 0; w < NS; ++w) crow[s][w] = arow[s][w] = 0u;
+#pragma unroll 1
+        for (int s = 0; s < NS; ++s) {
           const uint32_t a = lane + 32 * s;
           if (a >= n) continue;
-          const float4 pa = A[pos[s]];
-          const uint32_t* adrow = b.adjd + it.m.adj_base + pos[s] * it.W;
-#pragma unroll
+          const uint32_t ps = pick<NS>(pos, s);
+          const float4 pa = A[ps];
+          const uint32_t* adrow = b.adjd + it.m.adj_base + ps * it.W;
+#pragma unroll 1
           for (int w = 0; w < NS; ++w) {
             if (uint32_t(w) >= it.W) break;
             // bonded partners and the atom itself are not bump pairs (scoring.cpp:53-55)
-            const uint32_t skip = __ldg(adrow + w) | (pos[s] >> 5 == uint32_t(w) ? 1u << (pos[s] & 31) : 0u);
+            const uint32_t skip = __ldg(adrow + w) | (ps >> 5 == uint32_t(w) ? 1u << (ps & 31) : 0u);
             const uint32_t qe = min(n, 32u * w + 32u);
             uint32_t cw = 0u, aw = 0u;
             for (uint32_t q = 32u * w; q < qe; ++q) {
@@ -1108,9 +1234,9 @@ __global__ void __launch_bounds__(NT, 1)
               cw |= mg < -tau ? bit : 0u;
               aw |= (mg >= -tau && mg <= tau) ? bit : 0u;
             }
-            crow[s][w] = cw & ~skip;
-            arow[s][w] = aw & ~skip;
-            any_amb |= arow[s][w] != 0u;
+            put2<NS>(crow, s, w, cw & ~skip);
+            put2<NS>(arow, s, w, aw & ~skip);
+            any_amb |= (aw & ~skip) != 0u;
           }
         }
         if (__any_sync(FULL, any_amb)) {  // near-threshold pairs: exact FP64 verdict
@@ -1155,9 +1281,9 @@ __global__ void __launch_bounds__(NT, 1)
           const uint32_t a = lane + 32 * s;
           if (a < n && bit4(mo, a)) {
             const V3d pa{X[3 * a], X[3 * a + 1], X[3 * a + 2]};
-            const float gx = float(__ddiv_rn(__dsub_rn(pa.x, pk.origin[0]), pk.spacing));
-            const float gy = float(__ddiv_rn(__dsub_rn(pa.y, pk.origin[1]), pk.spacing));
-            const float gz = float(__ddiv_rn(__dsub_rn(pa.z, pk.origin[2]), pk.spacing));
+            const float gx = float(__dmul_rn(__dsub_rn(pa.x, pk.origin[0]), pk.inv_spacing));
+            const float gy = float(__dmul_rn(__dsub_rn(pa.y, pk.origin[1]), pk.inv_spacing));
+            const float gz = float(__dmul_rn(__dsub_rn(pa.z, pk.origin[2]), pk.inv_spacing));
             A[pos[s]] = make_float4(gx, gy, gz, rho[s]);
             ES[a] = sample_exact_ni(pk, pa);
             float am = 1e30f;
@@ -1235,33 +1361,89 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       };
-      {
-        uint32_t none[NS];
+      // rotamer r's bond (i, j), DFS range (s0, e0) and DFS position of atom_i
+      auto rot_info = [&](uint32_t rr, uint2& ij_, uint32_t& s0_, uint32_t& e0_, uint32_t& ip_) {
+        if (rr < 32) {
+          const uint32_t pij = __shfl_sync(FULL, rc_ij, rr), pse = __shfl_sync(FULL, rc_se, rr);
+          ij_ = make_uint2(pij & 0xffffu, pij >> 16);
+          s0_ = pse & 0xffffu;
+          e0_ = pse >> 16;
+          ip_ = __shfl_sync(FULL, rc_ip, rr);
+        } else {
+          ij_ = b.rots[it.m.rot_base + rr];
+          const ushort4 rd = b.rdfs[it.m.rot_base + rr];
+          s0_ = rd.x;
+          e0_ = rd.y;
+          ip_ = rd.z;
+        }
+      };
+      // M' = moving set minus atom_j (molecule.cpp:166-169) of rotamer rr, in original (mo) and
+      // DFS (md) bit spaces, and this lane's membership (inm). Fast layout: M' is the DFS range
+      // (s0, e0), so both follow from the range.
+      auto rot_masks = [&](uint32_t rr, uint2 ij_, uint32_t s0_, uint32_t e0_, uint32_t (&mo_)[NS],
+                           uint32_t (&md_)[NS], bool (&inm_)[NS]) {
+        if (it.m.fast_ok) {
 #pragma unroll
-        for (int w = 0; w < NS; ++w) none[w] = 0u;
-        GD_T(3);
-        refresh(true, none);
-      }
+          for (int s = 0; s < NS; ++s) {
+            inm_[s] = lane + 32 * s < n && pos[s] > s0_ && pos[s] < e0_;
+            mo_[s] = __ballot_sync(FULL, inm_[s]);  // slot s holds atoms 32 s + lane
+            md_[s] = range_word(uint32_t(s), s0_ + 1, e0_);
+          }
+        } else {
+#pragma unroll
+          for (int w = 0; w < NS; ++w) {
+            mo_[w] = uint32_t(w) < it.W ? __ldg(b.masks + it.m.mask_base + rr * it.W + w) : 0u;
+            md_[w] = 0u;
+          }
+#pragma unroll
+          for (int w = 0; w < NS; ++w)
+            if ((ij_.y >> 5) == uint32_t(w)) mo_[w] &= ~(1u << (ij_.y & 31));
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const uint32_t a = lane + 32 * s;
+            inm_[s] = a < n && bit4(mo_, a);
+#pragma unroll
+            for (int w = 0; w < NS; ++w)
+              if (inm_[s] && (pos[s] >> 5) == uint32_t(w)) md_[w] |= 1u << (pos[s] & 31);
+          }
+#pragma unroll
+          for (int w = 0; w < NS; ++w)
+            for (int o = 16; o > 0; o >>= 1) md_[w] |= __shfl_xor_sync(FULL, md_[w], o);
+        }
+      };
 
+      // The per-pose caches are rebuilt at ONE place, the top of the next step (one inlined copy
+      // of refresh in the kernel's code): the aligned pose (all atoms) before the
+      // first step, the atoms rotamer pend_r moved after a k != 0 commit.
+      constexpr uint32_t kRefreshAll = 0xffffffffu, kRefreshNone = 0xfffffffeu;
+      uint32_t pend_r = kRefreshAll;
       uint32_t vmask = 0u;  // step cache (rotamers r < 32): valid entries of CF
       for (uint32_t rep = 0; rep < pr.reps; ++rep) {
         for (uint32_t r = 0; r < R; ++r) {
+          if (pend_r != kRefreshNone) {
+            GD_T(3);
+            uint32_t pmo[NS], pmd[NS];
+            uint32_t ps0 = 0, pe0 = 0;
+            if (pend_r == kRefreshAll) {
+#pragma unroll
+              for (int w = 0; w < NS; ++w) pmo[w] = pmd[w] = 0u;
+            } else {
+              uint2 pij;
+              uint32_t pip;
+              bool pinm[NS];
+              rot_info(pend_r, pij, ps0, pe0, pip);
+              rot_masks(pend_r, pij, ps0, pe0, pmo, pmd, pinm);
+            }
+            // the cross-pair update pays off from NS = 4 (n > 64: C4 at clash 0.1 +13 %); at
+            // NS <= 2 the full row pass is cheaper than the per-atom votes (C2 at clash 0.1 -5 %)
+            if (NS >= 4 && it.m.fast_ok && pend_r != kRefreshAll) refresh_cross(pmo, pmd, ps0, pe0);
+            else refresh(pend_r == kRefreshAll, pmo);
+            pend_r = kRefreshNone;
+          }
           GD_T(4);
           uint2 ij;
           uint32_t s0, e0, ipos;
-          if (r < 32) {
-            const uint32_t pij = __shfl_sync(FULL, rc_ij, r), pse = __shfl_sync(FULL, rc_se, r);
-            ij = make_uint2(pij & 0xffffu, pij >> 16);
-            s0 = pse & 0xffffu;
-            e0 = pse >> 16;
-            ipos = __shfl_sync(FULL, rc_ip, r);
-          } else {
-            ij = b.rots[it.m.rot_base + r];
-            const ushort4 rd = b.rdfs[it.m.rot_base + r];
-            s0 = rd.x;
-            e0 = rd.y;
-            ipos = rd.z;
-          }
+          rot_info(r, ij, s0, e0, ipos);
           // M' = moving set minus atom_j (molecule.cpp:166-169), original (mo) and DFS (md) bit
           // spaces. Fast layout: M' is the DFS range (s0, e0), so both follow from the range.
           // Step cache: a rotamer whose last visit saw an invariant clash (fast layout, no razor
@@ -1293,36 +1475,7 @@ __global__ void __launch_bounds__(NT, 1)
               inm[s] = false;
             }
           } else {
-          // M' = moving set minus atom_j (molecule.cpp:166-169), original (mo) and DFS (md) bit
-            // spaces. Fast layout: M' is the DFS range (s0, e0), so both follow from the range.
-              if (it.m.fast_ok) {
-#pragma unroll
-              for (int s = 0; s < NS; ++s) {
-                inm[s] = lane + 32 * s < n && pos[s] > s0 && pos[s] < e0;
-                mo[s] = __ballot_sync(FULL, inm[s]);  // slot s holds atoms 32 s + lane
-                md[s] = range_word(uint32_t(s), s0 + 1, e0);
-              }
-            } else {
-#pragma unroll
-              for (int w = 0; w < NS; ++w) {
-                mo[w] = uint32_t(w) < it.W ? __ldg(b.masks + it.m.mask_base + r * it.W + w) : 0u;
-                md[w] = 0u;
-              }
-#pragma unroll
-              for (int w = 0; w < NS; ++w)
-                if ((ij.y >> 5) == uint32_t(w)) mo[w] &= ~(1u << (ij.y & 31));
-#pragma unroll
-              for (int s = 0; s < NS; ++s) {
-                const uint32_t a = lane + 32 * s;
-                inm[s] = a < n && bit4(mo, a);
-#pragma unroll
-                for (int w = 0; w < NS; ++w)
-                  if (inm[s] && (pos[s] >> 5) == uint32_t(w)) md[w] |= 1u << (pos[s] & 31);
-              }
-#pragma unroll
-              for (int w = 0; w < NS; ++w)
-                for (int o = 16; o > 0; o >>= 1) md[w] |= __shfl_xor_sync(FULL, md[w], o);
-            }
+            rot_masks(r, ij, s0, e0, mo, md, inm);
             // invariant pairs (both in M' or both outside) of the current pose: exact from crow
             bool inv_l = false, frag_l = false, cne_l = false;
 #pragma unroll
@@ -1375,13 +1528,13 @@ __global__ void __launch_bounds__(NT, 1)
             const uint32_t n_k = pr.S > 0 ? pr.S - 1 : 0;
             const bool slow = !it.m.fast_ok || frag || pr.S > 64 || pr.S < 2;
             if (lane == 0) {
-              atomicAdd(&sweep_ctr[0], 1ull);
-              if (inv) atomicAdd(&sweep_ctr[1], 1ull);
-              if (slow || !(skip_inv && inv)) {
-                atomicAdd(&sweep_ctr[2], 1ull);
-                atomicAdd(&sweep_ctr[3], (unsigned long long)(nm_c * n_k));
-                if (!inv || frag) atomicAdd(&sweep_ctr[4], (unsigned long long)(nm_c * (n - nm_c - 1) * n_k));
-              }
+              uint32_t* c = sweep_ctr[warp];
+              const bool scored = slow || !(skip_inv && inv);
+              c[0] += 1u;
+              c[1] += inv ? 1u : 0u;
+              c[2] += scored ? 1u : 0u;
+              c[3] += scored ? nm_c * n_k : 0u;
+              c[4] += scored && (!inv || frag) ? nm_c * (n - nm_c - 1) * n_k : 0u;
             }
           }
           int32_t step_k = -1;
@@ -1476,7 +1629,10 @@ __global__ void __launch_bounds__(NT, 1)
                 __syncwarp();
                 cnt = 0;
               };
-              for (uint32_t mq = s0 + 1; mq < e0; ++mq) {
+              // one fold call site: before each moved atom when its pairs might not fit, and at the end
+              for (uint32_t mq = s0 + 1;; ++mq) {
+                if (mq >= e0 || cnt + 32u * NS > pair_cap<NS>()) fold();
+                if (mq >= e0) break;
                 const float4 pm = A[mq];
                 const float ux = pm.x - fpi.x, uy = pm.y - fpi.y, uz = pm.z - fpi.z;
                 const float hm = fmaf(ux, ax, fmaf(uy, ay, uz * az));
@@ -1489,7 +1645,6 @@ __global__ void __launch_bounds__(NT, 1)
                   const bool fixed = q < n && (q < s0 || q >= e0);
                   const float dh = hq[t] - hm, dr = rq[t] - rm, tt = tq[t] + pm.w, T = tt + 1e-3f;
                   const bool surv = fixed && fmaf(dh, dh, dr * dr) < T * T;
-                  if (cnt + 32u > kPairCap) fold();  // room for this slot's (<= 32) new pairs
                   const uint32_t ball = __ballot_sync(FULL, surv);
                   if (surv) {
                     const float al = fmaf(dh, dh, fmaf(rq[t], rq[t], fmaf(-tt, tt, rm2)));
@@ -1500,7 +1655,6 @@ __global__ void __launch_bounds__(NT, 1)
                   cnt += __popc(ball);
                 }
               }
-              fold();
             }
             float res_s[2] = {-1e30f, -1e30f};
             uint32_t res_st[2] = {0u, 0u};
@@ -1573,18 +1727,26 @@ __global__ void __launch_bounds__(NT, 1)
               bk = 0;
               bs = score;
             } else if (!inv) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {  // cross pairs within tau of the threshold: exact
-                uint32_t pend = __ballot_sync(FULL, (res_st[h] & ST_XAMB) != 0u);
+              // Both passes' candidates go through one loop (bit 32 h + lane: pass h, lane's k),
+              // so each exact path below exists once in the kernel's code (instruction-cache
+              // footprint of the step), in ascending k.
+              {  // cross pairs within tau of the threshold: exact
+                unsigned long long pend = __ballot_sync(FULL, (res_st[0] & ST_XAMB) != 0u) |
+                                          (uint64_t(__ballot_sync(FULL, (res_st[1] & ST_XAMB) != 0u)) << 32);
                 while (pend) {
-                  const uint32_t src = __ffs(pend) - 1;
+                  const uint32_t bit = uint32_t(__ffsll(static_cast<long long>(pend)) - 1);
                   pend &= pend - 1;
+                  const uint32_t src = bit & 31u, h = bit >> 5;
                   const uint32_t k = (h == 0 ? 1u : 33u) + src;
                   ++st_sexact;
                   get_axis();
                   const bool cl = exact_clash_g<NS>(b, it.m.atom_base, it.m.adj_base, n, X, GD_MO4(mo), true, pi,
                                                     frag_quat(pr.dtab[k], axis), pr.clash, true, lane);
-                  if (lane == src) res_st[h] = (res_st[h] & (ST_SAMB | ST_ALLOUT)) | (cl ? ST_CLASH : ST_OK);
+                  const uint32_t nst = cl ? ST_CLASH : ST_OK;
+                  if (lane == src) {
+                    if (h == 0) res_st[0] = (res_st[0] & (ST_SAMB | ST_ALLOUT)) | nst;
+                    else res_st[1] = (res_st[1] & (ST_SAMB | ST_ALLOUT)) | nst;
+                  }
                 }
               }
               // Relative screening: all candidates share the fixed atoms (same coarse and exact
@@ -1616,19 +1778,20 @@ __global__ void __launch_bounds__(NT, 1)
                 bs = score;
               }
               bool allout_done = false;  // candidates with every moved atom clearly outside tie exactly
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const bool need = (res_st[h] & ST_OK) && ((res_st[h] & ST_SAMB) || res_s[h] >= thr_k);
-                uint32_t pend = __ballot_sync(FULL, need);
-                const uint32_t allout = __ballot_sync(FULL, (res_st[h] & ST_ALLOUT) != 0u);
+              {
+                const bool need0 = (res_st[0] & ST_OK) && ((res_st[0] & ST_SAMB) || res_s[0] >= thr_k);
+                const bool need1 = (res_st[1] & ST_OK) && ((res_st[1] & ST_SAMB) || res_s[1] >= thr_k);
+                unsigned long long pend = __ballot_sync(FULL, need0) | (uint64_t(__ballot_sync(FULL, need1)) << 32);
+                const unsigned long long allout = __ballot_sync(FULL, (res_st[0] & ST_ALLOUT) != 0u) |
+                                                  (uint64_t(__ballot_sync(FULL, (res_st[1] & ST_ALLOUT) != 0u)) << 32);
                 while (pend) {
-                  const uint32_t src = __ffs(pend) - 1;
+                  const uint32_t bit = uint32_t(__ffsll(static_cast<long long>(pend)) - 1);
                   pend &= pend - 1;
-                  if ((allout >> src) & 1u) {
+                  if ((allout >> bit) & 1ull) {
                     if (allout_done) continue;
                     allout_done = true;
                   }
-                  const uint32_t k = (h == 0 ? 1u : 33u) + src;
+                  const uint32_t k = ((bit >> 5) == 0 ? 1u : 33u) + (bit & 31u);
                   ++st_sexact;
                   get_axis();
                   const double sk = exact_candidate_score_g<NS>(pk, n, X, ES, GD_MO4(mo), true, pi,
@@ -1660,10 +1823,7 @@ __global__ void __launch_bounds__(NT, 1)
                   X[3 * a + 2] = v.z;
                 }
               __syncwarp();
-              // the cross-pair update pays off from NS = 4 (n > 64: C4 at clash 0.1 +13 %); at
-              // NS <= 2 the full row pass is cheaper than the per-atom votes (C2 at clash 0.1 -5 %)
-              if (NS >= 4 && it.m.fast_ok) refresh_cross(mo, md, s0, e0);
-              else refresh(false, mo);
+              pend_r = r;  // the caches of the moved atoms are rebuilt at the top of the next step
               vmask = 0u;  // the pose changed: every cached step head is stale
             }
           }
@@ -1675,7 +1835,16 @@ __global__ void __launch_bounds__(NT, 1)
     if (*(volatile int*)b.error != 0) break;
     GD_T(7);
     // ------------------------------------------------ restart result (K2 replays its pose)
-    if (lane == 0) b.rs_score[item] = score;
+    if (lane == 0) {
+      b.rs_score[item] = score;
+      uint32_t* c = sweep_ctr[warp];
+      if ((c[3] | c[4]) >= 0x80000000u) {  // keep the 32-bit per-warp counters far from wrapping
+        for (int i = 0; i < 5; ++i) {
+          atomicAdd(b.stats + 16 + i, (unsigned long long)c[i]);
+          c[i] = 0u;
+        }
+      }
+    }
     __syncwarp();
   }
   if (lane == 0) {
@@ -1691,7 +1860,11 @@ __global__ void __launch_bounds__(NT, 1)
 #endif
   }
   __syncthreads();
-  if (threadIdx.x < 5) atomicAdd(b.stats + 16 + threadIdx.x, sweep_ctr[threadIdx.x]);
+  if (threadIdx.x < 5) {
+    unsigned long long t = 0ull;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) t += sweep_ctr[w][threadIdx.x];
+    atomicAdd(b.stats + 16 + threadIdx.x, t);
+  }
 }
 
 // Shared-memory plan of one persistent kernel: the pocket cells (when they fit next to 8 warp
@@ -1740,7 +1913,7 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   const uint32_t npad_max = (b.max_n + 3) & ~3u;
   const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
   // A (4 floats/atom) + SCR1 (1 double/atom) + PL + X (3 doubles/atom) + ES (1 double/atom)
-  const uint32_t slot_b = 6 * npad_max + 4 * kPairCap + 8 * npad_max + 32;
+  const uint32_t slot_b = 6 * npad_max + 4 * pair_cap<NS>() + 8 * npad_max + 32;
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
   // cells in shared memory: issue-bound, 16 warps x 128 registers; cells through L1 (large grids):
   // 12 warps x 151 registers (C5 +4 %)
@@ -1755,7 +1928,7 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
     if ((e = cudaStreamWaitEvent(stream_b, mid, 0)) != cudaSuccess) return e;
     stream = stream_b;
   }
-  constexpr size_t kK1bStatic = 256;  // the kernel's __shared__ DevPocket, rounded up
+  constexpr size_t kK1bStatic = 1024;  // the kernel's __shared__ DevPocket + per-warp counters, rounded up
   SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC, kK1bStatic);
   if (pb.warps < 1) return cudaErrorInvalidConfiguration;
   // the FP64 field goes to shared memory too when it fits beside the slots (24^3: 110 KB)

@@ -37,6 +37,7 @@ struct DevPocket {
   uint32_t cell_dims[3]; // dims - 1
   double origin[3];
   double spacing;
+  double inv_spacing;    // 1 / spacing (FP32 grid coordinates of the coarse path only)
   double maxc[3];        // dims - 1 as doubles (sample_field's outside test, scoring.cpp:16-18)
   float inv_spacing_f;
   float q_eps;           // quantisation bound of one coarse sample (inf: fast path off)
