@@ -35,10 +35,13 @@ extern "C" {
 #define GD_ERR_DEGENERATE_AXIS 4 /* DegenerateAxisError (molecule.cpp:156-158)                 */
 #define GD_ERR_CUDA 5            /* device / runtime failure (no CPU fallback exists)           */
 #define GD_ERR_NO_POCKET 6       /* gd_dock_* before gd_set_pocket                              */
-#define GD_ERR_UNSUPPORTED 7     /* ligand larger than the kernel's atom limit (GD_MAX_ATOMS)   */
+#define GD_ERR_UNSUPPORTED 7     /* ligand larger than GD_MAX_ATOMS (the FP64 kernel's per-warp
+                                    shared-memory pose, 7 doubles per atom in 200 KB)          */
 #define GD_ERR_PARSE 8           /* ParseError        (errors.hpp:15-27): malformed .lgd text     */
 
-#define GD_MAX_ATOMS 256          /* per ligand; the reference has no fixed limit               */
+#define GD_MAX_ATOMS 3584         /* per ligand (the reference has no fixed limit): <= 128 atoms
+                                    run the two-stage fast kernels, 129..256 the coarse K1a screen
+                                    + the FP64 sweep, larger ones the all-FP64 kernel             */
 #define GD_MAX_ROTAMERS 128       /* kMaxRotamers, molecule.hpp:29                              */
 
 typedef struct gd_ctx gd_ctx;

@@ -17,6 +17,7 @@
 // rotations; dihedral sweep = lanes over candidate angles k (32 per pass, the remainder split
 // 2..32 lanes per candidate over the fixed atoms); FP64 master pose = atom a lives in lane a%32,
 // register slot a/32.
+#include <algorithm>
 #include <type_traits>
 
 #include "gd_exact.cuh"
@@ -40,6 +41,9 @@ constexpr int kAlignUnroll = GD_ALIGN_UNROLL;
 #define GD_ALPHA_CHUNK 4
 #endif
 constexpr int kAlphaChunk = GD_ALPHA_CHUNK;
+#ifndef GD_CROSS_REFRESH_MIN_NS
+#define GD_CROSS_REFRESH_MIN_NS 4  // after a commit: incremental cross-pair rows from this NS up (NS = 2: full rows, -18 % time)
+#endif
 #ifndef GD_K1A_X2
 #define GD_K1A_X2 1  // K1a samples in f32x2 pairs (bit-identical to the scalar form)
 #endif
@@ -329,7 +333,14 @@ struct Item {
 
 // The exact FP64 sampler and whole-rotation scorer are out-of-line: they run on rare paths and
 // inlining them at every call site blew the kernel past the instruction cache.
+#ifndef GD_SAMPLE_NOINLINE
+#define GD_SAMPLE_NOINLINE 1
+#endif
+#if GD_SAMPLE_NOINLINE
 __device__ __noinline__ double sample_exact_ni(const DevPocket& pk, V3d p) { return sample_exact(pk, p); }
+#else
+__device__ __forceinline__ double sample_exact_ni(const DevPocket& pk, V3d p) { return sample_exact(pk, p); }
+#endif
 
 // best_rotation_in_range's score of rotation q (docking.cpp:77-83), atoms in index order.
 __device__ __noinline__ double exact_rotation_score(const DevPocket& pk, const double* gpose, uint32_t n, V3d cen,
@@ -392,6 +403,8 @@ __device__ __forceinline__ bool exact_clash_g(const DevBatch& b, uint32_t atom_b
 // Exact score of dihedral candidate k (score_pose, scoring.cpp:40-45): M' atoms rotated by q about
 // pi and sampled in FP64 (none when rotate is false: the current pose, k = 0), the others from the
 // exact per-atom cache, summed in atom order.
+// scr[a] keeps every atom's value until the next call: the caller copies the moved atoms' new
+// exact samples of its best candidate from there (a k != 0 commit stores them as the pose's ES).
 template <int NS>
 __device__ __forceinline__ double exact_candidate_score_g(const DevPocket& pk, uint32_t n, const double* X,
                                                        const double* ES, uint32_t mo0, uint32_t mo1, uint32_t mo2,
@@ -979,6 +992,7 @@ __global__ void __launch_bounds__(NT, 1)
   double* X = reinterpret_cast<double*>(PL + pair_cap<NS>());
   double* ES = X + 3 * ((b.max_n + 3) & ~3u);
   float* CF = reinterpret_cast<float*>(ES + ((b.max_n + 3) & ~3u));  // step cache: fixed-side sums
+  double* BEST = reinterpret_cast<double*>(CF + 32);  // best candidate's moved-atom exact samples
   double* SCR1 = reinterpret_cast<double*>(SURV);
   double* SCR3 = reinterpret_cast<double*>(A);
   const CoarseGrid cg{cells,
@@ -1199,7 +1213,7 @@ __global__ void __launch_bounds__(NT, 1)
             const float gy = float(__dmul_rn(__dsub_rn(pa.y, pk.origin[1]), pk.inv_spacing));
             const float gz = float(__dmul_rn(__dsub_rn(pa.z, pk.origin[2]), pk.inv_spacing));
             A[pick<NS>(pos, s)] = make_float4(gx, gy, gz, pick<NS>(rho, s));
-            ES[a] = sample_exact_ni(pk, pa);
+            if (all) ES[a] = sample_exact_ni(pk, pa);  // after a commit ES is already the new one
             float am = 1e30f;
             put<NS>(cs, s, coarse_sample(cg, gx, gy, gz, am));
             put<NS>(samb, s, am <= ptol);
@@ -1284,8 +1298,7 @@ __global__ void __launch_bounds__(NT, 1)
             const float gx = float(__dmul_rn(__dsub_rn(pa.x, pk.origin[0]), pk.inv_spacing));
             const float gy = float(__dmul_rn(__dsub_rn(pa.y, pk.origin[1]), pk.inv_spacing));
             const float gz = float(__dmul_rn(__dsub_rn(pa.z, pk.origin[2]), pk.inv_spacing));
-            A[pos[s]] = make_float4(gx, gy, gz, rho[s]);
-            ES[a] = sample_exact_ni(pk, pa);
+            A[pos[s]] = make_float4(gx, gy, gz, rho[s]);  // (ES: stored by the commit)
             float am = 1e30f;
             cs[s] = coarse_sample(cg, gx, gy, gz, am);
             samb[s] = am <= ptol;
@@ -1434,9 +1447,9 @@ __global__ void __launch_bounds__(NT, 1)
               rot_info(pend_r, pij, ps0, pe0, pip);
               rot_masks(pend_r, pij, ps0, pe0, pmo, pmd, pinm);
             }
-            // the cross-pair update pays off from NS = 4 (n > 64: C4 at clash 0.1 +13 %); at
-            // NS <= 2 the full row pass is cheaper than the per-atom votes (C2 at clash 0.1 -5 %)
-            if (NS >= 4 && it.m.fast_ok && pend_r != kRefreshAll) refresh_cross(pmo, pmd, ps0, pe0);
+            // after a commit only the rows' cross-pair bits change: the incremental update walks
+            // the moved atoms instead of recomputing all n^2 pairs (GD_CROSS_REFRESH_MIN_NS)
+            if (NS >= GD_CROSS_REFRESH_MIN_NS && it.m.fast_ok && pend_r != kRefreshAll) refresh_cross(pmo, pmd, ps0, pe0);
             else refresh(pend_r == kRefreshAll, pmo);
             pend_r = kRefreshNone;
           }
@@ -1542,6 +1555,12 @@ __global__ void __launch_bounds__(NT, 1)
           bool committed = false;
           uint32_t bk = 0;
           double bs = 0.0;
+          // the moved atoms' exact samples of the best candidate so far, from the scorer's scratch
+          auto keep_best = [&]() {
+#pragma unroll
+            for (int t = 0; t < NS; ++t)
+              if (inm[t]) BEST[lane + 32 * t] = SCR1[lane + 32 * t];
+          };
 
           if (!it.m.fast_ok || frag || pr.S > 64 || pr.S < 2) {
             // ---------------- slow path: every candidate exactly (non-tree layouts, pairs of the
@@ -1561,6 +1580,7 @@ __global__ void __launch_bounds__(NT, 1)
                 committed = true;
                 bk = k;
                 bs = sk;
+                keep_best();
               }
             }
           } else if (!(skip_inv && inv)) {
@@ -1800,6 +1820,7 @@ __global__ void __launch_bounds__(NT, 1)
                     committed = true;
                     bk = k;
                     bs = sk;
+                    keep_best();
                   }
                 }
               }
@@ -1821,6 +1842,9 @@ __global__ void __launch_bounds__(NT, 1)
                   X[3 * a] = v.x;
                   X[3 * a + 1] = v.y;
                   X[3 * a + 2] = v.z;
+                  // the exact sample of the new position: computed (bit for bit: same FP64
+                  // rotation, same sampler) when candidate bk was scored exactly
+                  ES[a] = BEST[a];
                 }
               __syncwarp();
               pend_r = r;  // the caches of the moved atoms are rebuilt at the top of the next step
@@ -1913,7 +1937,7 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   const uint32_t npad_max = (b.max_n + 3) & ~3u;
   const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
   // A (4 floats/atom) + SCR1 (1 double/atom) + PL + X (3 doubles/atom) + ES (1 double/atom)
-  const uint32_t slot_b = 6 * npad_max + 4 * pair_cap<NS>() + 8 * npad_max + 32;
+  const uint32_t slot_b = 6 * npad_max + 4 * pair_cap<NS>() + 8 * npad_max + 32 + 2 * npad_max;
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
   // cells in shared memory: issue-bound, 16 warps x 128 registers; cells through L1 (large grids):
   // 12 warps x 151 registers (C5 +4 %)
@@ -1956,7 +1980,8 @@ cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch
 
 cudaError_t launch_align_big(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                              cudaStream_t stream) {
-  const uint32_t slot_a = 4 * ((b.max_n + 3) & ~3u);
+  // (ligands beyond kAlignBigMaxAtoms are skipped by the kernel: the FP64 kernel aligns them)
+  const uint32_t slot_a = 4 * ((std::min(b.max_n, kAlignBigMaxAtoms) + 3) & ~3u);
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS / 32, 8);
   const SmemPlan pg = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS_L1 / 32, 8);
   return pa.cells_in_smem

@@ -10,9 +10,8 @@
 
 namespace gdk {
 
-constexpr int kMaxAtoms = 256;
-constexpr uint32_t kFastMaxAtoms = 128;  // the fast kernels keep <= 128 atoms per warp in registers      // GD_MAX_ATOMS
-constexpr int kMaxWords = kMaxAtoms / 32;
+constexpr uint32_t kFastMaxAtoms = 128;  // the fast kernels keep <= 128 atoms per warp in registers
+constexpr uint32_t kAlignBigMaxAtoms = 256;  // K1a's coarse screen (NS = 8) for the FP64 sweep's ligands
 constexpr int kAlignCand = 64;      // alignment candidates handed from K1a to K1b per restart
 
 // Per-ligand metadata (32 B, one coalesced load per warp).

@@ -12,6 +12,8 @@
 // and dock_fast_kernel (gd_fast.cuh: FP32 coarse screen + FP64 refinement). DESIGN.md §3.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "gd_exact.cuh"
 #include "gd_fast.cuh"
 #include "gd_internal.h"
@@ -76,7 +78,8 @@ __global__ void __launch_bounds__(1024, 1)
     if (n < min_n) continue;  // mixed batch: the fast kernels' ligand
     // min_n > 0: K1a (NS = 8) ran for these ligands; its candidate list (ncand >= 0) contains
     // every rotation that can be the exact argmax
-    const int32_t ncand = min_n > 0 ? b.rs_ncand[item] : -1;
+    // (ligands beyond kAlignBigMaxAtoms had no K1a: every rotation in FP64)
+    const int32_t ncand = min_n > 0 && n <= kAlignBigMaxAtoms ? b.rs_ncand[item] : -1;
 
     // ---- starting pose (docking.cpp:52-69); q and target come from the host packer (libm).
     for (uint32_t a = lane; a < n; a += 32) {
@@ -404,9 +407,15 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
   }
   if (ev && (e = cudaEventRecord(ev[2], stream)) != cudaSuccess) return e;
   if (b.n_lig > 0) {
-    const uint32_t threads = 128;  // 4 warps, one ligand each, 3 max_n doubles of pose per warp
+    // up to 4 warps, one ligand each, 3 max_n doubles of pose per warp (within 200 KB)
+    const size_t per_warp = 3 * size_t(b.max_n) * sizeof(double);
+    const uint32_t warps = uint32_t(std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / per_warp)));
+    const uint32_t threads = 32 * warps;
     const uint32_t blocks = (b.n_lig * 32 + threads - 1) / threads;
-    const size_t smem = size_t(threads / 32) * 3 * b.max_n * sizeof(double);
+    const size_t smem = size_t(warps) * per_warp;
+    if (smem > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) != cudaSuccess)
+      return e;
     finalize_kernel<<<blocks, threads, smem, stream>>>(pr, b);
     ++*launches;
   }

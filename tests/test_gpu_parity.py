@@ -114,6 +114,32 @@ def test_edge_cases_match_oracle(ctx, port):
         assert np.array_equal(out.step_k, ref.step_k), spec
 
 
+@pytest.mark.parametrize("atoms,rots", [(300, 12), (1000, 24)])
+def test_large_ligands_match_oracle(ctx, port, atoms, rots):
+    """The reference has no atom cap (only kMaxRotamers = 128, molecule.hpp:29). Ligands beyond
+    256 atoms run the all-FP64 kernel (alignment included); in a mixed batch the others keep their
+    fast kernels. Bit-exact against the oracle, including the clash-0.1 commit path."""
+    from oracle import Params
+    pocket = gd.make_pocket()
+    small = gd.make_library(gd.LibrarySpec(3, 40, 8, 1))
+    big = gd.make_library(gd.LibrarySpec(1, atoms, rots, 11))
+    mid = gd.make_library(gd.LibrarySpec(1, 200, 16, 12))
+    lib = gd.Library.from_ligands([small.ligand(0), big.ligand(0), small.ligand(1), mid.ligand(0), small.ligand(2)])
+    p = gd.DockParams(n_restarts=2, num_repetitions=1, rotation_steps=(8, 8, 4), dihedral_steps=6, clash_factor=0.1)
+    out = ctx.dock(lib, pocket, p, trace=True)
+    ref = port.dock(lib, pocket, Params(**p.__dict__), trace=True)
+    for k_out, k_ref in [("best_score", "best_score"), ("best_restart", "best_restart"), ("final_xyz", "final_xyz"),
+                         ("final_dihedrals", "final_dih"), ("align_index", "align_index"), ("step_k", "step_k")]:
+        assert np.array_equal(getattr(out, k_out), getattr(ref, k_ref)), k_out
+    assert (out.step_k > 0).any()  # commits happened
+
+
+def test_atom_limit_is_reported(ctx):
+    big = gd.make_library(gd.LibrarySpec(1, 3585, 0, 3))
+    with pytest.raises(gd.GeoDockError, match="supports up to 3584"):
+        ctx.dock(big, gd.make_pocket(), gd.DockParams(n_restarts=1, rotation_steps=(1, 1, 1)))
+
+
 def test_uniform_field_ties_to_lowest_index(ctx, port):
     """docking_test.cpp:138-155: on a uniform field every fully-inside orientation scores exactly 1.0,
     so the lowest such grid index must win (exact-tie handling of the argmax)."""
