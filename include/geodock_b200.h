@@ -127,6 +127,11 @@ typedef struct {
   uint64_t sweep_scored_steps;    /* steps whose S-1 candidates were scored                */
   uint64_t sweep_samples;         /* moved-atom samples of the scored candidates           */
   uint64_t cross_pairs;           /* bump cross pairs (moved x fixed x candidate) evaluated */
+  uint64_t sweep_moves;           /* k != 0 commits (the pose changed: its caches are refreshed) */
+  uint64_t step_exact_score_evals;  /* FP64 candidate scores: near the best coarse score     */
+  uint64_t step_exact_allout_evals; /* FP64 candidate scores: every moved atom outside (one per step) */
+  uint64_t step_exact_face_evals;   /* FP64 candidate scores: a moved atom within ptol of a face */
+  uint64_t step_exact_clash_evals;  /* FP64 cross-pair checks of candidates near the bump threshold */
 } gd_stats;
 
 /* Kernel variants. FAST = two-stage (FP32 coarse screen + exact FP64 refinement, bit-identical

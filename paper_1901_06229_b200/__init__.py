@@ -106,7 +106,10 @@ class _Stats(C.Structure):
                 ("launches", C.c_uint32), ("exact_fallback", C.c_uint32),
                 ("align_second_passes", C.c_uint64), ("sweep_steps", C.c_uint64),
                 ("sweep_invariant_steps", C.c_uint64), ("sweep_scored_steps", C.c_uint64),
-                ("sweep_samples", C.c_uint64), ("cross_pairs", C.c_uint64)]
+                ("sweep_samples", C.c_uint64), ("cross_pairs", C.c_uint64),
+                ("sweep_moves", C.c_uint64), ("step_exact_score_evals", C.c_uint64),
+                ("step_exact_allout_evals", C.c_uint64), ("step_exact_face_evals", C.c_uint64),
+                ("step_exact_clash_evals", C.c_uint64)]
 
 
 _lib = None

@@ -6,6 +6,7 @@
 // the reference's own FP64 formulas evaluated with the same libm, so the device sees the same
 // bits the reference computes (compiled with -ffp-contract=off, no -march).
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <atomic>
 #include <condition_variable>
@@ -149,6 +150,8 @@ struct gd_ctx {
   double4* d_grid = nullptr;
   float4* d_grid_f = nullptr;
   float4* d_frames = nullptr;
+  uint32_t* d_frame_tab = nullptr;  // K1a frame schedule: kept frames + twin table (upload_grid_f)
+  uint32_t n_kept = 0;
   double4* d_dtab = nullptr;
   float2* d_dtab_f = nullptr;
   uint32_t G = 0;
@@ -358,6 +361,75 @@ int upload_grid_f(gd_ctx* ctx) {
   ctx->d_frames = nullptr;
   GD_CUDA(ctx, cudaMalloc(&ctx->d_frames, sizeof(float4) * fr.size()));
   GD_CUDA(ctx, cudaMemcpy(ctx->d_frames, fr.data(), sizeof(float4) * fr.size(), cudaMemcpyHostToDevice));
+  // Twin frames (the coarse alignment screens each distinct rotation once): frame f
+  // is a twin of an earlier kept frame f0 with alpha shift s when F_f = Rz(alpha_s) F_f0, so that
+  // R(i, f) = Rz(alpha_i) F_f = R((i + s) mod a, f0). On the default 16 x 16 x 8 grid the beta = 0 and
+  // beta = pi rows collapse this way (14 of 128 frames; the 2048 rotations hold 1840 distinct
+  // quaternions). Table layout (u32): [0, nf) per frame: (twin list offset << 8) | twin count for a
+  // kept frame, 0xffffffff for a twin; [nf, nf + n_kept) the kept frames in index order; then the
+  // twin lists, (f' | s << 16). The exact FP64 re-scoring in K1b scores every twin itself.
+  {
+    const uint32_t na = st[0];
+    std::vector<std::array<double, 9>> fm(nf);
+    for (unsigned j = 0; j < st[1]; ++j) {
+      const double beta = st[1] == 1 ? 0.0 : gdh::kPi * static_cast<double>(j) / static_cast<double>(st[1] - 1);
+      for (unsigned k = 0; k < st[2]; ++k) {
+        const double gamma = gdh::kTwoPi * static_cast<double>(k) / static_cast<double>(st[2]);
+        const gdh::Q q = gdh::compose(gdh::about_axis(0.0, 1.0, 0.0, beta), gdh::about_axis(0.0, 0.0, 1.0, gamma));
+        const double w = q.w, x = q.x, y = q.y, z = q.z;
+        fm[size_t(j) * st[2] + k] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                                     2 * (x * y + w * z),     1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                                     2 * (x * z - w * y),     2 * (y * z + w * x),     1 - 2 * (x * x + y * y)};
+      }
+    }
+    std::vector<int32_t> rep(nf, -1), shift(nf, 0);
+    std::vector<uint32_t> kept;
+    for (uint32_t f = 0; f < nf; ++f) {
+      for (uint32_t f0 : kept) {
+        for (uint32_t sh = 0; sh < na && rep[f] < 0; ++sh) {
+          const double al = gdh::kTwoPi * static_cast<double>(sh) / static_cast<double>(na);
+          const double c = std::cos(al), sn = std::sin(al);
+          const auto& m0 = fm[f0];
+          double err = 0.0;
+          for (int col = 0; col < 3; ++col) {  // Rz(alpha) F_f0 against F_f
+            const double r0 = c * m0[col] - sn * m0[3 + col], r1 = sn * m0[col] + c * m0[3 + col], r2 = m0[6 + col];
+            err = std::max({err, std::fabs(r0 - fm[f][col]), std::fabs(r1 - fm[f][3 + col]), std::fabs(r2 - fm[f][6 + col])});
+          }
+          if (err < 1e-12) {
+            rep[f] = int32_t(f0);
+            shift[f] = int32_t(sh);
+          }
+        }
+        if (rep[f] >= 0) break;
+      }
+      if (rep[f] < 0) kept.push_back(f);
+    }
+    std::vector<uint32_t> tab(nf + kept.size(), 0u);
+    for (uint32_t i = 0; i < kept.size(); ++i) tab[nf + i] = kept[i];
+    for (uint32_t f0 : kept) {
+      uint32_t cnt = 0;
+      const uint32_t off = uint32_t(tab.size());
+      for (uint32_t f = 0; f < nf; ++f)
+        if (rep[f] == int32_t(f0)) {
+          tab.push_back(f | (uint32_t(shift[f]) << 16));
+          ++cnt;
+        }
+      tab[f0] = (off << 8) | cnt;
+    }
+    for (uint32_t f = 0; f < nf; ++f)
+      if (rep[f] >= 0) tab[f] = 0xffffffffu;
+    if (const char* env = std::getenv("GD_NO_TWINS"))  // experiments: screen every frame
+      if (env[0] == '1') {
+        tab.assign(2 * size_t(nf), 0u);
+        for (uint32_t f = 0; f < nf; ++f) tab[nf + f] = f;
+        kept.assign(nf, 0u);
+      }
+    ctx->n_kept = uint32_t(kept.size());
+    cudaFree(ctx->d_frame_tab);
+    ctx->d_frame_tab = nullptr;
+    GD_CUDA(ctx, cudaMalloc(&ctx->d_frame_tab, sizeof(uint32_t) * tab.size()));
+    GD_CUDA(ctx, cudaMemcpy(ctx->d_frame_tab, tab.data(), sizeof(uint32_t) * tab.size(), cudaMemcpyHostToDevice));
+  }
   return GD_OK;
 }
 
@@ -415,6 +487,8 @@ DevParams dev_params(const gd_ctx* ctx) {
   pr.dtab = ctx->d_dtab;
   pr.dtab_f = ctx->d_dtab_f;
   pr.frames = ctx->d_frames;
+  pr.frame_tab = ctx->d_frame_tab;
+  pr.n_kept = ctx->n_kept;
   for (int i = 0; i < 3; ++i) pr.steps[i] = ctx->params.rotation_steps[i];
   for (uint32_t i = 0; i < 16; ++i) {
     const double alpha = i < pr.steps[0] ? gdh::kTwoPi * static_cast<double>(i) / static_cast<double>(pr.steps[0]) : 0.0;
@@ -505,6 +579,7 @@ void gd_destroy(gd_ctx* ctx) {
   cudaFree(ctx->d_grid);
   cudaFree(ctx->d_grid_f);
   cudaFree(ctx->d_frames);
+  cudaFree(ctx->d_frame_tab);
   cudaFree(ctx->d_dtab);
   cudaFree(ctx->d_dtab_f);
   cudaFree(ctx->d_stats);
@@ -1095,6 +1170,11 @@ int read_device_status(gd_ctx* ctx, const std::function<std::string(uint32_t)>& 
   ctx->last.sweep_scored_steps = st[18];
   ctx->last.sweep_samples = st[19];
   ctx->last.cross_pairs = st[20];
+  ctx->last.sweep_moves = st[21];
+  ctx->last.step_exact_score_evals = st[22];
+  ctx->last.step_exact_allout_evals = st[23];
+  ctx->last.step_exact_face_evals = st[24];
+  ctx->last.step_exact_clash_evals = st[25];
   if (err[0] == GD_ERR_DEGENERATE_AXIS) {
     return set_err(ctx, GD_ERR_DEGENERATE_AXIS, "rotamer axis atoms coincide in ligand '" + name_of(uint32_t(err[1])) + "'");
   }
@@ -1386,6 +1466,11 @@ int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
   ctx->last.sweep_scored_steps = st[18];
   ctx->last.sweep_samples = st[19];
   ctx->last.cross_pairs = st[20];
+  ctx->last.sweep_moves = st[21];
+  ctx->last.step_exact_score_evals = st[22];
+  ctx->last.step_exact_allout_evals = st[23];
+  ctx->last.step_exact_face_evals = st[24];
+  ctx->last.step_exact_clash_evals = st[25];
   *out = ctx->last;
   return GD_OK;
 }

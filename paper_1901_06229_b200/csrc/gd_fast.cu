@@ -27,6 +27,18 @@ namespace gdk {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+// branch-weight hints: rare paths of the sweep laid out away from the per-step hot path
+// (instruction-cache footprint)
+#ifndef GD_HINTS
+#define GD_HINTS 0
+#endif
+#if GD_HINTS
+#define GD_UNLIKELY(x) __builtin_expect(!!(x), 0)
+#define GD_LIKELY(x) __builtin_expect(!!(x), 1)
+#else
+#define GD_UNLIKELY(x) (x)
+#define GD_LIKELY(x) (x)
+#endif
 constexpr float kMagic = 8388608.0f;  // 2^23: RZ-add leaves floor(g) in the mantissa
 constexpr int KTOP = 4;               // per-lane top coarse alignment candidates kept
 
@@ -41,9 +53,14 @@ constexpr int kAlignUnroll = GD_ALIGN_UNROLL;
 #define GD_ALPHA_CHUNK 4
 #endif
 constexpr int kAlphaChunk = GD_ALPHA_CHUNK;
-#ifndef GD_CROSS_REFRESH_MIN_NS
-#define GD_CROSS_REFRESH_MIN_NS 4  // after a commit: incremental cross-pair rows from this NS up (NS = 2: full rows, -18 % time)
+#ifndef GD_REG_ROWS_MAX_NS
+#define GD_REG_ROWS_MAX_NS 2  // pair-state rows in registers up to this NS, shared-memory rows beyond
 #endif
+constexpr uint32_t kZCap = 32;  // razor-thin pairs tracked per pose (beyond: every step takes the slow path)
+// per-warp sweep counters -> gd_stats (16 + i): steps, invariant-clash steps, scored steps, moved-atom
+// samples, cross pairs, k != 0 commits, FP64 candidate scores (other / all-outside / near a face),
+// FP64 cross-pair checks
+constexpr uint32_t kSweepCtr = 10;
 #ifndef GD_K1A_X2
 #define GD_K1A_X2 1  // K1a samples in f32x2 pairs (bit-identical to the scalar form)
 #endif
@@ -362,8 +379,16 @@ __device__ __noinline__ double exact_rotation_score(const DevPocket& pk, const d
 
 // Exact FP64 test of the non-bonded pairs of candidate k (rotate: M' atoms rotated by q about pi).
 // cross_only: only pairs with exactly one atom in M' (the invariant pairs are known exactly).
+#ifndef GD_EXACT_NOINLINE
+#define GD_EXACT_NOINLINE 0
+#endif
+#if GD_EXACT_NOINLINE
+#define GD_EXACT_FN __noinline__
+#else
+#define GD_EXACT_FN __forceinline__
+#endif
 template <int NS>
-__device__ __forceinline__ bool exact_clash_g(const DevBatch& b, uint32_t atom_base, uint32_t adj_base, uint32_t n,
+__device__ GD_EXACT_FN bool exact_clash_g(const DevBatch& b, uint32_t atom_base, uint32_t adj_base, uint32_t n,
                                            const double* X, uint32_t mo0, uint32_t mo1, uint32_t mo2, uint32_t mo3,
                                            bool rotate, V3d pi, Qd q, double clash, bool cross_only, uint32_t lane) {
   const uint32_t mo[4] = {mo0, mo1, mo2, mo3};
@@ -406,7 +431,7 @@ __device__ __forceinline__ bool exact_clash_g(const DevBatch& b, uint32_t atom_b
 // scr[a] keeps every atom's value until the next call: the caller copies the moved atoms' new
 // exact samples of its best candidate from there (a k != 0 commit stores them as the pose's ES).
 template <int NS>
-__device__ __forceinline__ double exact_candidate_score_g(const DevPocket& pk, uint32_t n, const double* X,
+__device__ GD_EXACT_FN double exact_candidate_score_g(const DevPocket& pk, uint32_t n, const double* X,
                                                        const double* ES, uint32_t mo0, uint32_t mo1, uint32_t mo2,
                                                        uint32_t mo3, bool rotate, V3d pi, Qd q, uint32_t lane,
                                                        double* scr) {
@@ -600,16 +625,52 @@ __global__ void __launch_bounds__(NT, 1)
     unsigned long long amb_mask = 0ull;  // rotations j (g = lane + 32 j) with a face-ambiguous sample
     const uint32_t npad = meta.npad;
     const bool big_grid = pr.G > 64u * 32u;
+    // Separable form (default grids): R_g = Rz(alpha_i) F_f with frame f = j*c + k, g = i*b*c + f.
+    // Lane l owns frames f = l + 32 m and all alpha of each; the frame's z row, its box term, floor
+    // and cell plane are shared by the alpha rotations and x, y need a 2D rotation only.
+    const uint32_t n_frames = pr.steps[1] * pr.steps[2];
+    const bool separable = pr.steps[0] >= 8 && pr.steps[0] <= 16 && n_frames <= 128;
+    // quarter-turn units (see the loop below): per restart n_units = kept frames x upf
+    const bool qt = separable && pr.steps[0] % (4 * kQtGroups) == 0;
+    const uint32_t nq = pr.steps[0] / 4, upf = qt ? nq / kQtGroups : 1u;
+    const uint32_t n_units = qt ? pr.n_kept * upf : 0u;
+    const uint32_t n_full = n_units & ~31u, n_rem = n_units - n_full;
+    const uint32_t gsz = n_rem <= 1u ? 32u : 32u >> (32 - __clz(n_rem - 1u));  // lanes per shared unit
+    const uint32_t n_iter = n_full / 32u + (n_rem ? 1u : 0u);
+    const bool twins = qt && pr.n_kept < n_frames;
+    auto unit_of = [&](uint32_t mu) -> uint32_t { return mu * 32u >= n_full ? n_full + lane / gsz : lane + 32u * mu; };
+    auto amb_to_g = [&](uint32_t bit) -> uint32_t {
+      if (qt) {  // bit = 8 mu + 4 gi + q of the lane's unit mu
+        const uint32_t u = unit_of(bit >> 3);
+        const uint32_t ia = (u % upf) * kQtGroups + ((bit >> 2) & 1u) + (bit & 3u) * nq;
+        return ia * n_frames + __ldg(pr.frame_tab + n_frames + u / upf);
+      }
+      return separable ? (bit & 15u) * n_frames + lane + 32u * (bit >> 4) : lane + 32u * bit;
+    };
+    // rotation g and its twins (rotations of the frames upload_grid_f folded into g's frame)
+    auto twin_count = [&](uint32_t g) -> uint32_t {
+      return twins ? (__ldg(pr.frame_tab + g % n_frames) & 0xffu) : 0u;
+    };
+    auto put_with_twins = [&](uint32_t at, uint32_t g) {
+      uint16_t* cl = b.rs_cand + size_t(item) * kAlignCand;
+      if (at < uint32_t(kAlignCand)) cl[at] = uint16_t(g);
+      const uint32_t nt = twin_count(g);
+      if (nt) {
+        const uint32_t f0 = g % n_frames, ia = g / n_frames, e = __ldg(pr.frame_tab + f0) >> 8;
+        for (uint32_t i = 0; i < nt; ++i) {
+          const uint32_t tw = __ldg(pr.frame_tab + e + i);
+          const uint32_t ia2 = (ia + pr.steps[0] - (tw >> 16)) % pr.steps[0];
+          if (at + 1 + i < uint32_t(kAlignCand)) cl[at + 1 + i] = uint16_t(ia2 * n_frames + (tw & 0xffffu));
+        }
+      }
+    };
     // collect mode (second pass): every rotation whose upper key reaches thr_c goes straight to
     // the restart's candidate list (rs_ncand counts them)
     bool collect = false;
     float thr_c = 0.f;
     auto insert = [&](float key_hi, uint32_t g) {
       if (collect) {
-        if (key_hi >= thr_c) {
-          const int at = atomicAdd(b.rs_ncand + item, 1);
-          if (at < kAlignCand) b.rs_cand[size_t(item) * kAlignCand + at] = uint16_t(g);
-        }
+        if (key_hi >= thr_c) put_with_twins(uint32_t(atomicAdd(b.rs_ncand + item, int(1u + twin_count(g)))), g);
         return;
       }
       if (key_hi > top_s[KTOP - 1]) {
@@ -631,30 +692,32 @@ __global__ void __launch_bounds__(NT, 1)
         dropped = fmaxf(dropped, key_hi);
       }
     };
-    // Separable form (default grids): R_g = Rz(alpha_i) F_f with frame f = j*c + k, g = i*b*c + f.
-    // Lane l owns frames f = l + 32 m and all alpha of each; the frame's z row, its box term, floor
-    // and cell plane are shared by the alpha rotations and x, y need a 2D rotation only.
-    const uint32_t n_frames = pr.steps[1] * pr.steps[2];
-    const bool separable = pr.steps[0] >= 8 && pr.steps[0] <= 16 && n_frames <= 128;
-    auto amb_to_g = [&](uint32_t bit) -> uint32_t {
-      return separable ? (bit & 15u) * n_frames + lane + 32u * (bit >> 4) : lane + 32u * bit;
-    };
     for (int pass = 0; pass < 2; ++pass) {
-      if (separable && pr.steps[0] % (4 * kQtGroups) == 0) {
+      if (qt) {
         // Quarter-turn symmetry: alpha_{c + q na/4} = alpha_c + q pi/2, so one 2D rotation
         // (rx, ry) = Rz(alpha_c) (wx, wy) gives the four samples t + (rx, ry), t + (-ry, rx),
         // t - (rx, ry), t + (ry, -rx): two FADDs per sample for x, y. kQtGroups consecutive c share
         // one pass over the atoms (the frame transform and the z terms are per atom).
-        const uint32_t nq = pr.steps[0] / 4;
         // byte offset of a cell from the three RZ-floor bit patterns: 16 bx + 16 cx by + zoff16
         const uint32_t cx16 = cg.cx * 16u, cxy16 = cg.cxy * 16u;
         // (shared: absolute 32-bit shared addresses; global: byte offsets from cg.cells)
         const uint32_t base16 = (SC ? uint32_t(__cvta_generic_to_shared(cg.cells)) : 0u) - cg.koff * 16u;
         const uint32_t dummy16 = (SC ? uint32_t(__cvta_generic_to_shared(cg.cells)) : 0u) + cg.dummy * 16u;
-        for (uint32_t f = lane, m = 0; f < n_frames; f += 32, ++m) {
+        // Work units: (kept frame, kQtGroups consecutive quarter-turn groups), 8 rotations each; twin
+        // frames (the same rotations as a kept frame's, upload_grid_f) are not screened: their
+        // rotations enter the candidate list with their twin's. Lane l takes units l + 32 mu; the
+        // n_rem units beyond the last full round are shared by groups of gsz lanes (atoms split
+        // over the group, partial sums combined by shuffles), so no lane screens a ninth unit
+        // while others idle.
+        for (uint32_t mu = 0; mu < n_iter; ++mu) {
+          const bool coop = mu * 32u >= n_full;  // warp-uniform
+          const uint32_t gs = coop ? gsz : 1u, sub = coop ? (lane & (gsz - 1u)) : 0u;
+          const uint32_t u = coop ? n_full + lane / gsz : lane + 32u * mu;
+          const bool active = u < n_units;
+          const uint32_t f = active ? __ldg(pr.frame_tab + n_frames + u / upf) : 0u;
+          const uint32_t c0 = (u % upf) * kQtGroups;
           const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
-  #pragma unroll 1
-          for (uint32_t c0 = 0; c0 < nq; c0 += kQtGroups) {
+          {
             float acc[4 * kQtGroups], amn[4 * kQtGroups];
             float2 cs[kQtGroups];
   #pragma unroll
@@ -668,46 +731,6 @@ __global__ void __launch_bounds__(NT, 1)
             // dummy select; 1 uses its frame's z term for all its samples (one face-tracking update
             // per atom, a select per sample); 2 tests every sample
             float amz = 1e30f, bsum = 0.f;
-            auto atom = [&](uint32_t a, auto cls_tag) {
-              constexpr int CLS = decltype(cls_tag)::value;
-              const float4 v = A[a];
-              const float wx = fmaf(F0.x, v.x, fmaf(F0.y, v.y, F0.z * v.z));
-              const float wy = fmaf(F1.x, v.x, fmaf(F1.y, v.y, F1.z * v.z));
-              const float gz = fmaf(F2.x, v.x, fmaf(F2.y, v.y, fmaf(F2.z, v.z, tz)));
-              const float ez = CLS == 0 ? 0.f : fabsf(gz - cg.hz) - cg.hz;
-              if (CLS == 1) amz = fminf(amz, fabsf(ez));
-              const float rz = __fadd_rz(gz, kMagic);
-              const float fz = gz - (rz - kMagic);
-              const uint32_t zoff16 = __float_as_uint(rz) * cxy16 + base16;
-              const CellBias cb = cell_bias(fz, cg.nb);
-              bsum += cb.b0;  // every sample of this atom carries it
-  #pragma unroll
-              for (int gi = 0; gi < kQtGroups; ++gi) {
-                const float rx = fmaf(cs[gi].x, wx, -cs[gi].y * wy), ry = fmaf(cs[gi].y, wx, cs[gi].x * wy);
-                const float px[4] = {tx + rx, tx - ry, tx - rx, tx + ry};
-                const float py[4] = {ty + ry, ty + rx, ty - ry, ty - rx};
-  #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float gx = px[q], gy = py[q];
-                  const float rxf = __fadd_rz(gx, kMagic), ryf = __fadd_rz(gy, kMagic);
-                  const float fx = gx - (rxf - kMagic), fy = gy - (ryf - kMagic);
-                  uint32_t addr = __float_as_uint(ryf) * cx16 + (__float_as_uint(rxf) * 16u + zoff16);
-                  if (CLS == 1) addr = ez < 0.0f ? addr : dummy16;
-                  if (CLS == 2) {
-                    const float e = fmaxf(fmaxf(fabsf(gx - cg.hx) - cg.hx, fabsf(gy - cg.hy) - cg.hy), ez);
-                    amn[4 * gi + q] = fminf(amn[4 * gi + q], fabsf(e));
-                    addr = e < 0.0f ? addr : dummy16;
-                  }
-                  acc[4 * gi + q] += cell_lerp_b(load_cell<SC>(cg, addr), fx, fy, fz, cb.k);
-                }
-              }
-            };
-#if GD_K1A_X2
-            // The same samples, in pairs (quarter-turns q = 2h, 2h + 1 of one group) through the
-            // f32x2 pipe: every FP32 operation of the pair is one FADD2 / FMUL2 / FFMA2 (two
-            // lane-ops per issue slot), each element rounded exactly as the scalar form above, so
-            // the coarse values (and everything downstream) are bit-identical. Only the address
-            // arithmetic, the LDS and the byte-permute decodes stay per sample.
             float2 acc2[2 * kQtGroups];
   #pragma unroll
             for (int i = 0; i < 2 * kQtGroups; ++i) acc2[i] = make_float2(0.f, 0.f);
@@ -775,40 +798,52 @@ __global__ void __launch_bounds__(NT, 1)
                 }
               }
             };
+            if (active) {
+              // the samples in pairs (quarter-turns q = 2h, 2h + 1 of one group) through the f32x2 pipe
   #pragma unroll 1
-            for (uint32_t a = 0; a < nsafe; ++a) atom2(a, std::integral_constant<int, 0>{});
+              for (uint32_t a = sub; a < nsafe; a += gs) atom2(a, std::integral_constant<int, 0>{});
   #pragma unroll 1
-            for (uint32_t a = nsafe; a < nsafe + nxy; ++a) atom2(a, std::integral_constant<int, 1>{});
+              for (uint32_t a = nsafe + ((sub - nsafe) & (gs - 1u)); a < nsafe + nxy; a += gs)
+                atom2(a, std::integral_constant<int, 1>{});
   #pragma unroll 1
-            for (uint32_t a = nsafe + nxy; a < n; ++a) atom2(a, std::integral_constant<int, 2>{});
+              for (uint32_t a = nsafe + nxy + ((sub - nsafe - nxy) & (gs - 1u)); a < n; a += gs)
+                atom2(a, std::integral_constant<int, 2>{});
+            }
+            if (coop) {  // combine the group's partial sums (any order: the error bound is order-free)
+              for (uint32_t o = 1; o < gsz; o <<= 1) {
+  #pragma unroll
+                for (int i = 0; i < 2 * kQtGroups; ++i) {
+                  acc2[i].x += __shfl_xor_sync(FULL, acc2[i].x, o);
+                  acc2[i].y += __shfl_xor_sync(FULL, acc2[i].y, o);
+                }
+  #pragma unroll
+                for (int i = 0; i < 4 * kQtGroups; ++i) amn[i] = fminf(amn[i], __shfl_xor_sync(FULL, amn[i], o));
+                bsum += __shfl_xor_sync(FULL, bsum, o);
+                amz = fminf(amz, __shfl_xor_sync(FULL, amz, o));
+              }
+            }
   #pragma unroll
             for (int i = 0; i < 2 * kQtGroups; ++i) {
               acc[2 * i] = acc2[i].x;
               acc[2 * i + 1] = acc2[i].y;
             }
-#else
-  #pragma unroll 1
-            for (uint32_t a = 0; a < nsafe; ++a) atom(a, std::integral_constant<int, 0>{});
-  #pragma unroll 1
-            for (uint32_t a = nsafe; a < nsafe + nxy; ++a) atom(a, std::integral_constant<int, 1>{});
-  #pragma unroll 1
-            for (uint32_t a = nsafe + nxy; a < n; ++a) atom(a, std::integral_constant<int, 2>{});
-#endif
+            if (active && sub == 0u) {
   #pragma unroll
-            for (int i = 0; i < 4 * kQtGroups; ++i) amn[i] = fminf(amn[i], amz);
+              for (int i = 0; i < 4 * kQtGroups; ++i) amn[i] = fminf(amn[i], amz);
   #pragma unroll
-            for (int gi = 0; gi < kQtGroups; ++gi)
+              for (int gi = 0; gi < kQtGroups; ++gi)
   #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const uint32_t ia = c0 + gi + q * nq;
-                const float sc = (acc[4 * gi + q] - bsum) * inv_n_scale;
-                if (amn[4 * gi + q] <= ptol) {
-                  amb_mask |= 1ull << (16 * m + ia);
-                } else {
-                  insert(sc, ia * n_frames + f);
-                  lkey = fmaxf(lkey, sc);
+                for (int q = 0; q < 4; ++q) {
+                  const uint32_t ia = c0 + gi + q * nq;
+                  const float sc = (acc[4 * gi + q] - bsum) * inv_n_scale;
+                  if (amn[4 * gi + q] <= ptol) {
+                    amb_mask |= 1ull << (8u * mu + 4u * gi + q);
+                  } else {
+                    insert(sc, ia * n_frames + f);
+                    lkey = fmaxf(lkey, sc);
+                  }
                 }
-              }
+            }
           }
         }
       } else if (separable) {
@@ -910,7 +945,9 @@ __global__ void __launch_bounds__(NT, 1)
         break;
       }
       const float B = warp_max(lkey);
-      const float thr = B - 2.0f * eps;
+      // a twin's exact score differs from its kept rotation's by FP64 rounding of the quaternions
+      // (~1e-16): 1e-7 below the threshold covers it
+      const float thr = B - 2.0f * eps - (twins ? 1e-7f : 0.f);
       const bool dropped_any = __any_sync(FULL, dropped >= thr);
       const bool hard = B < -1e29f || B > 1e29f || big_grid;
       // candidate list for K1b (order irrelevant: K1b takes max exact score, lowest index)
@@ -919,10 +956,15 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int t = 0; t < KTOP; ++t) {
           const bool c = top_s[t] >= thr;
-          const uint32_t pend = __ballot_sync(FULL, c);
-          const uint32_t at = cnt + __popc(pend & ((1u << lane) - 1u));
-          if (c && at < uint32_t(kAlignCand)) b.rs_cand[size_t(item) * kAlignCand + at] = uint16_t(top_g[t]);
-          cnt += __popc(pend);
+          const uint32_t k = c ? 1u + twin_count(top_g[t]) : 0u;  // entries: the rotation and its twins
+          uint32_t incl = k;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= uint32_t(o)) incl += y;
+          }
+          if (c) put_with_twins(cnt + incl - k, top_g[t]);
+          cnt += __shfl_sync(FULL, incl, 31);
         }
       }
       if (!dropped_any || hard) {
@@ -957,9 +999,9 @@ __global__ void __launch_bounds__(NT, 1)
   // One DevPocket per CTA in shared memory (with the field pointer redirected below): the exact
   // samplers take it by reference, and a per-thread copy would live in local memory
   __shared__ DevPocket spk;
-  __shared__ uint32_t sweep_ctr[32][5];  // per warp: executed sweep work, see st_* below
+  __shared__ uint32_t sweep_ctr[32][kSweepCtr];  // per warp: executed sweep work, see st_* below
   if (threadIdx.x == 0) spk = pk_in;
-  if (threadIdx.x < 32 * 5) sweep_ctr[threadIdx.x / 5][threadIdx.x % 5] = 0u;
+  if (threadIdx.x < 32 * kSweepCtr) sweep_ctr[threadIdx.x / kSweepCtr][threadIdx.x % kSweepCtr] = 0u;
   __syncthreads();
   DevPocket& pk = spk;
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
@@ -993,6 +1035,12 @@ __global__ void __launch_bounds__(NT, 1)
   double* ES = X + 3 * ((b.max_n + 3) & ~3u);
   float* CF = reinterpret_cast<float*>(ES + ((b.max_n + 3) & ~3u));  // step cache: fixed-side sums
   double* BEST = reinterpret_cast<double*>(CF + 32);  // best candidate's moved-atom exact samples
+  // pair state of the current pose (DFS space): CR[x * NS + w] = exact clash partners of atom x,
+  // ZL = pairs whose exact margin is razor-thin, DINV = original index of DFS position x
+  uint32_t* CR = reinterpret_cast<uint32_t*>(BEST + ((b.max_n + 3) & ~3u));
+  uint32_t* AM = CR + NS * ((b.max_n + 3) & ~3u);  // pairs near the threshold, pending an FP64 verdict
+  uint32_t* ZL = AM + NS * ((b.max_n + 3) & ~3u);  // + its counter at ZL[kZCap]
+  uint32_t* DINV = ZL + kZCap + 4;
   double* SCR1 = reinterpret_cast<double*>(SURV);
   double* SCR3 = reinterpret_cast<double*>(A);
   const CoarseGrid cg{cells,
@@ -1051,6 +1099,7 @@ __global__ void __launch_bounds__(NT, 1)
       set_own(P, s, V3d{at.x, at.y, at.z});
       rad[s] = at.w;
       pos[s] = a < n ? b.dfs_pos[it.m.atom_base + a] : 0;
+      if (a < n) DINV[pos[s]] = a;
     }
     {
       const V3d c0 = centroid_smem<NS>(P, n, SCR3, lane);
@@ -1093,7 +1142,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int32_t ncand = b.rs_ncand[item];
     double best_s = -1.0;
     uint32_t best_g = 0xffffffffu;
-    if (ncand < 0 || pr.G > 65535u) {
+    if (GD_UNLIKELY(ncand < 0 || pr.G > 65535u)) {
       ++st_afall;
       for (uint32_t g = lane; g < pr.G; g += 32) {
         const double4 gq = pr.grid[g];
@@ -1114,12 +1163,10 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t g = __shfl_sync(FULL, c < 32 ? my_g0 : my_g1, c & 31);
         ++st_aexact;
         const double4 gq = pr.grid[g];
-        const Qd q{gq.x, gq.y, gq.z, gq.w};
-        double ns[NS];
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          ns[s] = lane + 32 * s < n ? sample_exact_ni(pk, rotated_about(own(P, s), cen, q)) : 0.0;
-        const double sc = __ddiv_rn(ordered_sum_smem<NS>(ns, n, SCR3, lane), double(n));
+        // the dihedral candidates' exact scorer with every atom rotated about the centroid: the
+        // same rotated_about, sample_field and index-order sum / n as docking.cpp:77-83
+        const double sc = exact_candidate_score_g<NS>(pk, n, X, ES, FULL, FULL, FULL, FULL, true, cen,
+                                                      Qd{gq.x, gq.y, gq.z, gq.w}, lane, SCR1);
         if (best_g == 0xffffffffu || sc > best_s || (sc == best_s && g < best_g)) {
           best_s = sc;
           best_g = g;
@@ -1180,13 +1227,13 @@ __global__ void __launch_bounds__(NT, 1)
       // full-angle (cos, sin) of the same candidates, for the algebraic cross-pair margins
       const float2 cf_p0 = make_float2(fmaf(-2.f * cq_p0.y, cq_p0.y, 1.f), 2.f * cq_p0.x * cq_p0.y);
       const float2 cf_p1 = make_float2(fmaf(-2.f * cq_p1.y, cq_p1.y, 1.f), 2.f * cq_p1.x * cq_p1.y);
-      // Per-pose caches, rebuilt after alignment and after every k != 0 commit (DESIGN.md §3.3):
+      // Per-pose caches, rebuilt after alignment and after every k != 0 commit (DESIGN.md §3.2):
       //   A[pos]     FP32 (gx, gy, gz, rho = cf*r/spacing) in DFS order,
       //   es, cs     exact FP64 and coarse per-atom samples, samb: coarse sample near a face,
-      //   crow       exact clash partners (DFS bit rows), arow: pairs within tau of the threshold.
+      //   CR, ctot   exact clash partners of every atom (DFS bit rows, shared) and the number of
+      //              clashing pairs, ZL / zcnt: pairs whose exact margin is razor-thin.
       float cs[NS];
       bool samb[NS];
-      uint32_t crow[NS][NS], arow[NS][NS];
       float rho[NS];
       float rmax = 0.f;
 #pragma unroll
@@ -1198,10 +1245,20 @@ __global__ void __launch_bounds__(NT, 1)
       // |computed - exact| of d^2 - t^2 for pairs near the threshold (d ~ t <= 2 rmax):
       // 2 d |dd| with |dd| <= 2 sqrt(3) ptol, plus FP32 rounding of t^2 and the chain.
       const float tau = 16.0f * rmax * ptol + 4e-6f * rmax * rmax + 1e-6f;
+      uint32_t ctot = 0u, zcnt = 0u;  // warp-uniform
+      // Small ligands (NS <= GD_REG_ROWS_MAX_NS) keep the rows in registers instead: crow = exact
+      // clash partners, arow = razor pairs (DFS bit rows of the lane's atoms), every row
+      // recomputed at each refresh (measured faster there: one short loop per row word).
+      constexpr bool kRegRows = NS <= GD_REG_ROWS_MAX_NS;
+      uint32_t crow[NS][NS], arow[NS][NS];
 
       // (loops over the NS atom slots are not unrolled here: one copy of each body in the code,
       // register arrays indexed through pick/put selects)
-      auto refresh = [&](bool all, const uint32_t (&mo)[NS]) {
+      // all: every atom of the aligned pose; otherwise the atoms a k != 0 commit moved (mo in
+      // original, md in DFS bit space). Only pairs with a moved atom change their distance, so only
+      // their rows are recomputed: each moved atom's row from one ballot per word, and its bit in
+      // every other atom's row by that atom's lane.
+      auto refresh = [&](bool all, const uint32_t (&mo)[NS], const uint32_t (&md)[NS]) {
 #pragma unroll 1
         for (int s = 0; s < NS; ++s) {
           const uint32_t a = lane + 32 * s;
@@ -1220,158 +1277,200 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
         __syncwarp();
-        bool any_amb = false;
+        if constexpr (kRegRows) {
+          bool any_amb = false;
 #pragma unroll
-        for (int s = 0; s < NS; ++s)
+          for (int s = 0; s < NS; ++s)
 #pragma unroll
-          for (int w = 0; w < NS; ++w) crow[s][w] = arow[s][w] = 0u;
+            for (int w = 0; w < NS; ++w) crow[s][w] = arow[s][w] = 0u;
 #pragma unroll 1
-        for (int s = 0; s < NS; ++s) {
-          const uint32_t a = lane + 32 * s;
-          if (a >= n) continue;
-          const uint32_t ps = pick<NS>(pos, s);
-          const float4 pa = A[ps];
-          const uint32_t* adrow = b.adjd + it.m.adj_base + ps * it.W;
+          for (int s = 0; s < NS; ++s) {
+            const uint32_t a = lane + 32 * s;
+            if (a >= n) continue;
+            const uint32_t ps = pick<NS>(pos, s);
+            const float4 pa = A[ps];
+            const uint32_t* adrow = b.adjd + it.m.adj_base + ps * it.W;
 #pragma unroll 1
-          for (int w = 0; w < NS; ++w) {
-            if (uint32_t(w) >= it.W) break;
-            // bonded partners and the atom itself are not bump pairs (scoring.cpp:53-55)
-            const uint32_t skip = __ldg(adrow + w) | (ps >> 5 == uint32_t(w) ? 1u << (ps & 31) : 0u);
-            const uint32_t qe = min(n, 32u * w + 32u);
-            uint32_t cw = 0u, aw = 0u;
-            for (uint32_t q = 32u * w; q < qe; ++q) {
-              const float4 pb = A[q];
-              const float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
-              const float t = pa.w + pb.w;
-              const float mg = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -t * t)));
-              const uint32_t bit = 1u << (q & 31);
-              cw |= mg < -tau ? bit : 0u;
-              aw |= (mg >= -tau && mg <= tau) ? bit : 0u;
+            for (int w = 0; w < NS; ++w) {
+              if (uint32_t(w) >= it.W) break;
+              // bonded partners and the atom itself are not bump pairs (scoring.cpp:53-55)
+              const uint32_t skip = __ldg(adrow + w) | (ps >> 5 == uint32_t(w) ? 1u << (ps & 31) : 0u);
+              const uint32_t qe = min(n, 32u * w + 32u);
+              uint32_t cw = 0u, aw = 0u;
+              for (uint32_t q = 32u * w; q < qe; ++q) {
+                const float4 pb = A[q];
+                const float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
+                const float t = pa.w + pb.w;
+                const float mg = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -t * t)));
+                const uint32_t bit = 1u << (q & 31);
+                cw |= mg < -tau ? bit : 0u;
+                aw |= (mg >= -tau && mg <= tau) ? bit : 0u;
+              }
+              put2<NS>(crow, s, w, cw & ~skip);
+              put2<NS>(arow, s, w, aw & ~skip);
+              any_amb |= (aw & ~skip) != 0u;
             }
-            put2<NS>(crow, s, w, cw & ~skip);
-            put2<NS>(arow, s, w, aw & ~skip);
-            any_amb |= (aw & ~skip) != 0u;
           }
-        }
-        if (__any_sync(FULL, any_amb)) {  // near-threshold pairs: exact FP64 verdict
-          for (uint32_t bb = 0; bb < n; ++bb) {
-            const V3d pb{X[3 * bb], X[3 * bb + 1], X[3 * bb + 2]};
-            const uint32_t q = b.dfs_pos[it.m.atom_base + bb];
-            const double rb = b.atoms[it.m.atom_base + bb].w;
-            const uint32_t bit = 1u << (q & 31), qw = q >> 5;
+          if (__any_sync(FULL, any_amb)) {  // near-threshold pairs: exact FP64 verdict
+            for (uint32_t bb = 0; bb < n; ++bb) {
+              const V3d pb{X[3 * bb], X[3 * bb + 1], X[3 * bb + 2]};
+              const uint32_t q = b.dfs_pos[it.m.atom_base + bb];
+              const double rb = b.atoms[it.m.atom_base + bb].w;
+              const uint32_t bit = 1u << (q & 31), qw = q >> 5;
 #pragma unroll
-            for (int s = 0; s < NS; ++s) {
-              // word qw of row s without a dynamic index (keeps crow/arow in registers)
-              const uint32_t aw = word_of<NS>(arow[s], qw);
-              if (aw & bit) {
-                // exact verdict (scoring.cpp:52-58: clash iff d^2 < thr^2 iff d^2 - thr^2 < 0); the
-                // pair stays flagged ("razor") only if its exact margin is within 1e-8 A^2, where
-                // the FP64 rounding of a rotated candidate (~1e-12 A^2) could flip an invariant pair
-                const uint32_t a = lane + 32 * s;
-                const double mg = pair_margin_exact(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, pb,
-                                                    b.atoms[it.m.atom_base + a].w, rb, pr.clash);
-                const uint32_t set_c = mg < 0.0 ? bit : 0u, clr_a = fabs(mg) <= 1e-8 ? 0u : bit;
+              for (int s = 0; s < NS; ++s) {
+                const uint32_t aw = word_of<NS>(arow[s], qw);
+                if (aw & bit) {
+                  // exact verdict (clash iff d^2 < thr^2); the pair stays flagged ("razor") only
+                  // if its exact margin is within 1e-8 A^2
+                  const uint32_t a = lane + 32 * s;
+                  const double mg = pair_margin_exact(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, pb,
+                                                      b.atoms[it.m.atom_base + a].w, rb, pr.clash);
+                  const uint32_t set_c = mg < 0.0 ? bit : 0u, clr_a = fabs(mg) <= 1e-8 ? 0u : bit;
 #pragma unroll
-                for (int w = 0; w < NS; ++w)
-                  if (qw == uint32_t(w)) {
-                    crow[s][w] |= set_c;
-                    arow[s][w] &= ~clr_a;
-                  }
+                  for (int w = 0; w < NS; ++w)
+                    if (qw == uint32_t(w)) {
+                      crow[s][w] |= set_c;
+                      arow[s][w] &= ~clr_a;
+                    }
+                }
               }
             }
           }
+        } else {
+        // Rows in FP32 against tau; pairs within tau of the threshold are marked in AM (both rows)
+        // and settled in FP64 by one pass below.
+        uint32_t* zc = ZL + kZCap;  // razor-pair counter
+        if (all) {
+          // every row, lane-owned: each lane its atoms' rows, one word at a time against the
+          // broadcast partners (the pair loop of bump_check, scoring.cpp:52-58)
+          zcnt = 0u;
+#pragma unroll 1
+          for (int s = 0; s < NS; ++s) {
+            if (lane + 32u * s >= n) continue;
+            const uint32_t ps = pick<NS>(pos, s);
+            const float4 pa = A[ps];
+            const uint32_t* adrow = b.adjd + it.m.adj_base + ps * it.W;
+#pragma unroll 1
+            for (int w = 0; w < NS; ++w) {
+              if (uint32_t(w) >= it.W) break;
+              // bonded partners and the atom itself are not bump pairs (scoring.cpp:53-55)
+              const uint32_t skip = __ldg(adrow + w) | (ps >> 5 == uint32_t(w) ? 1u << (ps & 31) : 0u);
+              const uint32_t qe = min(n, 32u * w + 32u);
+              uint32_t cw = 0u, aw = 0u;
+              for (uint32_t q = 32u * w; q < qe; ++q) {
+                const float4 pb = A[q];
+                const float dx = pa.x - pb.x, dy = pa.y - pb.y, dz = pa.z - pb.z;
+                const float t = pa.w + pb.w;
+                const float mg = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -t * t)));
+                const uint32_t bit = 1u << (q & 31);
+                cw |= mg < -tau ? bit : 0u;
+                aw |= (mg >= -tau && mg <= tau) ? bit : 0u;
+              }
+              CR[ps * NS + uint32_t(w)] = cw & ~skip;
+              AM[ps * NS + uint32_t(w)] = aw & ~skip;
+            }
+          }
+        } else {
+          // after a commit: the rows of the moved atoms (one ballot per word), and their bits in
+          // the partners' rows (by the partner's lane). Razor pairs with a moved atom leave the list.
+          if (zcnt != 0u && zcnt <= kZCap) {
+            const uint32_t e = lane < zcnt ? ZL[lane] : 0u;
+            const bool keep = lane < zcnt && !bit4<NS>(md, e & 0xffffu) && !bit4<NS>(md, e >> 16);
+            const uint32_t kb = __ballot_sync(FULL, keep);
+            __syncwarp();
+            if (keep) ZL[__popc(kb & ((1u << lane) - 1u))] = e;
+            zcnt = __popc(kb);
+          }
+#pragma unroll 1
+          for (int w0 = 0; w0 < NS; ++w0) {
+            uint32_t bits = word_of<NS>(md, uint32_t(w0));
+            while (bits) {
+              const uint32_t p = 32u * uint32_t(w0) + uint32_t(__ffs(bits) - 1);
+              bits &= bits - 1u;
+              const float4 pp = A[p];
+              const uint32_t pb = 1u << (p & 31);
+#pragma unroll 1
+              for (int t = 0; t < NS; ++t) {
+                if (uint32_t(t) >= it.W) break;
+                const uint32_t x = lane + 32u * uint32_t(t);
+                const uint32_t bw = __ldg(b.adjd + it.m.adj_base + p * it.W + t);
+                bool c = false, am = false;
+                if (x < n && x != p && !((bw >> lane) & 1u)) {
+                  const float4 px = A[x];
+                  const float dx = pp.x - px.x, dy = pp.y - px.y, dz = pp.z - px.z;
+                  const float tt = pp.w + px.w;
+                  const float mg = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -tt * tt)));
+                  c = mg < -tau;
+                  am = mg >= -tau && mg <= tau;
+                }
+                const uint32_t wc = __ballot_sync(FULL, c), wa = __ballot_sync(FULL, am);
+                if (lane == 0) {
+                  CR[p * NS + uint32_t(t)] = wc;
+                  AM[p * NS + uint32_t(t)] = wa;
+                }
+                if (x < n && x != p) {
+                  uint32_t& rc = CR[x * NS + (p >> 5)];
+                  rc = (rc & ~pb) | (c ? pb : 0u);
+                  AM[x * NS + (p >> 5)] |= am ? pb : 0u;
+                }
+              }
+              __syncwarp();
+            }
+          }
         }
-      };
-      // After a k != 0 commit (tree layout): only the cross pairs M' x F' changed (both in M',
-      // both outside, and any pair with atom_j or atom_i on the axis keep their distance), so
-      // instead of all n^2 pairs the warp walks M' (|M'| ~ 2.4 atoms on C2): every lane tests its
-      // atoms against moved atom m, updates its own row at m's bit, and the lanes' verdicts are
-      // OR-reduced into m's row words, which m's owner lane writes back over its F' bits. FP32
-      // verdicts within tau of the threshold are settled in FP64 on the spot (the same
-      // pair_margin_exact and razor rule as refresh, which is symmetric in the pair).
-      auto refresh_cross = [&](const uint32_t (&mo)[NS], const uint32_t (&md)[NS], uint32_t s0, uint32_t e0) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          const uint32_t a = lane + 32 * s;
-          if (a < n && bit4(mo, a)) {
-            const V3d pa{X[3 * a], X[3 * a + 1], X[3 * a + 2]};
-            const float gx = float(__dmul_rn(__dsub_rn(pa.x, pk.origin[0]), pk.inv_spacing));
-            const float gy = float(__dmul_rn(__dsub_rn(pa.y, pk.origin[1]), pk.inv_spacing));
-            const float gz = float(__dmul_rn(__dsub_rn(pa.z, pk.origin[2]), pk.inv_spacing));
-            A[pos[s]] = make_float4(gx, gy, gz, rho[s]);  // (ES: stored by the commit)
-            float am = 1e30f;
-            cs[s] = coarse_sample(cg, gx, gy, gz, am);
-            samb[s] = am <= ptol;
+        // near-threshold pairs: exact verdict (scoring.cpp:52-58: clash iff d^2 < thr^2), each pair
+        // once (marked in both rows, settled from the lower one). A pair whose exact margin is
+        // within 1e-8 A^2 is "razor": the FP64 rounding of a rotated candidate (~1e-12 A^2) could
+        // flip it (ZL).
+        if (lane == 0) *zc = zcnt;
+        __syncwarp();
+#pragma unroll 1
+        for (int t = 0; t < NS; ++t) {
+          const uint32_t x = lane + 32u * uint32_t(t);
+          if (x >= n) continue;
+#pragma unroll 1
+          for (uint32_t w = 0; w < it.W; ++w) {
+            uint32_t aw = AM[x * NS + w];
+            if (GD_LIKELY(!aw)) continue;
+            AM[x * NS + w] = 0u;
+            aw &= ~range_word(w, 0u, x + 1u);  // partners above x
+            while (aw) {
+              const uint32_t q = 32u * w + uint32_t(__ffs(aw) - 1);
+              aw &= aw - 1u;
+              const uint32_t xo = DINV[x], qo = DINV[q];
+              const double mgx = pair_margin_exact(V3d{X[3 * xo], X[3 * xo + 1], X[3 * xo + 2]},
+                                                   V3d{X[3 * qo], X[3 * qo + 1], X[3 * qo + 2]},
+                                                   b.atoms[it.m.atom_base + xo].w, b.atoms[it.m.atom_base + qo].w,
+                                                   pr.clash);
+              const uint32_t qb = 1u << (q & 31), xb = 1u << (x & 31);
+              if (mgx < 0.0) {
+                atomicOr(CR + x * NS + w, qb);
+                atomicOr(CR + q * NS + (x >> 5), xb);
+              } else {
+                atomicAnd(CR + x * NS + w, ~qb);
+                atomicAnd(CR + q * NS + (x >> 5), ~xb);
+              }
+              if (fabs(mgx) <= 1e-8) {
+                const uint32_t at = atomicAdd(zc, 1u);
+                if (at < kZCap) ZL[at] = x | (q << 16);
+              }
+            }
           }
         }
         __syncwarp();
-        bool fixed[NS];  // F': outside M' and neither atom_j (DFS s0) nor a padding slot
+        zcnt = *zc;
+        uint32_t cnt = 0u;
 #pragma unroll
-        for (int s = 0; s < NS; ++s) fixed[s] = lane + 32 * s < n && !(pos[s] >= s0 && pos[s] < e0);
-        uint32_t keep[NS];  // bits of a moved row that stay: M' and atom_j
+        for (int t = 0; t < NS; ++t) {
+          const uint32_t x = lane + 32u * uint32_t(t);
+          if (x < n) {
 #pragma unroll
-        for (int w = 0; w < NS; ++w) keep[w] = md[w] | ((s0 >> 5) == uint32_t(w) ? 1u << (s0 & 31) : 0u);
-        for (uint32_t p = s0 + 1; p < e0; ++p) {
-          const float4 pm = A[p];
-          uint32_t own_lane = 0, own_s = 0;
-#pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            const uint32_t bl = __ballot_sync(FULL, lane + 32 * s < n && pos[s] == p);
-            if (bl) {
-              own_lane = __ffs(bl) - 1;
-              own_s = uint32_t(s);
-            }
+            for (int w = 0; w < NS; ++w)
+              if (uint32_t(w) < it.W) cnt += __popc(CR[x * NS + uint32_t(w)]);
           }
-          const uint32_t m = own_lane + 32 * own_s;
-          const uint32_t pbit = 1u << (p & 31), pw = p >> 5;
-          uint32_t cm[NS], amw[NS];
-#pragma unroll
-          for (int w = 0; w < NS; ++w) cm[w] = amw[w] = 0u;
-#pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            if (!fixed[s]) continue;
-            const float4 pa = A[pos[s]];
-            const float dx = pa.x - pm.x, dy = pa.y - pm.y, dz = pa.z - pm.z;
-            const float t = pa.w + pm.w;
-            const float mg = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, -t * t)));
-            bool c = mg < -tau, amb = mg >= -tau && mg <= tau;
-            if (amb) {  // exact verdict; the pair stays flagged only within the razor margin
-              const uint32_t a = lane + 32 * s;
-              const double mgx = pair_margin_exact(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]},
-                                                   V3d{X[3 * m], X[3 * m + 1], X[3 * m + 2]}, rad[s],
-                                                   b.atoms[it.m.atom_base + m].w, pr.clash);
-              c = mgx < 0.0;
-              amb = fabs(mgx) <= 1e-8;
-            }
-#pragma unroll
-            for (int w = 0; w < NS; ++w) {
-              if (pw == uint32_t(w)) {
-                crow[s][w] = (crow[s][w] & ~pbit) | (c ? pbit : 0u);
-                arow[s][w] = (arow[s][w] & ~pbit) | (amb ? pbit : 0u);
-              }
-              if ((pos[s] >> 5) == uint32_t(w)) {
-                const uint32_t qb = 1u << (pos[s] & 31);
-                cm[w] |= c ? qb : 0u;
-                amw[w] |= amb ? qb : 0u;
-              }
-            }
-          }
-#pragma unroll
-          for (int w = 0; w < NS; ++w) {
-            cm[w] = __reduce_or_sync(FULL, cm[w]);
-            amw[w] = __reduce_or_sync(FULL, amw[w]);
-          }
-          if (lane == own_lane) {
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-              if (uint32_t(s) == own_s) {
-#pragma unroll
-                for (int w = 0; w < NS; ++w) {
-                  crow[s][w] = (crow[s][w] & keep[w]) | cm[w];
-                  arow[s][w] = (arow[s][w] & keep[w]) | amw[w];
-                }
-              }
-          }
+        }
+        ctot = __reduce_add_sync(FULL, cnt) >> 1;  // every clashing pair sits in two rows
         }
       };
       // rotamer r's bond (i, j), DFS range (s0, e0) and DFS position of atom_i
@@ -1433,7 +1532,7 @@ __global__ void __launch_bounds__(NT, 1)
       uint32_t vmask = 0u;  // step cache (rotamers r < 32): valid entries of CF
       for (uint32_t rep = 0; rep < pr.reps; ++rep) {
         for (uint32_t r = 0; r < R; ++r) {
-          if (pend_r != kRefreshNone) {
+          if (GD_UNLIKELY(pend_r != kRefreshNone)) {
             GD_T(3);
             uint32_t pmo[NS], pmd[NS];
             uint32_t ps0 = 0, pe0 = 0;
@@ -1447,10 +1546,7 @@ __global__ void __launch_bounds__(NT, 1)
               rot_info(pend_r, pij, ps0, pe0, pip);
               rot_masks(pend_r, pij, ps0, pe0, pmo, pmd, pinm);
             }
-            // after a commit only the rows' cross-pair bits change: the incremental update walks
-            // the moved atoms instead of recomputing all n^2 pairs (GD_CROSS_REFRESH_MIN_NS)
-            if (NS >= GD_CROSS_REFRESH_MIN_NS && it.m.fast_ok && pend_r != kRefreshAll) refresh_cross(pmo, pmd, ps0, pe0);
-            else refresh(pend_r == kRefreshAll, pmo);
+            refresh(pend_r == kRefreshAll, pmo, pmd);
             pend_r = kRefreshNone;
           }
           GD_T(4);
@@ -1489,35 +1585,65 @@ __global__ void __launch_bounds__(NT, 1)
             }
           } else {
             rot_masks(r, ij, s0, e0, mo, md, inm);
-            // invariant pairs (both in M' or both outside) of the current pose: exact from crow
-            bool inv_l = false, frag_l = false, cne_l = false;
+            if constexpr (kRegRows) {
+              bool inv_l = false, frag_l = false, cne_l = false;
 #pragma unroll
-            for (int s = 0; s < NS; ++s) {
-              if (lane + 32 * s >= n) continue;
-              // Invariant pairs: both in M', both outside M', and (m, atom_j) — j lies on the axis,
-              // so |m - j| does not change with the angle either. Their exact verdicts (crow) hold
-              // for every candidate unless the exact margin is razor-thin (arow after refresh).
-              const bool isj = pos[s] == s0;
+              for (int s = 0; s < NS; ++s) {
+                if (lane + 32 * s >= n) continue;
+                // Invariant pairs: both in M', both outside M', and (m, atom_j) — j lies on the
+                // axis, so |m - j| does not change with the angle either. Their exact verdicts
+                // (crow) hold for every candidate unless the exact margin is razor-thin (arow).
+                const bool isj = pos[s] == s0;
 #pragma unroll
-              for (int w = 0; w < NS; ++w) {
-                const uint32_t lo = 32u * w;
-                const uint32_t valid = lo + 32u <= n ? FULL : (lo >= n ? 0u : ((1u << (n - lo)) - 1u));
-                const uint32_t mdj = md[w] | ((s0 >> 5) == uint32_t(w) ? 1u << (s0 & 31) : 0u);
-                inv_l |= (crow[s][w] & (inm[s] ? mdj : isj ? valid : (~md[w] & valid))) != 0u;
-                if (inm[s]) frag_l |= (arow[s][w] & mdj) != 0u;
-                if (isj) frag_l |= (arow[s][w] & md[w]) != 0u;
-                cne_l |= crow[s][w] != 0u;
+                for (int w = 0; w < NS; ++w) {
+                  const uint32_t lo = 32u * w;
+                  const uint32_t valid = lo + 32u <= n ? FULL : (lo >= n ? 0u : ((1u << (n - lo)) - 1u));
+                  const uint32_t mdj = md[w] | ((s0 >> 5) == uint32_t(w) ? 1u << (s0 & 31) : 0u);
+                  inv_l |= (crow[s][w] & (inm[s] ? mdj : isj ? valid : (~md[w] & valid))) != 0u;
+                  if (inm[s]) frag_l |= (arow[s][w] & mdj) != 0u;
+                  if (isj) frag_l |= (arow[s][w] & md[w]) != 0u;
+                  cne_l |= crow[s][w] != 0u;
+                }
+                if (!inm[s]) fsum += cs[s];
               }
-              if (!inm[s]) fsum += cs[s];
+              inv = __any_sync(FULL, inv_l);
+              frag = __any_sync(FULL, frag_l);
+              elig0 = !__any_sync(FULL, cne_l);  // k = 0: the current pose passes bump_check
+            } else {
+            // Invariant pairs: both in M', both outside M', and (m, atom_j) — j lies on the axis, so
+            // |m - j| does not change with the angle either. Their exact verdicts hold for every
+            // candidate unless the exact margin is razor-thin (ZL). Of the pose's ctot clashing
+            // pairs, `cross` have one atom in M' and the other outside M' + {j}: an invariant clash
+            // exists iff ctot > cross, and k = 0 (the current pose) passes bump_check iff ctot == 0.
+            uint32_t mj[NS];
+#pragma unroll
+            for (int w = 0; w < NS; ++w) mj[w] = md[w] | ((s0 >> 5) == uint32_t(w) ? 1u << (s0 & 31) : 0u);
+            uint32_t cross = 0u;
+#pragma unroll
+            for (int t = 0; t < NS; ++t) {
+              const uint32_t x = lane + 32u * uint32_t(t);
+              if (x < n && ((md[t] >> lane) & 1u)) {
+#pragma unroll
+                for (int w = 0; w < NS; ++w)
+                  if (uint32_t(w) < it.W) cross += __popc(CR[x * NS + uint32_t(w)] & ~mj[w]);
+              }
             }
-            inv = __any_sync(FULL, inv_l);
-            frag = __any_sync(FULL, frag_l);
-            elig0 = !__any_sync(FULL, cne_l);  // k = 0: the current pose passes bump_check
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              if (lane + 32 * s < n && !inm[s]) fsum += cs[s];
+            inv = ctot > __reduce_add_sync(FULL, cross);
+            elig0 = ctot == 0u;
+            frag = zcnt > kZCap;
+            if (GD_UNLIKELY(zcnt != 0u && !frag)) {  // a razor pair inside M' + {j}: its distance moves by rounding
+              const uint32_t e = lane < zcnt ? ZL[lane] : 0u;
+              frag = __any_sync(FULL, lane < zcnt && bit4<NS>(mj, e & 0xffffu) && bit4<NS>(mj, e >> 16));
+            }
+            }
             fsum = warp_sum(fsum);
             if (pr.S > 1) {
               const float4 fi = A[it.m.fast_ok ? ipos : 0u], fj = A[it.m.fast_ok ? s0 : 0u];
               const float dx = fj.x - fi.x, dy = fj.y - fi.y, dz = fj.z - fi.z;
-              if (!it.m.fast_ok || dx * dx + dy * dy + dz * dz < 1e-6f) {
+              if (GD_UNLIKELY(!it.m.fast_ok || dx * dx + dy * dy + dz * dz < 1e-6f)) {
                 const V3d qi{X[3 * ij.x], X[3 * ij.x + 1], X[3 * ij.x + 2]};
                 const V3d delta = vsub(V3d{X[3 * ij.y], X[3 * ij.y + 1], X[3 * ij.y + 2]}, qi);
                 if (__dsqrt_rn(vdot(delta, delta)) < 1e-12) {
@@ -1562,7 +1688,7 @@ __global__ void __launch_bounds__(NT, 1)
               if (inm[t]) BEST[lane + 32 * t] = SCR1[lane + 32 * t];
           };
 
-          if (!it.m.fast_ok || frag || pr.S > 64 || pr.S < 2) {
+          if (GD_UNLIKELY(!it.m.fast_ok || frag || pr.S > 64 || pr.S < 2)) {
             // ---------------- slow path: every candidate exactly (non-tree layouts, pairs of the
             // moving fragment within tau of the threshold, or unusual S)
             ++st_sfall;
@@ -1753,12 +1879,13 @@ __global__ void __launch_bounds__(NT, 1)
               {  // cross pairs within tau of the threshold: exact
                 unsigned long long pend = __ballot_sync(FULL, (res_st[0] & ST_XAMB) != 0u) |
                                           (uint64_t(__ballot_sync(FULL, (res_st[1] & ST_XAMB) != 0u)) << 32);
-                while (pend) {
+                while (GD_UNLIKELY(pend != 0ull)) {
                   const uint32_t bit = uint32_t(__ffsll(static_cast<long long>(pend)) - 1);
                   pend &= pend - 1;
                   const uint32_t src = bit & 31u, h = bit >> 5;
                   const uint32_t k = (h == 0 ? 1u : 33u) + src;
                   ++st_sexact;
+                  if (lane == 0) sweep_ctr[warp][9] += 1u;
                   get_axis();
                   const bool cl = exact_clash_g<NS>(b, it.m.atom_base, it.m.adj_base, n, X, GD_MO4(mo), true, pi,
                                                     frag_quat(pr.dtab[k], axis), pr.clash, true, lane);
@@ -1804,7 +1931,7 @@ __global__ void __launch_bounds__(NT, 1)
                 unsigned long long pend = __ballot_sync(FULL, need0) | (uint64_t(__ballot_sync(FULL, need1)) << 32);
                 const unsigned long long allout = __ballot_sync(FULL, (res_st[0] & ST_ALLOUT) != 0u) |
                                                   (uint64_t(__ballot_sync(FULL, (res_st[1] & ST_ALLOUT) != 0u)) << 32);
-                while (pend) {
+                while (GD_UNLIKELY(pend != 0ull)) {
                   const uint32_t bit = uint32_t(__ffsll(static_cast<long long>(pend)) - 1);
                   pend &= pend - 1;
                   if ((allout >> bit) & 1ull) {
@@ -1813,6 +1940,8 @@ __global__ void __launch_bounds__(NT, 1)
                   }
                   const uint32_t k = ((bit >> 5) == 0 ? 1u : 33u) + (bit & 31u);
                   ++st_sexact;
+                  const uint32_t stk = __shfl_sync(FULL, (bit >> 5) == 0 ? res_st[0] : res_st[1], bit & 31u);
+                  if (lane == 0) sweep_ctr[warp][((allout >> bit) & 1ull) ? 7 : (stk & ST_SAMB) ? 8 : 6] += 1u;
                   get_axis();
                   const double sk = exact_candidate_score_g<NS>(pk, n, X, ES, GD_MO4(mo), true, pi,
                                                                 frag_quat(pr.dtab[k], axis), lane, SCR1);
@@ -1830,7 +1959,7 @@ __global__ void __launch_bounds__(NT, 1)
             step_k = int32_t(bk);
             score = bs;
             ++st_commit;
-            if (bk != 0) {  // commit = rotate_fragment(current, r, k*delta), FP64
+            if (GD_UNLIKELY(bk != 0)) {  // commit = rotate_fragment(current, r, k*delta), FP64
               get_axis();
               const double4 dt = pr.dtab[bk];
               const Qd q = frag_quat(dt, axis);
@@ -1848,6 +1977,7 @@ __global__ void __launch_bounds__(NT, 1)
                 }
               __syncwarp();
               pend_r = r;  // the caches of the moved atoms are rebuilt at the top of the next step
+              if (lane == 0) sweep_ctr[warp][5] += 1u;
               vmask = 0u;  // the pose changed: every cached step head is stale
             }
           }
@@ -1863,7 +1993,7 @@ __global__ void __launch_bounds__(NT, 1)
       b.rs_score[item] = score;
       uint32_t* c = sweep_ctr[warp];
       if ((c[3] | c[4]) >= 0x80000000u) {  // keep the 32-bit per-warp counters far from wrapping
-        for (int i = 0; i < 5; ++i) {
+        for (int i = 0; i < int(kSweepCtr); ++i) {
           atomicAdd(b.stats + 16 + i, (unsigned long long)c[i]);
           c[i] = 0u;
         }
@@ -1884,7 +2014,7 @@ __global__ void __launch_bounds__(NT, 1)
 #endif
   }
   __syncthreads();
-  if (threadIdx.x < 5) {
+  if (threadIdx.x < kSweepCtr) {
     unsigned long long t = 0ull;
     for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) t += sweep_ctr[w][threadIdx.x];
     atomicAdd(b.stats + 16 + threadIdx.x, t);
@@ -1937,7 +2067,9 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   const uint32_t npad_max = (b.max_n + 3) & ~3u;
   const uint32_t slot_a = 4 * npad_max;                    // A (float4 per atom)
   // A (4 floats/atom) + SCR1 (1 double/atom) + PL + X (3 doubles/atom) + ES (1 double/atom)
-  const uint32_t slot_b = 6 * npad_max + 4 * pair_cap<NS>() + 8 * npad_max + 32 + 2 * npad_max;
+  // + CR and BR (NS words per atom each) + ZL (+ counter) + DINV
+  const uint32_t slot_b = 6 * npad_max + 4 * pair_cap<NS>() + 8 * npad_max + 32 + 2 * npad_max + 2 * NS * npad_max +
+                          kZCap + 4 + npad_max;
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
   // cells in shared memory: issue-bound, 16 warps x 128 registers; cells through L1 (large grids):
   // 12 warps x 151 registers (C5 +4 %)
@@ -1952,7 +2084,7 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
     if ((e = cudaStreamWaitEvent(stream_b, mid, 0)) != cudaSuccess) return e;
     stream = stream_b;
   }
-  constexpr size_t kK1bStatic = 1024;  // the kernel's __shared__ DevPocket + per-warp counters, rounded up
+  constexpr size_t kK1bStatic = 2048;  // the kernel's __shared__ DevPocket + per-warp counters, rounded up
   SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC, kK1bStatic);
   if (pb.warps < 1) return cudaErrorInvalidConfiguration;
   // the FP64 field goes to shared memory too when it fits beside the slots (24^3: 110 KB)
@@ -1960,7 +2092,10 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t field_bytes = size_t(pk.dims[0]) * pk.dims[1] * pk.dims[2] * sizeof(double);
-  const uint32_t fs = pb.smem + field_bytes + kK1bStatic <= size_t(optin) ? 1u : 0u;
+#ifndef GD_K1B_FIELD_SMEM
+#define GD_K1B_FIELD_SMEM 1
+#endif
+  const uint32_t fs = GD_K1B_FIELD_SMEM && pb.smem + field_bytes + kK1bStatic <= size_t(optin) ? 1u : 0u;
   if (fs) pb.smem += field_bytes;
   auto kb = pb.cells_in_smem ? dock_fast_kernel<NS, NTB, true> : dock_fast_kernel<NS, NTB, false>;
   e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pb.smem));

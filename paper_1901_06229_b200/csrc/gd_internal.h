@@ -52,6 +52,8 @@ struct DevParams {
   const double4* dtab;     // S entries: (cos(k*delta/2), sin(k*delta/2), k*delta, 0)
   const float2* dtab_f;    // S entries: (cos, sin) in FP32 (coarse path)
   const float4* frames;    // b*c x 3 float4 rows of Ry(beta_j) Rz(gamma_k) / spacing (separable coarse path)
+  const uint32_t* frame_tab;  // kept frames + twin lists of the separable coarse path (upload_grid_f)
+  uint32_t n_kept;         // frames the coarse alignment screens (the others are twins of these)
   float2 acs[16];          // (cos alpha_i, sin alpha_i), i < steps[0] (kernel parameter: constant bank)
   uint32_t steps[3];       // rotation_steps
   uint32_t n_restarts;
