@@ -152,6 +152,7 @@ struct gd_ctx {
   float4* d_frames = nullptr;
   uint32_t* d_frame_tab = nullptr;  // K1a frame schedule: kept frames + twin table (upload_grid_f)
   uint32_t n_kept = 0;
+  uint32_t n_twin_frames = 0;
   double4* d_dtab = nullptr;
   float2* d_dtab_f = nullptr;
   uint32_t G = 0;
@@ -191,7 +192,7 @@ struct Layout {
   size_t n_items = 0;
   std::vector<uint32_t> mask_base, adj_base;
   size_t o_meta, o_atoms, o_start, o_rots, o_dih0, o_masks, o_adj, o_dfs, o_rdfs, o_adjd, host_bytes;
-  size_t o_cand, o_ncand, o_rs_score, o_rs_ascore, o_rs_aidx, o_rs_stepk;
+  size_t o_cand, o_ncand, o_rs_score, o_rs_ascore, o_rs_aidx, o_rs_stepk, o_rs_pose, o_rs_es, o_rs_ext;
   size_t o_best, o_brs, o_fxyz, o_fdih, o_ctr, o_order, o_ord_scr, o_ord_tmp, ord_tmp_bytes = 0, total;
 };
 
@@ -404,8 +405,20 @@ int upload_grid_f(gd_ctx* ctx) {
       }
       if (rep[f] < 0) kept.push_back(f);
     }
-    std::vector<uint32_t> tab(nf + kept.size(), 0u);
-    for (uint32_t i = 0; i < kept.size(); ++i) tab[nf + i] = kept[i];
+    // K1a work units (kept frame, first of two quarter-turn groups c0), ordered by (gamma, c0, beta):
+    // consecutive lanes take neighbouring beta rows, so the 8 lanes of one shared-memory phase
+    // sample nearby points and share cells (fewer bank conflicts; tools/bank_sim.py: 9.4 -> 6.5
+    // wavefronts per LDS.128 on C2).
+    const uint32_t nq = na / 4;
+    std::vector<uint32_t> units;
+    for (uint32_t k = 0; k < st[2]; ++k)
+      for (uint32_t c0 = 0; c0 < std::max<uint32_t>(nq, 1); c0 += 2)
+        for (uint32_t j = 0; j < st[1]; ++j) {
+          const uint32_t f = j * st[2] + k;
+          if (std::find(kept.begin(), kept.end(), f) != kept.end()) units.push_back(f | (c0 << 16));
+        }
+    std::vector<uint32_t> tab(nf + units.size(), 0u);
+    for (uint32_t i = 0; i < units.size(); ++i) tab[nf + i] = units[i];
     for (uint32_t f0 : kept) {
       uint32_t cnt = 0;
       const uint32_t off = uint32_t(tab.size());
@@ -418,13 +431,18 @@ int upload_grid_f(gd_ctx* ctx) {
     }
     for (uint32_t f = 0; f < nf; ++f)
       if (rep[f] >= 0) tab[f] = 0xffffffffu;
-    if (const char* env = std::getenv("GD_NO_TWINS"))  // experiments: screen every frame
+    if (const char* env = std::getenv("GD_NO_TWINS"))  // experiments: screen every frame, frame-major units
       if (env[0] == '1') {
-        tab.assign(2 * size_t(nf), 0u);
-        for (uint32_t f = 0; f < nf; ++f) tab[nf + f] = f;
-        kept.assign(nf, 0u);
+        units.clear();
+        for (uint32_t f = 0; f < nf; ++f)
+          for (uint32_t c0 = 0; c0 < std::max<uint32_t>(nq, 1); c0 += 2) units.push_back(f | (c0 << 16));
+        tab.assign(nf + units.size(), 0u);
+        for (uint32_t i = 0; i < units.size(); ++i) tab[nf + i] = units[i];
       }
-    ctx->n_kept = uint32_t(kept.size());
+    ctx->n_kept = uint32_t(units.size());  // K1a work units
+    ctx->n_twin_frames = nf - uint32_t(kept.size());
+    if (const char* env = std::getenv("GD_NO_TWINS"))
+      if (env[0] == '1') ctx->n_twin_frames = 0;
     cudaFree(ctx->d_frame_tab);
     ctx->d_frame_tab = nullptr;
     GD_CUDA(ctx, cudaMalloc(&ctx->d_frame_tab, sizeof(uint32_t) * tab.size()));
@@ -489,6 +507,7 @@ DevParams dev_params(const gd_ctx* ctx) {
   pr.frames = ctx->d_frames;
   pr.frame_tab = ctx->d_frame_tab;
   pr.n_kept = ctx->n_kept;
+  pr.n_twin_frames = ctx->n_twin_frames;
   for (int i = 0; i < 3; ++i) pr.steps[i] = ctx->params.rotation_steps[i];
   for (uint32_t i = 0; i < 16; ++i) {
     const double alpha = i < pr.steps[0] ? gdh::kTwoPi * static_cast<double>(i) / static_cast<double>(pr.steps[0]) : 0.0;
@@ -824,6 +843,9 @@ Layout plan_layout(const gd_library* lib, const gd_params& P) {
   y.o_rs_ascore = ar.take<double>(y.n_items);
   y.o_rs_aidx = ar.take<uint32_t>(y.n_items);
   y.o_rs_stepk = ar.take<int32_t>(size_t(y.Rt) * N * reps);
+  y.o_rs_pose = ar.take<double>(size_t(y.A) * N * 3);  // K1r -> K1b: aligned FP64 pose per restart
+  y.o_rs_es = ar.take<double>(size_t(y.A) * N);        // and its exact per-atom samples
+  y.o_rs_ext = ar.take<float>(y.n_items);
   y.o_best = ar.take<double>(L);
   y.o_brs = ar.take<uint32_t>(L);
   y.o_fxyz = ar.take<double>(size_t(y.A) * 3);
@@ -1115,6 +1137,9 @@ DevBatch bind_batch(const gd_ctx* ctx, const Layout& y, unsigned char* D, uint32
   d.rs_align_score = reinterpret_cast<double*>(D + y.o_rs_ascore);
   d.rs_align_index = reinterpret_cast<uint32_t*>(D + y.o_rs_aidx);
   d.rs_step_k = reinterpret_cast<int32_t*>(D + y.o_rs_stepk);
+  d.rs_pose = reinterpret_cast<double*>(D + y.o_rs_pose);
+  d.rs_es = reinterpret_cast<double*>(D + y.o_rs_es);
+  d.rs_ext = reinterpret_cast<float*>(D + y.o_rs_ext);
   d.best_score = reinterpret_cast<double*>(D + y.o_best);
   d.best_restart = reinterpret_cast<uint32_t*>(D + y.o_brs);
   d.final_xyz = reinterpret_cast<double*>(D + y.o_fxyz);

@@ -88,6 +88,9 @@ __host__ __device__ constexpr uint32_t pair_cap() { return 32u * NS + 32u; }
 #ifndef GD_ALIGN_THREADS_L1
 #define GD_ALIGN_THREADS_L1 384  // K1a when the cells do not fit shared memory (read through L1)
 #endif
+#ifndef GD_REFINE_THREADS
+#define GD_REFINE_THREADS 512  // K1r: 16 warps x 128 registers (1024 threads spill the FP64 scorer)
+#endif
 #ifndef GD_FAST_THREADS_NS4
 #define GD_FAST_THREADS_NS4 256  // NS = 4: 255 registers (no spills) beat 16 warps at 128 (C4 clash 0.1 +15 %)
 #endif
@@ -630,20 +633,22 @@ __global__ void __launch_bounds__(NT, 1)
     // and cell plane are shared by the alpha rotations and x, y need a 2D rotation only.
     const uint32_t n_frames = pr.steps[1] * pr.steps[2];
     const bool separable = pr.steps[0] >= 8 && pr.steps[0] <= 16 && n_frames <= 128;
-    // quarter-turn units (see the loop below): per restart n_units = kept frames x upf
+    // quarter-turn units (see the loop below): (kept frame, c0) in upload_grid_f's order
     const bool qt = separable && pr.steps[0] % (4 * kQtGroups) == 0;
-    const uint32_t nq = pr.steps[0] / 4, upf = qt ? nq / kQtGroups : 1u;
-    const uint32_t n_units = qt ? pr.n_kept * upf : 0u;
+    const uint32_t nq = pr.steps[0] / 4;
+    static_assert(kQtGroups == 2, "upload_grid_f builds K1a's work units for two quarter-turn groups");
+    const uint32_t n_units = qt ? pr.n_kept : 0u;
     const uint32_t n_full = n_units & ~31u, n_rem = n_units - n_full;
     const uint32_t gsz = n_rem <= 1u ? 32u : 32u >> (32 - __clz(n_rem - 1u));  // lanes per shared unit
+    const uint32_t lgsz = 31u - __clz(gsz);
     const uint32_t n_iter = n_full / 32u + (n_rem ? 1u : 0u);
-    const bool twins = qt && pr.n_kept < n_frames;
-    auto unit_of = [&](uint32_t mu) -> uint32_t { return mu * 32u >= n_full ? n_full + lane / gsz : lane + 32u * mu; };
+    const bool twins = qt && pr.n_twin_frames > 0;
+    auto unit_of = [&](uint32_t mu) -> uint32_t { return mu * 32u >= n_full ? n_full + (lane >> lgsz) : lane + 32u * mu; };
     auto amb_to_g = [&](uint32_t bit) -> uint32_t {
       if (qt) {  // bit = 8 mu + 4 gi + q of the lane's unit mu
         const uint32_t u = unit_of(bit >> 3);
-        const uint32_t ia = (u % upf) * kQtGroups + ((bit >> 2) & 1u) + (bit & 3u) * nq;
-        return ia * n_frames + __ldg(pr.frame_tab + n_frames + u / upf);
+        const uint32_t ue = __ldg(pr.frame_tab + n_frames + u);
+        return ((ue >> 16) + ((bit >> 2) & 1u) + (bit & 3u) * nq) * n_frames + (ue & 0xffffu);
       }
       return separable ? (bit & 15u) * n_frames + lane + 32u * (bit >> 4) : lane + 32u * bit;
     };
@@ -712,10 +717,10 @@ __global__ void __launch_bounds__(NT, 1)
         for (uint32_t mu = 0; mu < n_iter; ++mu) {
           const bool coop = mu * 32u >= n_full;  // warp-uniform
           const uint32_t gs = coop ? gsz : 1u, sub = coop ? (lane & (gsz - 1u)) : 0u;
-          const uint32_t u = coop ? n_full + lane / gsz : lane + 32u * mu;
+          const uint32_t u = coop ? n_full + (lane >> lgsz) : lane + 32u * mu;
           const bool active = u < n_units;
-          const uint32_t f = active ? __ldg(pr.frame_tab + n_frames + u / upf) : 0u;
-          const uint32_t c0 = (u % upf) * kQtGroups;
+          const uint32_t ue = active ? __ldg(pr.frame_tab + n_frames + u) : 0u;
+          const uint32_t f = ue & 0xffffu, c0 = ue >> 16;
           const float4 F0 = __ldg(pr.frames + 3 * f), F1 = __ldg(pr.frames + 3 * f + 1), F2 = __ldg(pr.frames + 3 * f + 2);
           {
             float acc[4 * kQtGroups], amn[4 * kQtGroups];
@@ -742,7 +747,7 @@ __global__ void __launch_bounds__(NT, 1)
               cs_c[gi] = make_float2(cs[gi].y, cs[gi].x);
             }
             const float2 T2x = make_float2(tx, tx), T2y = make_float2(ty, ty);
-            const float2 M2 = make_float2(kMagic, kMagic), NM2 = make_float2(-kMagic, -kMagic);
+            const float2 M2 = make_float2(kMagic, kMagic), N12 = make_float2(-1.f, -1.f);
             auto atom2 = [&](uint32_t a, auto cls_tag) {
               constexpr int CLS = decltype(cls_tag)::value;
               const float4 v = A[a];
@@ -766,12 +771,13 @@ __global__ void __launch_bounds__(NT, 1)
   #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                   // samples q = 2h, 2h + 1: t + (rx, ry), t + (-ry, rx) | t - (rx, ry), t + (ry, -rx)
-                  const float2 gx = h == 0 ? __fadd2_rn(T2x, X01) : __fadd2_rn(T2x, make_float2(-X01.x, -X01.y));
-                  const float2 gy = h == 0 ? __fadd2_rn(T2y, Y01) : __fadd2_rn(T2y, make_float2(-Y01.x, -Y01.y));
+                  // (differences as fma(a, -1, b): the same rounding as b - a, without separate negations)
+                  const float2 gx = h == 0 ? __fadd2_rn(T2x, X01) : __ffma2_rn(X01, N12, T2x);
+                  const float2 gy = h == 0 ? __fadd2_rn(T2y, Y01) : __ffma2_rn(Y01, N12, T2y);
                   const float2 rX = __fadd2_rz(gx, M2), rY = __fadd2_rz(gy, M2);
-                  const float2 tX = __fadd2_rn(rX, NM2), tY = __fadd2_rn(rY, NM2);  // floor(g), exact
-                  const float2 fX = __fadd2_rn(gx, make_float2(-tX.x, -tX.y));
-                  const float2 fY = __fadd2_rn(gy, make_float2(-tY.x, -tY.y));
+                  const float2 ntX = __ffma2_rn(rX, N12, M2), ntY = __ffma2_rn(rY, N12, M2);  // -floor(g), exact
+                  const float2 fX = __fadd2_rn(gx, ntX);
+                  const float2 fY = __fadd2_rn(gy, ntY);
                   uint32_t ad0 = __float_as_uint(rY.x) * cx16 + (__float_as_uint(rX.x) * 16u + zoff16);
                   uint32_t ad1 = __float_as_uint(rY.y) * cx16 + (__float_as_uint(rX.y) * 16u + zoff16);
                   if (CLS == 1) {
@@ -792,7 +798,7 @@ __global__ void __launch_bounds__(NT, 1)
                   const float2 c1 = __ffma2_rn(FZ, make_float2(dec_dz(wA.z), dec_dz(wB.z)), make_float2(dec_c0(wA.z), dec_c0(wB.z)));
                   const float2 d1 = __ffma2_rn(FZ, make_float2(dec_dz(wA.w), dec_dz(wB.w)), make_float2(dec_d0(wA.w), dec_d0(wB.w)));
                   const float2 x0 = __ffma2_rn(fX, d0, c0), x1 = __ffma2_rn(fX, d1, c1);
-                  const float2 dx = __fadd2_rn(x1, make_float2(-x0.x, -x0.y));
+                  const float2 dx = __ffma2_rn(x0, N12, x1);
                   const float2 r = __ffma2_rn(fY, dx, __ffma2_rn(fX, NK, x0));
                   acc2[2 * gi + h] = __fadd2_rn(acc2[2 * gi + h], r);
                 }
@@ -987,6 +993,169 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 
+// ============================================================================ K1r: exact alignment
+// Per (ligand, restart): the FP64 start pose (docking.cpp:52-69), K1a's candidate rotations
+// re-scored in the reference's arithmetic (best_rotation_in_range + combine, docking.cpp:71-108;
+// every rotation when K1a handed over the restart), apply_rotation_choice (docking.cpp:110-118),
+// and the exact per-atom samples of the aligned pose: handed to K1b through HBM (rs_pose, rs_es),
+// so the sweep kernel holds only the sweep (its instruction footprint). Warp per
+// restart, pose in the warp's shared slot (3 n doubles) + 3 n doubles of index-order scratch.
+template <int NS, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    align_refine_kernel(DevPocket pk_in, DevParams pr, DevBatch b, uint32_t slot_doubles, uint32_t field_in_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ DevPocket spk;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) spk = pk_in;
+  __syncthreads();
+  DevPocket& pk = spk;
+  double* slots = reinterpret_cast<double*>(smem_raw);
+  if (field_in_smem) {
+    double* sf = slots + size_t(blockDim.x >> 5) * slot_doubles;
+    const uint32_t nv = pk.dims[0] * pk.dims[1] * pk.dims[2];
+    for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) sf[v] = pk_in.field[v];
+    if (threadIdx.x == 0) pk.field = sf;
+    __syncthreads();
+  }
+  const uint32_t npad = (b.max_n + 3) & ~3u;
+  double* X = slots + size_t(warp) * slot_doubles;  // pose, atom order
+  double* SCR = X + 3 * npad;                       // index-order sums
+  const uint32_t N = pr.n_restarts;
+  const uint64_t total = uint64_t(b.n_lig) * N;
+  uint32_t st_aexact = 0, st_afall = 0;
+  // centroid (geometry.cpp:40-46) of the pose in X: index-order sums of x, y, z (lanes 0, 1, 2)
+  // times 1/n
+  auto centroid = [&](uint32_t n) -> V3d {
+    double sum = 0.0;
+    if (lane < 3)
+      for (uint32_t a = 0; a < n; ++a) sum = __dadd_rn(sum, X[3 * a + lane]);
+    const V3d tot{__shfl_sync(FULL, sum, 0), __shfl_sync(FULL, sum, 1), __shfl_sync(FULL, sum, 2)};
+    return vscale(__ddiv_rn(1.0, double(n)), tot);
+  };
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(b.work_counter + 3, 1u);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= total) break;
+    if (b.order) item = b.order[item];
+    const uint32_t lig = item / N, rs = item - lig * N;
+    const LigMeta m = b.meta[lig];
+    const uint32_t n = m.n;
+    if (n > 32u * NS || n <= b.fast_min_n) continue;  // another launch's ligand (mixed batch)
+    // ---- starting pose (docking.cpp:52-69): r.apply(p - centroid) + target, FP64
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const uint32_t a = lane + 32 * s;
+      if (a < n) {
+        const double4 at = b.atoms[m.atom_base + a];
+        X[3 * a] = at.x;
+        X[3 * a + 1] = at.y;
+        X[3 * a + 2] = at.z;
+      }
+    }
+    __syncwarp();
+    {
+      const V3d c0 = centroid(n);
+      const double4 q4 = b.start[2 * size_t(item)];
+      const double4 t4 = b.start[2 * size_t(item) + 1];
+      const Qd qs{q4.x, q4.y, q4.z, q4.w};
+      const V3d tgt{t4.x, t4.y, t4.z};
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const uint32_t a = lane + 32 * s;
+        if (a < n) {
+          const V3d v = vadd(qapply(qs, vsub(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, c0)), tgt);
+          X[3 * a] = v.x;
+          X[3 * a + 1] = v.y;
+          X[3 * a + 2] = v.z;
+        }
+      }
+      __syncwarp();
+    }
+    const V3d cen = centroid(n);  // best_rotation_in_range's centroid (docking.cpp:76)
+    // the ligand extent about the centroid: K1b's position error bound
+    float ext = 0.f;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const uint32_t a = lane + 32 * s;
+      if (a < n) {
+        const V3d v = vsub(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, cen);
+        ext = fmaxf(ext, float(__dsqrt_rn(vdot(v, v))));
+      }
+    }
+    ext = warp_max(ext);
+    // ---- exact FP64 re-scoring of K1a's candidates, or (ncand < 0) of every rotation
+    const int32_t ncand = b.rs_ncand[item];
+    double best_s = -1.0;
+    uint32_t best_g = 0xffffffffu;
+    if (ncand < 0 || pr.G > 65535u) {
+      ++st_afall;
+      for (uint32_t g = lane; g < pr.G; g += 32) {
+        const double4 gq = pr.grid[g];
+        const double sc = exact_rotation_score(pk, X, n, cen, Qd{gq.x, gq.y, gq.z, gq.w});
+        if (best_g == 0xffffffffu || sc > best_s) {  // g ascending within a lane: first max wins
+          best_s = sc;
+          best_g = g;
+        }
+      }
+    } else {
+      // warp-cooperative: candidates one at a time, lanes over atoms, index-order sum / n
+      static_assert(kAlignCand <= 64, "two candidate words per lane");
+      const uint16_t* cl = b.rs_cand + size_t(item) * kAlignCand;
+      const uint32_t my_g0 = lane < uint32_t(ncand) ? cl[lane] : 0u;
+      const uint32_t my_g1 = lane + 32 < uint32_t(ncand) ? cl[lane + 32] : 0u;
+      for (int32_t c = 0; c < ncand; ++c) {
+        const uint32_t g = __shfl_sync(FULL, c < 32 ? my_g0 : my_g1, c & 31);
+        ++st_aexact;
+        const double4 gq = pr.grid[g];
+        const double sc = exact_candidate_score_g<NS>(pk, n, X, SCR, FULL, FULL, FULL, FULL, true, cen,
+                                                      Qd{gq.x, gq.y, gq.z, gq.w}, lane, SCR);
+        if (best_g == 0xffffffffu || sc > best_s || (sc == best_s && g < best_g)) {
+          best_s = sc;
+          best_g = g;
+        }
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {  // combine (docking.cpp:93-108)
+      const double os = __shfl_xor_sync(FULL, best_s, off);
+      const uint32_t og = __shfl_xor_sync(FULL, best_g, off);
+      if (og != 0xffffffffu && (best_g == 0xffffffffu || os > best_s || (os == best_s && og < best_g))) {
+        best_s = os;
+        best_g = og;
+      }
+    }
+    // ---- apply_rotation_choice (docking.cpp:110-118) + the exact samples of the aligned pose
+    {
+      const double4 gq = pr.grid[best_g];
+      const Qd q{gq.x, gq.y, gq.z, gq.w};
+      const size_t base = size_t(m.atom_base) * N + size_t(rs) * n;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const uint32_t a = lane + 32 * s;
+        if (a < n) {
+          const V3d v = rotated_about(V3d{X[3 * a], X[3 * a + 1], X[3 * a + 2]}, cen, q);
+          b.rs_pose[3 * (base + a)] = v.x;
+          b.rs_pose[3 * (base + a) + 1] = v.y;
+          b.rs_pose[3 * (base + a) + 2] = v.z;
+          b.rs_es[base + a] = sample_exact_ni(pk, v);
+        }
+      }
+    }
+    if (lane == 0) {
+      b.rs_align_index[item] = best_g;
+      b.rs_align_score[item] = best_s;
+      b.rs_ext[item] = ext;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    atomicAdd(b.stats + 1, (unsigned long long)st_aexact);
+    atomicAdd(b.stats + 2, (unsigned long long)st_afall);
+  }
+}
+
 // ============================================================================ the kernel
 // NT = threads per CTA (launch bound): 64 registers at 1024 threads spilled the smem bases inside
 // the hot loops, so the kernel trades warps for registers.
@@ -1024,9 +1193,7 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
   }
   float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
-  // Behind the atom slot, one double per atom: the FP64 scratch of the index-order sums (SCR1, n
-  // doubles, while A is live). Before the sweep A is not live yet and A + SCR1 hold 3 n doubles
-  // (SCR3, the centroid sums).
+  // Behind the atom slot, one double per atom: the FP64 scratch of the index-order sums (SCR1).
   uint32_t* SURV = reinterpret_cast<uint32_t*>(A + ((b.max_n + 3) & ~3u));
   // per-step cross-pair list (alpha, beta, gamma) behind SCR1, then the sweep's FP64 pose X (3 per
   // atom, atom order) and exact per-atom samples ES
@@ -1042,7 +1209,6 @@ __global__ void __launch_bounds__(NT, 1)
   uint32_t* ZL = AM + NS * ((b.max_n + 3) & ~3u);  // + its counter at ZL[kZCap]
   uint32_t* DINV = ZL + kZCap + 4;
   double* SCR1 = reinterpret_cast<double*>(SURV);
-  double* SCR3 = reinterpret_cast<double*>(A);
   const CoarseGrid cg{cells,
                       0.5f * float(pk.cell_dims[0]),
                       0.5f * float(pk.cell_dims[1]),
@@ -1056,7 +1222,7 @@ __global__ void __launch_bounds__(NT, 1)
   const uint64_t total = uint64_t(b.n_lig) * N;
   const bool skip_inv = (pr.mode & GD_FLAG_SKIP_INVARIANT_CLASH) != 0;
   // per-warp counters (32-bit: a warp's share of one launch stays far below 2^32)
-  uint32_t st_aexact = 0, st_afall = 0, st_sexact = 0, st_sfall = 0, st_commit = 0, st_items = 0;
+  uint32_t st_sexact = 0, st_sfall = 0, st_commit = 0, st_items = 0;
   // executed sweep work (the roofline's numerator counts only what ran): steps,
   // steps with an invariant clash, steps whose candidates were scored, moved-atom samples of the
   // scored candidates, and bump cross pairs (moved x fixed x candidates) of the steps that
@@ -1087,122 +1253,37 @@ __global__ void __launch_bounds__(NT, 1)
     it.W = (it.n + 31) >> 5;
     const uint32_t n = it.n, R = it.m.nr;
 
-    // ------------------------------------------------ starting pose (docking.cpp:52-69), FP64
-    Pose<NS> P;
+    // ------------------------------------------------ the aligned pose (K1r: start pose, exact
+    // alignment, apply_rotation_choice; docking.cpp:52-118) and its exact per-atom samples
     uint32_t pos[NS];
     double rad[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const uint32_t a = lane + 32 * s;
-      double4 at = make_double4(0.0, 0.0, 0.0, 0.0);
-      if (a < n) at = b.atoms[it.m.atom_base + a];
-      set_own(P, s, V3d{at.x, at.y, at.z});
-      rad[s] = at.w;
-      pos[s] = a < n ? b.dfs_pos[it.m.atom_base + a] : 0;
-      if (a < n) DINV[pos[s]] = a;
-    }
     {
-      const V3d c0 = centroid_smem<NS>(P, n, SCR3, lane);
-      const double4 q4 = b.start[2 * size_t(item)];
-      const double4 t4 = b.start[2 * size_t(item) + 1];
-      const Qd qs{q4.x, q4.y, q4.z, q4.w};
-      const V3d tgt{t4.x, t4.y, t4.z};
-#pragma unroll
-      for (int s = 0; s < NS; ++s) set_own(P, s, vadd(qapply(qs, vsub(own(P, s), c0)), tgt));
-    }
-    const V3d cen = centroid_smem<NS>(P, n, SCR3, lane);  // best_rotation_in_range's centroid (docking.cpp:76)
-    // FP64 start pose to the warp's X slot (read by the full FP64 alignment); the ligand extent
-    // about the centroid sets the position error bound of the FP32 sweep below.
-    float ext = 0.f;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const uint32_t a = lane + 32 * s;
-      if (a < n) {
-        X[3 * a] = P.x[s];
-        X[3 * a + 1] = P.y[s];
-        X[3 * a + 2] = P.z[s];
-        const V3d v = vsub(own(P, s), cen);
-        ext = fmaxf(ext, float(__dsqrt_rn(vdot(v, v))));
-      }
-    }
-    __syncwarp();
-    // Position error bound (grid units, per axis) of every FP32 coordinate this item produces:
-    // rounding of coordinates up to the grid size, plus the rotation error of the FP32 frames
-    // (the dihedral axis from FP32 endpoints is good to ~1e-6 rad) times the ligand extent.
-    // DESIGN.md §3.2 derives the constants.
-    const float ext_g = warp_max(ext) * pk.inv_spacing_f;
-    const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
-    const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
-    const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
-    const float inv_n_scale = pk.coarse_scale / float(n);
-
-    GD_T(2);
-    // ------------------------------------------------ exact FP64 re-scoring (docking.cpp:71-91) of
-    // K1a's candidate rotations, or (ncand < 0: overflow / plateau) of every rotation
-    const int32_t ncand = b.rs_ncand[item];
-    double best_s = -1.0;
-    uint32_t best_g = 0xffffffffu;
-    if (GD_UNLIKELY(ncand < 0 || pr.G > 65535u)) {
-      ++st_afall;
-      for (uint32_t g = lane; g < pr.G; g += 32) {
-        const double4 gq = pr.grid[g];
-        const double s = exact_rotation_score(pk, X, n, cen, Qd{gq.x, gq.y, gq.z, gq.w});
-        if (best_g == 0xffffffffu || s > best_s) {  // g ascending within a lane: first max wins
-          best_s = s;
-          best_g = g;
-        }
-      }
-    } else {
-      // warp-cooperative exact scoring: candidates one at a time, lanes over atoms (P still holds
-      // the start pose), index-order sum through shuffles; every lane ends with the same best
-      static_assert(kAlignCand <= 64, "two candidate words per lane");
-      const uint16_t* cl = b.rs_cand + size_t(item) * kAlignCand;
-      const uint32_t my_g0 = lane < uint32_t(ncand) ? cl[lane] : 0u;
-      const uint32_t my_g1 = lane + 32 < uint32_t(ncand) ? cl[lane + 32] : 0u;
-      for (int32_t c = 0; c < ncand; ++c) {
-        const uint32_t g = __shfl_sync(FULL, c < 32 ? my_g0 : my_g1, c & 31);
-        ++st_aexact;
-        const double4 gq = pr.grid[g];
-        // the dihedral candidates' exact scorer with every atom rotated about the centroid: the
-        // same rotated_about, sample_field and index-order sum / n as docking.cpp:77-83
-        const double sc = exact_candidate_score_g<NS>(pk, n, X, ES, FULL, FULL, FULL, FULL, true, cen,
-                                                      Qd{gq.x, gq.y, gq.z, gq.w}, lane, SCR1);
-        if (best_g == 0xffffffffu || sc > best_s || (sc == best_s && g < best_g)) {
-          best_s = sc;
-          best_g = g;
-        }
-      }
-    }
-    for (int off = 16; off > 0; off >>= 1) {  // combine (docking.cpp:93-108)
-      const double os = __shfl_xor_sync(FULL, best_s, off);
-      const uint32_t og = __shfl_xor_sync(FULL, best_g, off);
-      if (og != 0xffffffffu && (best_g == 0xffffffffu || os > best_s || (os == best_s && og < best_g))) {
-        best_s = os;
-        best_g = og;
-      }
-    }
-    {  // apply_rotation_choice (docking.cpp:110-118)
-      const double4 gq = pr.grid[best_g];
-      const Qd q{gq.x, gq.y, gq.z, gq.w};
+      const size_t base = size_t(it.m.atom_base) * N + size_t(it.rs) * n;
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const uint32_t a = lane + 32 * s;
-        set_own(P, s, rotated_about(own(P, s), cen, q));
         rad[s] = a < n ? b.atoms[it.m.atom_base + a].w : 0.0;
         pos[s] = a < n ? b.dfs_pos[it.m.atom_base + a] : 0;
-        if (a < n) {  // from here on the pose lives in the warp's shared slot
-          X[3 * a] = P.x[s];
-          X[3 * a + 1] = P.y[s];
-          X[3 * a + 2] = P.z[s];
+        if (a < n) {
+          DINV[pos[s]] = a;
+          X[3 * a] = b.rs_pose[3 * (base + a)];
+          X[3 * a + 1] = b.rs_pose[3 * (base + a) + 1];
+          X[3 * a + 2] = b.rs_pose[3 * (base + a) + 2];
+          ES[a] = b.rs_es[base + a];
         }
       }
       __syncwarp();
     }
-    double score = best_s;
-    if (lane == 0) {
-      b.rs_align_index[item] = best_g;
-      b.rs_align_score[item] = best_s;
-    }
+    // Position error bound (grid units, per axis) of every FP32 coordinate this item produces:
+    // rounding of coordinates up to the grid size, plus the rotation error of the FP32 frames
+    // (the dihedral axis from FP32 endpoints is good to ~1e-6 rad) times the ligand extent.
+    // DESIGN.md §3.3 derives the constants.
+    const float ext_g = b.rs_ext[item] * pk.inv_spacing_f;
+    const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
+    const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
+    const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
+    const float inv_n_scale = pk.coarse_scale / float(n);
+    double score = b.rs_align_score[item];
     // (the final pose and dihedrals are replayed by K2 from the decision trace)
 
     // ------------------------------------------------ dihedral sweep (docking.cpp:155-167, 197-215)
@@ -1270,7 +1351,6 @@ __global__ void __launch_bounds__(NT, 1)
             const float gy = float(__dmul_rn(__dsub_rn(pa.y, pk.origin[1]), pk.inv_spacing));
             const float gz = float(__dmul_rn(__dsub_rn(pa.z, pk.origin[2]), pk.inv_spacing));
             A[pick<NS>(pos, s)] = make_float4(gx, gy, gz, pick<NS>(rho, s));
-            if (all) ES[a] = sample_exact_ni(pk, pa);  // after a commit ES is already the new one
             float am = 1e30f;
             put<NS>(cs, s, coarse_sample(cg, gx, gy, gz, am));
             put<NS>(samb, s, am <= ptol);
@@ -2003,8 +2083,6 @@ __global__ void __launch_bounds__(NT, 1)
   }
   if (lane == 0) {
     atomicAdd(b.stats + 0, (unsigned long long)st_items);
-    atomicAdd(b.stats + 1, (unsigned long long)st_aexact);
-    atomicAdd(b.stats + 2, (unsigned long long)st_afall);
     atomicAdd(b.stats + 3, (unsigned long long)st_sexact);
     atomicAdd(b.stats + 4, (unsigned long long)st_sfall);
     atomicAdd(b.stats + 5, (unsigned long long)st_commit);
@@ -2083,6 +2161,22 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   if (stream_b && stream_b != stream) {  // K1b on its own stream, after this batch's K1a
     if ((e = cudaStreamWaitEvent(stream_b, mid, 0)) != cudaSuccess) return e;
     stream = stream_b;
+  }
+  // K1r (exact alignment): 3 n doubles of pose + 3 n of scratch per warp, 32 warps, FP64 field in
+  // shared memory when it fits
+  {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const uint32_t slot_r = 6 * npad_max;
+    size_t smem_r = size_t(slot_r) * sizeof(double) * (GD_REFINE_THREADS / 32);
+    const size_t fbytes = size_t(pk.dims[0]) * pk.dims[1] * pk.dims[2] * sizeof(double);
+    const uint32_t fs_r = smem_r + fbytes + 1024 <= size_t(optin) ? 1u : 0u;
+    if (fs_r) smem_r += fbytes;
+    auto kr = align_refine_kernel<NS, GD_REFINE_THREADS>;
+    if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_r))) != cudaSuccess) return e;
+    kr<<<n_sms, GD_REFINE_THREADS, smem_r, stream>>>(pk, pr, b, slot_r, fs_r);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   constexpr size_t kK1bStatic = 2048;  // the kernel's __shared__ DevPocket + per-warp counters, rounded up
   SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC, kK1bStatic);

@@ -52,8 +52,9 @@ struct DevParams {
   const double4* dtab;     // S entries: (cos(k*delta/2), sin(k*delta/2), k*delta, 0)
   const float2* dtab_f;    // S entries: (cos, sin) in FP32 (coarse path)
   const float4* frames;    // b*c x 3 float4 rows of Ry(beta_j) Rz(gamma_k) / spacing (separable coarse path)
-  const uint32_t* frame_tab;  // kept frames + twin lists of the separable coarse path (upload_grid_f)
-  uint32_t n_kept;         // frames the coarse alignment screens (the others are twins of these)
+  const uint32_t* frame_tab;  // twin lists + K1a work units of the separable coarse path (upload_grid_f)
+  uint32_t n_kept;         // K1a work units (kept frame | c0 << 16); twin frames are not screened
+  uint32_t n_twin_frames;  // frames folded into a kept frame (0: every frame is screened)
   float2 acs[16];          // (cos alpha_i, sin alpha_i), i < steps[0] (kernel parameter: constant bank)
   uint32_t steps[3];       // rotation_steps
   uint32_t n_restarts;
@@ -93,6 +94,12 @@ struct DevBatch {
   double* rs_align_score;
   uint32_t* rs_align_index;
   int32_t* rs_step_k;      // rot_base*N*reps + (restart*reps + rep)*R + r
+  // K1r -> K1b (fast path): the aligned FP64 pose of restart rs of ligand l at
+  // rs_pose[3 (atom_base(l) N + rs n(l) + a) ..], its exact per-atom samples in rs_es (same index /
+  // 3), and the ligand's extent about its centroid (the coarse position bound) in rs_ext[item]
+  double* rs_pose;
+  double* rs_es;
+  float* rs_ext;
   // per-ligand results
   double* best_score;
   uint32_t* best_restart;

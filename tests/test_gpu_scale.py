@@ -44,9 +44,25 @@ def test_fast_equals_exact_at_scale(pair, count, atoms, rots, clash, grid):
     out = fast.dock(lib, pocket, p, trace=True)
     st = fast.stats()
     _same(out, exact.dock(lib, pocket, p, trace=True))
-    if (count, atoms, clash) == (1200, 40, 0.75):
-        # K1a's second coarse pass (a lane's top-4 overflowed) occurs at this size and is exact too
-        assert st["align_second_passes"] > 0, st
+    assert st["restarts"] == count * p.n_restarts, st
+
+
+def test_second_pass_on_plateau(pair):
+    """A field clamped to 1.0 over the whole box (the reference clamps its blobs to [0, 1],
+    generate.cpp:44-64): every rotation that keeps the ligand inside ties exactly, so K1a's lanes
+    overflow their top-4, collect every candidate in a second pass (with the twin rotations of the
+    folded frames), overflow the 64-entry list and hand the restart to the FP64 alignment. The
+    argmax is the lowest such index (docking.cpp:84), as in the all-FP64 kernel."""
+    fast, exact = pair
+    n = 24
+    field = np.ones(n ** 3)
+    pocket = gd.Pocket((n, n, n), (0.0, 0.0, 0.0), 0.75, field)
+    lib = gd.make_library(gd.LibrarySpec(40, 12, 3, 9))
+    p = gd.DockParams(n_restarts=8, clash_factor=0.3)
+    out = fast.dock(lib, pocket, p, trace=True)
+    st = fast.stats()
+    assert st["align_second_passes"] > 0, st
+    _same(out, exact.dock(lib, pocket, p, trace=True))
 
 
 def test_executor_chunks_match_staged_run(pair):
