@@ -111,7 +111,8 @@ typedef struct {
   uint64_t align_exact_evals;  /* FP64 re-scored alignment candidates              */
   uint64_t align_fallbacks;    /* restarts whose alignment fell back to full FP64   */
   uint64_t step_exact_evals;   /* FP64 re-scored dihedral candidates               */
-  uint64_t step_fallbacks;     /* dihedral steps evaluated fully in FP64           */
+  uint64_t step_fallbacks;     /* restarts the fast sweep handed to the FP64 kernel (razor-thin
+                                  pairs in a moving fragment, non-tree layouts, S outside [2,64]) */
   uint64_t commits;            /* committed dihedral steps                          */
   uint64_t h2d_bytes;          /* bytes uploaded by the last gd_stage               */
   uint64_t d2h_bytes;          /* bytes downloaded by the last gd_fetch             */

@@ -192,7 +192,7 @@ struct Layout {
   size_t n_items = 0;
   std::vector<uint32_t> mask_base, adj_base;
   size_t o_meta, o_atoms, o_start, o_rots, o_dih0, o_masks, o_adj, o_dfs, o_rdfs, o_adjd, host_bytes;
-  size_t o_cand, o_ncand, o_rs_score, o_rs_ascore, o_rs_aidx, o_rs_stepk, o_rs_pose, o_rs_es, o_rs_ext;
+  size_t o_cand, o_ncand, o_rs_score, o_rs_ascore, o_rs_aidx, o_rs_stepk, o_rs_pose, o_rs_es, o_rs_ext, o_slow;
   size_t o_best, o_brs, o_fxyz, o_fdih, o_ctr, o_order, o_ord_scr, o_ord_tmp, ord_tmp_bytes = 0, total;
 };
 
@@ -846,6 +846,7 @@ Layout plan_layout(const gd_library* lib, const gd_params& P) {
   y.o_rs_pose = ar.take<double>(size_t(y.A) * N * 3);  // K1r -> K1b: aligned FP64 pose per restart
   y.o_rs_es = ar.take<double>(size_t(y.A) * N);        // and its exact per-atom samples
   y.o_rs_ext = ar.take<float>(y.n_items);
+  y.o_slow = ar.take<uint32_t>(y.n_items);  // K1b -> FP64 kernel: restarts handed over
   y.o_best = ar.take<double>(L);
   y.o_brs = ar.take<uint32_t>(L);
   y.o_fxyz = ar.take<double>(size_t(y.A) * 3);
@@ -1140,11 +1141,13 @@ DevBatch bind_batch(const gd_ctx* ctx, const Layout& y, unsigned char* D, uint32
   d.rs_pose = reinterpret_cast<double*>(D + y.o_rs_pose);
   d.rs_es = reinterpret_cast<double*>(D + y.o_rs_es);
   d.rs_ext = reinterpret_cast<float*>(D + y.o_rs_ext);
+  d.slow_items = reinterpret_cast<uint32_t*>(D + y.o_slow);
   d.best_score = reinterpret_cast<double*>(D + y.o_best);
   d.best_restart = reinterpret_cast<uint32_t*>(D + y.o_brs);
   d.final_xyz = reinterpret_cast<double*>(D + y.o_fxyz);
   d.final_dih = reinterpret_cast<double*>(D + y.o_fdih);
   d.work_counter = reinterpret_cast<unsigned int*>(D + y.o_ctr);
+  d.slow_count = d.work_counter + 19;
   const bool ordered = y.n_items > 0 && !std::getenv("GD_NATURAL_ORDER");  // (A/B experiments)
   d.order = ordered ? reinterpret_cast<uint32_t*>(D + y.o_order) : nullptr;
   d.order_scratch = reinterpret_cast<uint32_t*>(D + y.o_ord_scr);
@@ -1176,14 +1179,9 @@ int launch_batch(gd_ctx* ctx, const DevBatch& d, cudaStream_t s, cudaEvent_t* ev
   return GD_OK;
 }
 
-// name_of(l): the name of library ligand l (DegenerateAxisError names the ligand like the
-// reference, molecule.cpp:156-158)
-int read_device_status(gd_ctx* ctx, const std::function<std::string(uint32_t)>& name_of) {
-  int err[2] = {0, 0};
-  unsigned long long st[32];
-  GD_CUDA(ctx, cudaMemcpy(err, ctx->d_error, sizeof err, cudaMemcpyDeviceToHost));
-  GD_CUDA(ctx, cudaMemcpy(st, ctx->d_stats, sizeof st, cudaMemcpyDeviceToHost));
-  ctx->last.restarts = st[0];
+// The device counters (gd_stats order) into ctx->last.
+static void fill_stats(gd_ctx* ctx, const unsigned long long* st) {
+  ctx->last.restarts = st[0] + st[7];  // fast sweep + restarts it handed to the FP64 kernel
   ctx->last.align_exact_evals = st[1];
   ctx->last.align_fallbacks = st[2];
   ctx->last.step_exact_evals = st[3];
@@ -1200,6 +1198,16 @@ int read_device_status(gd_ctx* ctx, const std::function<std::string(uint32_t)>& 
   ctx->last.step_exact_allout_evals = st[23];
   ctx->last.step_exact_face_evals = st[24];
   ctx->last.step_exact_clash_evals = st[25];
+}
+
+// name_of(l): the name of library ligand l (DegenerateAxisError names the ligand like the
+// reference, molecule.cpp:156-158)
+int read_device_status(gd_ctx* ctx, const std::function<std::string(uint32_t)>& name_of) {
+  int err[2] = {0, 0};
+  unsigned long long st[32];
+  GD_CUDA(ctx, cudaMemcpy(err, ctx->d_error, sizeof err, cudaMemcpyDeviceToHost));
+  GD_CUDA(ctx, cudaMemcpy(st, ctx->d_stats, sizeof st, cudaMemcpyDeviceToHost));
+  fill_stats(ctx, st);
   if (err[0] == GD_ERR_DEGENERATE_AXIS) {
     return set_err(ctx, GD_ERR_DEGENERATE_AXIS, "rotamer axis atoms coincide in ligand '" + name_of(uint32_t(err[1])) + "'");
   }
@@ -1479,23 +1487,7 @@ int gd_last_stats(gd_ctx* ctx, gd_stats* out) {
       for (int i = 0; i < 8; ++i) std::fprintf(stderr, "phase %-16s %6.2f%%\n", names[i], tot ? 100.0 * st[8 + i] / tot : 0.0);
     }
   }
-  ctx->last.restarts = st[0];
-  ctx->last.align_exact_evals = st[1];
-  ctx->last.align_fallbacks = st[2];
-  ctx->last.step_exact_evals = st[3];
-  ctx->last.step_fallbacks = st[4];
-  ctx->last.commits = st[5];
-  ctx->last.align_second_passes = st[6];
-  ctx->last.sweep_steps = st[16];
-  ctx->last.sweep_invariant_steps = st[17];
-  ctx->last.sweep_scored_steps = st[18];
-  ctx->last.sweep_samples = st[19];
-  ctx->last.cross_pairs = st[20];
-  ctx->last.sweep_moves = st[21];
-  ctx->last.step_exact_score_evals = st[22];
-  ctx->last.step_exact_allout_evals = st[23];
-  ctx->last.step_exact_face_evals = st[24];
-  ctx->last.step_exact_clash_evals = st[25];
+  fill_stats(ctx, st);
   *out = ctx->last;
   return GD_OK;
 }

@@ -1284,10 +1284,22 @@ __global__ void __launch_bounds__(NT, 1)
     const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
     const float inv_n_scale = pk.coarse_scale / float(n);
     double score = b.rs_align_score[item];
+    // restarts this kernel does not decide go to the FP64 kernel, which repeats them in the
+    // reference's arithmetic throughout (launch_dock runs it after this kernel, on the same stream)
+    bool abandoned = false;
+    auto handoff = [&]() {
+      if (lane == 0) b.slow_items[atomicAdd(b.slow_count, 1u)] = item;
+      ++st_sfall;
+      --st_items;
+      abandoned = true;
+    };
     // (the final pose and dihedrals are replayed by K2 from the decision trace)
 
     // ------------------------------------------------ dihedral sweep (docking.cpp:155-167, 197-215)
-    if (R > 0 && pr.reps > 0 && pr.S > 0) {
+    // (non-tree layouts, whose moving sets are not DFS ranges, and S outside [2, 64] are the FP64
+    // kernel's)
+    if (R > 0 && pr.reps > 0 && pr.S > 0 && (!it.m.fast_ok || pr.S > 64 || pr.S < 2)) handoff();
+    if (R > 0 && pr.reps > 0 && pr.S > 0 && !abandoned) {
       // Per-restart register caches (no global load on a step's critical path): lane r holds
       // rotamer r's bond (i | j << 16) and DFS range (s0 | e0 << 16, pos(i)) for r < 32 (later
       // rotamers load from global), and the FP32 half-angle (cos, sin) of its candidates k = lane + 1
@@ -1574,33 +1586,11 @@ __global__ void __launch_bounds__(NT, 1)
       // (s0, e0), so both follow from the range.
       auto rot_masks = [&](uint32_t rr, uint2 ij_, uint32_t s0_, uint32_t e0_, uint32_t (&mo_)[NS],
                            uint32_t (&md_)[NS], bool (&inm_)[NS]) {
-        if (it.m.fast_ok) {
 #pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            inm_[s] = lane + 32 * s < n && pos[s] > s0_ && pos[s] < e0_;
-            mo_[s] = __ballot_sync(FULL, inm_[s]);  // slot s holds atoms 32 s + lane
-            md_[s] = range_word(uint32_t(s), s0_ + 1, e0_);
-          }
-        } else {
-#pragma unroll
-          for (int w = 0; w < NS; ++w) {
-            mo_[w] = uint32_t(w) < it.W ? __ldg(b.masks + it.m.mask_base + rr * it.W + w) : 0u;
-            md_[w] = 0u;
-          }
-#pragma unroll
-          for (int w = 0; w < NS; ++w)
-            if ((ij_.y >> 5) == uint32_t(w)) mo_[w] &= ~(1u << (ij_.y & 31));
-#pragma unroll
-          for (int s = 0; s < NS; ++s) {
-            const uint32_t a = lane + 32 * s;
-            inm_[s] = a < n && bit4(mo_, a);
-#pragma unroll
-            for (int w = 0; w < NS; ++w)
-              if (inm_[s] && (pos[s] >> 5) == uint32_t(w)) md_[w] |= 1u << (pos[s] & 31);
-          }
-#pragma unroll
-          for (int w = 0; w < NS; ++w)
-            for (int o = 16; o > 0; o >>= 1) md_[w] |= __shfl_xor_sync(FULL, md_[w], o);
+        for (int s = 0; s < NS; ++s) {
+          inm_[s] = lane + 32 * s < n && pos[s] > s0_ && pos[s] < e0_;
+          mo_[s] = __ballot_sync(FULL, inm_[s]);  // slot s holds atoms 32 s + lane
+          md_[s] = range_word(uint32_t(s), s0_ + 1, e0_);
         }
       };
 
@@ -1721,9 +1711,9 @@ __global__ void __launch_bounds__(NT, 1)
             }
             fsum = warp_sum(fsum);
             if (pr.S > 1) {
-              const float4 fi = A[it.m.fast_ok ? ipos : 0u], fj = A[it.m.fast_ok ? s0 : 0u];
+              const float4 fi = A[ipos], fj = A[s0];
               const float dx = fj.x - fi.x, dy = fj.y - fi.y, dz = fj.z - fi.z;
-              if (GD_UNLIKELY(!it.m.fast_ok || dx * dx + dy * dy + dz * dz < 1e-6f)) {
+              if (GD_UNLIKELY(dx * dx + dy * dy + dz * dz < 1e-6f)) {
                 const V3d qi{X[3 * ij.x], X[3 * ij.x + 1], X[3 * ij.x + 2]};
                 const V3d delta = vsub(V3d{X[3 * ij.y], X[3 * ij.y + 1], X[3 * ij.y + 2]}, qi);
                 if (__dsqrt_rn(vdot(delta, delta)) < 1e-12) {
@@ -1732,28 +1722,22 @@ __global__ void __launch_bounds__(NT, 1)
                 }
               }
             }
-            if (r < 32 && inv && !frag && it.m.fast_ok && pr.S >= 2 && pr.S <= 64) {
+            if (r < 32 && inv && !frag) {
               if (lane == 0) CF[r] = fsum;
               vmask |= 1u << r;
             }
           }
           {
-            uint32_t nm_c = e0 - s0 - 1;
-            if (!it.m.fast_ok) {
-              nm_c = 0;
-#pragma unroll
-              for (int w = 0; w < NS; ++w) nm_c += __popc(mo[w]);
-            }
-            const uint32_t n_k = pr.S > 0 ? pr.S - 1 : 0;
-            const bool slow = !it.m.fast_ok || frag || pr.S > 64 || pr.S < 2;
+            const uint32_t nm_c = e0 - s0 - 1;
+            const uint32_t n_k = pr.S - 1;
             if (lane == 0) {
               uint32_t* c = sweep_ctr[warp];
-              const bool scored = slow || !(skip_inv && inv);
+              const bool scored = !(skip_inv && inv);
               c[0] += 1u;
               c[1] += inv ? 1u : 0u;
               c[2] += scored ? 1u : 0u;
               c[3] += scored ? nm_c * n_k : 0u;
-              c[4] += scored && (!inv || frag) ? nm_c * (n - nm_c - 1) * n_k : 0u;
+              c[4] += scored && !inv ? nm_c * (n - nm_c - 1) * n_k : 0u;
             }
           }
           int32_t step_k = -1;
@@ -1768,27 +1752,12 @@ __global__ void __launch_bounds__(NT, 1)
               if (inm[t]) BEST[lane + 32 * t] = SCR1[lane + 32 * t];
           };
 
-          if (GD_UNLIKELY(!it.m.fast_ok || frag || pr.S > 64 || pr.S < 2)) {
-            // ---------------- slow path: every candidate exactly (non-tree layouts, pairs of the
-            // moving fragment within tau of the threshold, or unusual S)
-            ++st_sfall;
-            get_axis();
-            for (uint32_t k = 0; k < pr.S; ++k) {
-              const Qd q = frag_quat(pr.dtab[k], axis);
-              const double sk = exact_candidate_score_g<NS>(pk, n, X, ES, GD_MO4(mo), k != 0, pi, q, lane, SCR1);
-              bool clash;
-              if (k == 0) clash = !elig0;
-              else if (frag) clash = exact_clash_g<NS>(b, it.m.atom_base, it.m.adj_base, n, X, GD_MO4(mo), true, pi, q,
-                                                       pr.clash, false, lane);
-              else clash = inv || exact_clash_g<NS>(b, it.m.atom_base, it.m.adj_base, n, X, GD_MO4(mo), true, pi, q,
-                                                    pr.clash, true, lane);
-              if (!clash && (!committed || sk > bs)) {
-                committed = true;
-                bk = k;
-                bs = sk;
-                keep_best();
-              }
-            }
+          if (GD_UNLIKELY(frag)) {
+            // a pair of the moving fragment within the razor margin of its bump threshold (its
+            // FP64 distance moves by rounding under the rotation): the restart goes to the FP64
+            // kernel, which repeats it in the reference's arithmetic throughout
+            handoff();
+            break;
           } else if (!(skip_inv && inv)) {
             GD_T(5);
             // ---------------- coarse evaluation of every candidate k = 1 .. S-1 (faithful sweep)
@@ -2063,10 +2032,11 @@ __global__ void __launch_bounds__(NT, 1)
           }
           if (lane == 0) b.rs_step_k[trace_at] = step_k;
         }
-        if (*(volatile int*)b.error != 0) break;
+        if (abandoned || *(volatile int*)b.error != 0) break;
       }
     }
     if (*(volatile int*)b.error != 0) break;
+    if (abandoned) continue;
     GD_T(7);
     // ------------------------------------------------ restart result (K2 replays its pose)
     if (lane == 0) {

@@ -100,6 +100,11 @@ struct DevBatch {
   double* rs_pose;
   double* rs_es;
   float* rs_ext;
+  // restarts K1b hands to the FP64 kernel (a step it cannot decide with its cached pair state:
+  // razor-thin pairs inside the moving fragment, non-tree layouts, S outside [2, 64]); count in
+  // work_counter[19]
+  uint32_t* slow_items;
+  unsigned int* slow_count;  // = the batch's work_counter + 19 (class launches keep this pointer)
   // per-ligand results
   double* best_score;
   uint32_t* best_restart;

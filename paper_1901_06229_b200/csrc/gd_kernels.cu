@@ -54,7 +54,8 @@ __device__ __forceinline__ void st3(double* P, uint32_t a, V3d v) {
 // orders. Shared memory per warp: pose P[3n], candidate C[3n], samples S[n] (doubles).
 // --------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024, 1)
-    dock_exact_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t smem_stride, uint32_t min_n) {
+    dock_exact_kernel(DevPocket pk, DevParams pr, DevBatch b, uint32_t smem_stride, uint32_t min_n,
+                      uint32_t list_mode) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
@@ -65,21 +66,28 @@ __global__ void __launch_bounds__(1024, 1)
   const uint32_t N = pr.n_restarts;
   const uint64_t total = uint64_t(b.n_lig) * N;
 
+  // list mode: the restarts the fast sweep handed over (b.slow_items, b.slow_count of them)
+  const uint32_t n_list = list_mode ? *(volatile unsigned int*)b.slow_count : 0u;
   for (;;) {
     uint32_t item = 0;
     if (lane == 0) item = atomicAdd(b.work_counter, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= total) break;
+    if (list_mode) {
+      if (item >= n_list) break;
+      item = b.slow_items[item];
+    } else if (item >= total) {
+      break;
+    }
     if (*(volatile int*)b.error != 0) break;
     const uint32_t lig = item / N;
     const uint32_t rs = item - lig * N;
     const LigMeta m = b.meta[lig];
     const uint32_t n = m.n, R = m.nr, W = (n + 31) >> 5;
-    if (n < min_n) continue;  // mixed batch: the fast kernels' ligand
-    // min_n > 0: K1a (NS = 8) ran for these ligands; its candidate list (ncand >= 0) contains
+    if (!list_mode && n < min_n) continue;  // mixed batch: the fast kernels' ligand
+    // min_n > 0 (or list mode): K1a ran for these ligands; its candidate list (ncand >= 0) contains
     // every rotation that can be the exact argmax
     // (ligands beyond kAlignBigMaxAtoms had no K1a: every rotation in FP64)
-    const int32_t ncand = min_n > 0 && n <= kAlignBigMaxAtoms ? b.rs_ncand[item] : -1;
+    const int32_t ncand = (list_mode || min_n > 0) && n <= kAlignBigMaxAtoms ? b.rs_ncand[item] : -1;
 
     // ---- starting pose (docking.cpp:52-69); q and target come from the host packer (libm).
     for (uint32_t a = lane; a < n; a += 32) {
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(1024, 1)
     if (failed) break;
     // ---- restart result
     if (lane == 0) b.rs_score[item] = score;
-    if (lane == 0) atomicAdd(b.stats + 0, 1ull);
+    if (lane == 0) atomicAdd(b.stats + (list_mode ? 7 : 0), 1ull);
     __syncwarp();
   }
 }
@@ -340,7 +348,7 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
     if (e != cudaSuccess) return e;
   }
   // the FP64 kernel over the ligands with n >= min_n, on counter `ctr`
-  auto launch_exact = [&](cudaStream_t st, uint32_t min_n, unsigned int* ctr) -> cudaError_t {
+  auto launch_exact = [&](cudaStream_t st, uint32_t min_n, unsigned int* ctr, uint32_t list_mode = 0u) -> cudaError_t {
     const uint32_t stride = 7 * b.max_n;  // doubles per warp
     const size_t per_warp = size_t(stride) * sizeof(double);
     int warps = int((200 * 1024) / per_warp);
@@ -351,7 +359,7 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
     if (r != cudaSuccess) return r;
     DevBatch bx = b;
     bx.work_counter = ctr;
-    dock_exact_kernel<<<n_sms, 32 * warps, smem, st>>>(pk, pr, bx, stride, min_n);
+    dock_exact_kernel<<<n_sms, 32 * warps, smem, st>>>(pk, pr, bx, stride, min_n, list_mode);
     ++*launches;
     return cudaGetLastError();
   };
@@ -384,6 +392,8 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
         if (e != cudaSuccess) return e;
         *launches += 2;
       }
+      // the restarts the fast sweeps handed over (usually none: one short launch)
+      if ((e = launch_exact(split ? stream_b : stream, 0u, b.work_counter + 18, 1u)) != cudaSuccess) return e;
       if (b.max_n > kFastMaxAtoms) {
         // ligands beyond 128 atoms: K1a (NS = 8) for their candidates, then the FP64 kernel
         DevBatch bb = b;
