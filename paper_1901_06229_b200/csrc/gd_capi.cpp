@@ -900,32 +900,47 @@ int check_contract(gd_ctx* ctx, const gd_library* lib) {
 
 // Per-thread scratch of the packer (no heap traffic per ligand once warm).
 struct PackScratch {
-  std::vector<uint32_t> start, nbr, fill, stack, order, msize;
-  std::vector<char> seen, in_any, vis;
-  std::vector<uint16_t> pos;
+  std::vector<uint32_t> start, nbr, fill, order, tin, low, par, sz, cover, msize;
   std::vector<std::pair<uint32_t, uint32_t>> st;
 };
 
-// DFS from `from` over the CSR graph with the edge (skip_a, skip_b) removed (reachable,
-// molecule.cpp:22-41); seen[] marks the component.
-inline void dfs_mark(const PackScratch& g, uint32_t n, uint32_t from, uint32_t skip_a, uint32_t skip_b,
-                     std::vector<char>& seen, std::vector<uint32_t>& stack) {
-  seen.assign(n, 0);
-  stack.clear();
-  stack.push_back(from);
-  seen[from] = 1;
-  while (!stack.empty()) {
-    const uint32_t u = stack.back();
-    stack.pop_back();
-    for (uint32_t e = g.start[u]; e < g.start[u + 1]; ++e) {
-      const uint32_t w = g.nbr[e];
-      if ((u == skip_a && w == skip_b) || (u == skip_b && w == skip_a)) continue;
-      if (!seen[w]) {
-        seen[w] = 1;
-        stack.push_back(w);
-      }
+// Iterative DFS from `root` over the CSR graph, neighbours in CSR order: preorder (order, tin),
+// parent, subtree size and low-link (lowest preorder index reachable from the subtree by one
+// non-parent edge; every edge to the parent is skipped, so parallel bonds count as one edge, as
+// in reachable(), molecule.cpp:22-41, which drops all (i, j) edges). Returns the atoms visited.
+inline uint32_t dfs_tree(PackScratch& g, uint32_t n, uint32_t root) {
+  constexpr uint32_t NONE = ~0u;
+  g.tin.assign(n, NONE);
+  g.low.resize(n);
+  g.par.resize(n);
+  g.sz.resize(n);
+  g.order.clear();
+  g.st.clear();
+  g.tin[root] = g.low[root] = 0;
+  g.par[root] = NONE;
+  g.order.push_back(root);
+  g.st.push_back({root, g.start[root]});
+  while (!g.st.empty()) {
+    auto& top = g.st.back();
+    const uint32_t u = top.first;
+    if (top.second == g.start[u + 1]) {
+      g.st.pop_back();
+      g.sz[u] = uint32_t(g.order.size()) - g.tin[u];
+      if (g.par[u] != NONE) g.low[g.par[u]] = std::min(g.low[g.par[u]], g.low[u]);
+      continue;
+    }
+    const uint32_t w = g.nbr[top.second++];
+    if (w == g.par[u]) continue;
+    if (g.tin[w] == NONE) {
+      g.par[w] = u;
+      g.tin[w] = g.low[w] = uint32_t(g.order.size());
+      g.order.push_back(w);
+      g.st.push_back({w, g.start[w]});
+    } else {
+      g.low[u] = std::min(g.low[u], g.tin[w]);
     }
   }
+  return uint32_t(g.order.size());
 }
 
 // Host SoA packing of a (rebased, atom_off[0] == 0) library into H[0, host_bytes), fused with
@@ -990,9 +1005,13 @@ int64_t pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, 
       g.nbr[g.fill[x]++] = z;
       g.nbr[g.fill[z]++] = x;
     }
-    dfs_mark(g, n, 0, ~0u, ~0u, g.seen, g.stack);
-    for (uint32_t a = 0; a < n; ++a)
-      if (!g.seen[a]) return bad();  // bond graph is not connected
+    // One DFS from atom 0 (preorder, subtree sizes, low-links) answers every graph question of
+    // validate_ligand / finalize_ligand: connectivity (molecule.cpp:214-222), and per rotamer the
+    // ring check and the moving set (molecule.cpp:88-98). The component of atom_j with the (i, j)
+    // bonds removed excludes atom_i iff (i, j) is a bridge, i.e. a tree edge (p, c) with
+    // low[c] > tin[p]; it is then subtree(j) when j is the child, else everything but subtree(i),
+    // a range (or the complement of one) of preorder positions.
+    if (dfs_tree(g, n, 0) != n) return bad();  // bond graph is not connected
     LigMeta m{};
     m.atom_base = lib->atom_off[l] - a0;
     m.rot_base = lib->rot_off[l] - r0;
@@ -1000,27 +1019,34 @@ int64_t pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, 
     m.adj_base = y.adj_base[l];
     m.n = uint16_t(n);
     m.nr = uint16_t(v.nr);
-    // moving sets (finalize_ligand, molecule.cpp:88-98) as bitmasks, from the ring-check DFS
-    g.in_any.assign(n, 0);
-    g.msize.assign(v.nr, 0);
+    g.cover.assign(n + 1, 0);  // difference array over preorder positions: in some moving set
+    g.msize.resize(v.nr);
     for (uint32_t r = 0; r < v.nr; ++r) {
       const uint32_t i = v.rots[2 * r], j = v.rots[2 * r + 1];
       if (i >= n || j >= n) return bad();
       bool bonded = false;
       for (uint32_t e = g.start[i]; e < g.start[i + 1]; ++e) bonded |= g.nbr[e] == j;
       if (!bonded) return bad();
-      dfs_mark(g, n, j, i, j, g.seen, g.stack);
-      if (g.seen[i]) return bad();  // the rotamer bond does not disconnect the graph
+      const bool j_child = g.par[j] == i;
+      const uint32_t c = j_child ? j : i, p = j_child ? i : j;
+      if (!(g.par[c] == p && g.low[c] > g.tin[p])) return bad();  // does not disconnect the graph
       rots[m.rot_base + r] = make_uint2(i, j);
       dih0[m.rot_base + r] = lib->dihedrals ? lib->dihedrals[lib->rot_off[l] + r] : 0.0;
       uint32_t* mk = masks + m.mask_base + r * W;
       std::fill(mk, mk + W, 0u);
-      for (uint32_t a = 0; a < n; ++a)
-        if (g.seen[a]) {
-          mk[a >> 5] |= 1u << (a & 31);
-          g.in_any[a] = 1;
-          ++g.msize[r];
-        }
+      const uint32_t s0 = g.tin[c], e0 = s0 + g.sz[c];
+      auto mark = [&](uint32_t q0, uint32_t q1) {
+        for (uint32_t q = q0; q < q1; ++q) mk[g.order[q] >> 5] |= 1u << (g.order[q] & 31);
+        g.cover[q0]++;
+        g.cover[q1]--;
+      };
+      if (j_child) {
+        mark(s0, e0);
+      } else {
+        mark(0, s0);
+        mark(e0, n);
+      }
+      g.msize[r] = j_child ? g.sz[c] : n - g.sz[c];
     }
     meta[l] = m;
     for (uint32_t a = 0; a < n; ++a) {
@@ -1035,49 +1061,29 @@ int64_t pack_library(const gd_ctx* ctx, const gd_library* lib, const Layout& y, 
       adj_l[z * W + (x >> 5)] |= 1u << (x & 31);
     }
     // DFS preorder from an atom outside every moving set: each moving set (the component of atom_j
-    // behind the bridge (i,j)) is then entered only through j and occupies one contiguous range
-    // [pos(j), pos(j) + |M|) — the layout the fast sweep's range loops need.
+    // behind the bridge (i,j)) is then entered only through j and is exactly j's subtree, one
+    // contiguous range [pos(j), pos(j) + |M|) — the layout the fast sweep's range loops need
+    // (DESIGN.md §3.3). When atom 0 is outside every moving set (the usual case) the validation
+    // DFS above is that preorder already; else it is rerun from the first such atom.
     {
-      uint32_t root = 0;
-      while (root < n && g.in_any[root]) ++root;
-      bool ok = root < n && n <= 128;
-      if (root >= n) root = 0;
-      g.order.clear();
-      g.vis.assign(n, 0);
-      g.st.clear();
-      g.st.push_back({root, g.start[root]});
-      g.vis[root] = 1;
-      g.order.push_back(root);
-      while (!g.st.empty()) {
-        auto& top = g.st.back();
-        if (top.second == g.start[top.first + 1]) {
-          g.st.pop_back();
-          continue;
-        }
-        const uint32_t w = g.nbr[top.second++];
-        if (!g.vis[w]) {
-          g.vis[w] = 1;
-          g.order.push_back(w);
-          g.st.push_back({w, g.start[w]});
-        }
+      uint32_t root = n, run = 0;
+      for (uint32_t q = 0; q < n && root == n; ++q) {
+        run += g.cover[q];
+        if (run == 0) root = g.order[q];
       }
-      g.pos.assign(n, 0);
-      for (uint32_t p = 0; p < g.order.size(); ++p) g.pos[g.order[p]] = uint16_t(p);
-      for (uint32_t a = 0; a < n; ++a) dfs[m.atom_base + a] = g.pos[a];
+      const bool ok = root < n && n <= 128;
+      if (root < n && root != 0) dfs_tree(g, n, root);
+      uint16_t* dl = dfs + m.atom_base;
+      for (uint32_t q = 0; q < n; ++q) dl[g.order[q]] = uint16_t(q);
       for (uint32_t r = 0; r < v.nr; ++r) {
         const uint32_t i = v.rots[2 * r], j = v.rots[2 * r + 1];
-        const uint32_t s0 = g.pos[j], e0 = g.pos[j] + g.msize[r];
-        const uint32_t* mk = masks + m.mask_base + r * W;
-        for (uint32_t a = 0; a < n && ok; ++a) {
-          const bool mv = (mk[a >> 5] >> (a & 31)) & 1u;
-          ok = mv == (g.pos[a] >= s0 && g.pos[a] < e0);
-        }
-        rdfs[m.rot_base + r] = make_ushort4(uint16_t(s0), uint16_t(e0), uint16_t(g.pos[i]), 0);
+        const uint32_t s0 = dl[j];
+        rdfs[m.rot_base + r] = make_ushort4(uint16_t(s0), uint16_t(s0 + g.msize[r]), dl[i], 0);
       }
       uint32_t* ad = adjd + m.adj_base;
       std::fill(ad, ad + size_t(n) * W, 0u);
       for (uint32_t e = 0; e < v.nb; ++e) {
-        const uint32_t x = g.pos[v.bonds[2 * e]], z = g.pos[v.bonds[2 * e + 1]];
+        const uint32_t x = dl[v.bonds[2 * e]], z = dl[v.bonds[2 * e + 1]];
         ad[x * W + (z >> 5)] |= 1u << (z & 31);
         ad[z * W + (x >> 5)] |= 1u << (x & 31);
       }

@@ -150,3 +150,44 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(gd.DeviceError):
         gd.Context(0)
+
+
+def test_packer_graph_checks_match_reference_on_random_graphs(reference):
+    """gd_host_pack's one-DFS graph checks (connectivity, bonded rotamer, bridge via low-links,
+    parallel bonds counted once) give the reference validate_ligand's verdict (molecule.cpp:176-238)
+    on random trees with extra ring bonds, parallel bonds and random rotamer bonds."""
+    rng = np.random.default_rng(5)
+    pocket = gd.make_pocket(gd.PocketSpec())
+    P = ctypes.POINTER
+    seen = {True: 0, False: 0}
+    for _ in range(400):
+        n = int(rng.integers(1, 40))
+        bonds = [(int(rng.integers(0, a)), a) for a in range(1, n)]
+        for _ in range(int(rng.integers(1, 3)) if rng.random() < 0.5 else 0):
+            x, z = (int(v) for v in rng.integers(0, n, 2))
+            if x != z:
+                bonds.append((x, z))
+        if n > 1 and rng.random() < 0.15:
+            bonds.append(bonds[int(rng.integers(0, len(bonds)))])
+        rots = []
+        for _ in range(int(rng.integers(0, min(n, 8))) if n > 1 else 0):
+            i, j = bonds[int(rng.integers(0, len(bonds)))]
+            rots.append((i, j) if rng.random() < 0.5 else (j, i))
+        xyz = rng.uniform(-3, 3, (n, 3))
+        rad = np.ones(n)
+        lib = _lig(xyz, rad, bonds, rots)
+        b = np.ascontiguousarray(np.asarray(bonds, np.uint32).reshape(-1, 2))
+        ro = np.ascontiguousarray(np.asarray(rots, np.uint32).reshape(-1, 2))
+        buf = ctypes.create_string_buffer(4096)
+        nv = reference.lib.ref_validate(ctypes.c_uint32(n), xyz.ctypes.data_as(P(ctypes.c_double)),
+                                        rad.ctypes.data_as(P(ctypes.c_double)), ctypes.c_uint32(len(b)),
+                                        b.ctypes.data_as(P(ctypes.c_uint32)), ctypes.c_uint32(len(ro)),
+                                        ro.ctypes.data_as(P(ctypes.c_uint32)), buf, ctypes.c_uint32(4096))
+        try:
+            gd.host_pack_seconds(lib, pocket, threads=1)
+            ok = True
+        except gd.ValidationError:
+            ok = False
+        assert ok == (nv == 0), (bonds, rots, buf.value)
+        seen[ok] += 1
+    assert seen[True] > 50 and seen[False] > 30
