@@ -20,11 +20,9 @@ def find(pat):
     raise KeyError(pat)
 
 
-marks = [("setup/start-pose", find("dock_fast_kernel(DevPocket pk")),
-         ("align-exact", find("exact FP64 re-scoring (docking.cpp:71-91)")),
+marks = [("setup/aligned-pose", find("dock_fast_kernel(DevPocket pk")),
          ("sweep-setup+refresh", find("dihedral sweep (docking.cpp:155-167")),
          ("step-head", find("for (uint32_t rep = 0; rep < pr.reps; ++rep)")),
-         ("step-slowpath", find("slow path: every candidate exactly")),
          ("step-axis", find("coarse evaluation of every candidate k = 1")),
          ("step-pairs", find("Cross pairs (DESIGN.md §3.2). Rotating M' by theta")),
          ("step-cand-setup", find("float res_s[2] = {-1e30f, -1e30f};")),
