@@ -1319,7 +1319,6 @@ __global__ void __launch_bounds__(NT, 1)
       const float2 cq_p1 = (lane >> lg2_all) < rem_all ? __ldg(pr.dtab_f + 33 + (lane >> lg2_all)) : make_float2(1.f, 0.f);
       // full-angle (cos, sin) of the same candidates, for the algebraic cross-pair margins
       const float2 cf_p0 = make_float2(fmaf(-2.f * cq_p0.y, cq_p0.y, 1.f), 2.f * cq_p0.x * cq_p0.y);
-      const float2 cf_p1 = make_float2(fmaf(-2.f * cq_p1.y, cq_p1.y, 1.f), 2.f * cq_p1.x * cq_p1.y);
       // Per-pose caches, rebuilt after alignment and after every k != 0 commit:
       //   A[pos]     FP32 (gx, gy, gz, rho = cf*r/spacing) in DFS order,
       //   es, cs     exact FP64 and coarse per-atom samples, samb: coarse sample near a face,
@@ -1722,8 +1721,9 @@ __global__ void __launch_bounds__(NT, 1)
                 }
               }
             }
-            if (r < 32 && inv && !frag) {
+            if (r < 32 && inv && !frag) {  // warp-uniform
               if (lane == 0) CF[r] = fsum;
+              __syncwarp();  // every lane reads CF[r] at a later step
               vmask |= 1u << r;
             }
           }
@@ -1760,7 +1760,20 @@ __global__ void __launch_bounds__(NT, 1)
             break;
           } else if (!(skip_inv && inv)) {
             GD_T(5);
-            // ---------------- coarse evaluation of every candidate k = 1 .. S-1 (faithful sweep)
+            float res_s[2] = {-1e30f, -1e30f};
+            uint32_t res_st[2] = {0u, 0u};
+            // ---------------- coarse evaluation of every candidate k = 1 .. S-1 (faithful sweep).
+            // With M' empty (atom_j a leaf: half the steps of the generated libraries) every
+            // candidate is the current pose: no moved atom, no sample, no cross pair, and the
+            // decision below needs none of the candidates' values.
+            if (e0 > s0 + 1) {
+            // pass-1 lanes per candidate: at most the moved atoms (no idle lanes to reduce over);
+            // the candidates' half-angles move to that lane layout by one shuffle
+            const uint32_t nm_s = e0 - s0 - 1;
+            const uint32_t sh1 = min(lg2_all, nm_s <= 1 ? 0u : 32u - __clz(nm_s - 1u));
+            const float2 cq1 = make_float2(__shfl_sync(FULL, cq_p1.x, min((lane >> sh1) << lg2_all, 31u)),
+                                           __shfl_sync(FULL, cq_p1.y, min((lane >> sh1) << lg2_all, 31u)));
+            const float2 cf1 = make_float2(fmaf(-2.f * cq1.y, cq1.y, 1.f), 2.f * cq1.x * cq1.y);
             const float4 fpi = A[ipos];
             const float4 fpj = A[s0];
             float ax = fpj.x - fpi.x, ay = fpj.y - fpi.y, az = fpj.z - fpi.z;
@@ -1809,7 +1822,7 @@ __global__ void __launch_bounds__(NT, 1)
               // |alpha|, |beta|, |gamma| <= 10 D^2 (D = largest distance from pi): FP32 rounding of
               // the terms and of the fold, the FP32 (cos, sin) and the non-unit FP32 axis, <= 8e-6 D^2
               tau_a = tau + 8e-6f * warp_max(d2);
-              const uint32_t sub1 = lane & ((1u << lg2_all) - 1u), gs1 = 1u << lg2_all;
+              const uint32_t sub1 = lane & ((1u << sh1) - 1u), gs1 = 1u << sh1;
               uint32_t cnt = 0;
               auto fold = [&]() {
                 __syncwarp();
@@ -1819,7 +1832,7 @@ __global__ void __launch_bounds__(NT, 1)
                 }
                 for (uint32_t e = sub1; e < cnt; e += gs1) {
                   const float4 pe = PL[e];
-                  mmin1 = fminf(mmin1, fmaf(pe.y, cf_p1.x, fmaf(pe.z, cf_p1.y, pe.x)));
+                  mmin1 = fminf(mmin1, fmaf(pe.y, cf1.x, fmaf(pe.z, cf1.y, pe.x)));
                 }
                 __syncwarp();
                 cnt = 0;
@@ -1851,11 +1864,9 @@ __global__ void __launch_bounds__(NT, 1)
                 }
               }
             }
-            float res_s[2] = {-1e30f, -1e30f};
-            uint32_t res_st[2] = {0u, 0u};
             const uint32_t n_cand = pr.S - 1;  // k = 1 .. S-1
             const uint32_t rem = n_cand > 32 ? n_cand - 32 : 0;
-            const uint32_t lg2 = lg2_all;
+            const uint32_t lg2 = sh1;
 #pragma unroll 1
             for (int pass = 0; pass < 2; ++pass) {
               if (pass == 1 && rem == 0) break;
@@ -1869,7 +1880,7 @@ __global__ void __launch_bounds__(NT, 1)
               if (active) {
                 // moved-atom samples at this lane's angle: the rotation matrix of the half-angle
                 // quaternion (about_axis, geometry.hpp:46-50) in FP32
-                const float2 cq = pass == 0 ? cq_p0 : cq_p1;
+                const float2 cq = pass == 0 ? cq_p0 : cq1;
                 const float qw = cq.x, qx = ax * cq.y, qy = ay * cq.y, qz = az * cq.y;
                 const float xx = qx * qx, yy = qy * qy, zz = qz * qz, xy = qx * qy, xz = qx * qz, yz = qy * qz;
                 const float wx = qw * qx, wy = qw * qy, wz = qw * qz;
@@ -1911,6 +1922,7 @@ __global__ void __launch_bounds__(NT, 1)
                   res_st[1] = t2;
                 }
               }
+            }
             }
 
             GD_T(6);
