@@ -25,7 +25,7 @@ marks = [("setup/aligned-pose", find("dock_fast_kernel(DevPocket pk")),
          ("step-head", find("for (uint32_t rep = 0; rep < pr.reps; ++rep)")),
          ("step-axis", find("coarse evaluation of every candidate k = 1")),
          ("step-pairs", find("Cross pairs (DESIGN.md §3.2). Rotating M' by theta")),
-         ("step-cand-setup", find("float res_s[2] = {-1e30f, -1e30f};")),
+         ("step-cand-setup", find("const uint32_t n_cand = pr.S - 1;  // k = 1 .. S-1")),
          ("step-cand-loop", find("for (uint32_t mq = s0 + 1 + sub; mq < e0; mq += gs) {")),
          ("step-cand-reduce", find("for (uint32_t o = 1; o < gs; o <<= 1) {  // group reduction")),
          ("step-decisions", find("exact decisions (reference semantics")),
