@@ -329,9 +329,10 @@ def run_ours(args):
         w_align = params.n_restarts * int(np.prod(params.rotation_steps)) * lspec["atoms"] * total
         ops_a = w_align * (15 + 21 * f_in)
         ops_b = st["sweep_samples"] * (15 + 21 * f_in) + 7 * st["cross_pairs"]
-        a = ops_a / (k1a_ms / 1e3) / 1e12 / world
-        b = ops_b / (k1b_ms / 1e3) / 1e12 / world if k1b_ms > 0 else 0.0
-        pth = (ops_a + ops_b) / ((k1a_ms + k1b_ms) / 1e3) / 1e12 / world
+        gpus = min(world, n_dev)  # per-GPU rate (ranks sharing one GPU in the gloo tests share its peak)
+        a = ops_a / (k1a_ms / 1e3) / 1e12 / gpus
+        b = ops_b / (k1b_ms / 1e3) / 1e12 / gpus if k1b_ms > 0 else 0.0
+        pth = (ops_a + ops_b) / ((k1a_ms + k1b_ms) / 1e3) / 1e12 / gpus
         return dict(peak=peak, peak_nominal=peak_nominal, ops_a=ops_a, ops_b=ops_b, a=a, b=b, path=pth)
 
     # ---- headline: the configured regime
