@@ -412,7 +412,7 @@ int upload_grid_f(gd_ctx* ctx) {
     const uint32_t nq = na / 4;
     std::vector<uint32_t> units;
     for (uint32_t k = 0; k < st[2]; ++k)
-      for (uint32_t c0 = 0; c0 < std::max<uint32_t>(nq, 1); c0 += 2)
+      for (uint32_t c0 = 0; c0 < std::max<uint32_t>(nq, 1); c0 += gdk::k1a_qt_groups())
         for (uint32_t j = 0; j < st[1]; ++j) {
           const uint32_t f = j * st[2] + k;
           if (std::find(kept.begin(), kept.end(), f) != kept.end()) units.push_back(f | (c0 << 16));
@@ -435,7 +435,7 @@ int upload_grid_f(gd_ctx* ctx) {
       if (env[0] == '1') {
         units.clear();
         for (uint32_t f = 0; f < nf; ++f)
-          for (uint32_t c0 = 0; c0 < std::max<uint32_t>(nq, 1); c0 += 2) units.push_back(f | (c0 << 16));
+          for (uint32_t c0 = 0; c0 < std::max<uint32_t>(nq, 1); c0 += gdk::k1a_qt_groups()) units.push_back(f | (c0 << 16));
         tab.assign(nf + units.size(), 0u);
         for (uint32_t i = 0; i < units.size(); ++i) tab[nf + i] = units[i];
       }

@@ -64,6 +64,9 @@ constexpr uint32_t kSweepCtr = 10;
 #ifndef GD_K1A_X2
 #define GD_K1A_X2 1  // K1a samples in f32x2 pairs (bit-identical to the scalar form)
 #endif
+#ifndef GD_K1A_TMA_STAGE
+#define GD_K1A_TMA_STAGE 0  // K1a's cells by TMA bulk copy (measured 1.5 % slower overall than the LDG loop)
+#endif
 #ifndef GD_QT_GROUPS
 #define GD_QT_GROUPS 2
 #endif
@@ -200,6 +203,43 @@ __device__ __forceinline__ void coarse_sample_iv(const CoarseGrid& cg, float gx,
                                 fminf(fmaxf(gz, 0.f), 2.f * cg.hz - 1e-3f), am);
   hi += v;
   if (e < -ptol) lo += v;
+}
+
+// ------------------------------------------------------------------ TMA staging
+// Copy `bytes` from global to this CTA's shared memory with TMA bulk copies (cp.async.bulk,
+// completion counted on an mbarrier): thread 0 arms the barrier with the byte count and issues the
+// copies, every thread waits on the barrier's phase. Used for the once-per-CTA staging of the
+// pocket cells and the FP64 field. Addresses or sizes that are not 16-byte multiples (an odd-size
+// field) take a cooperative copy instead. Ends with a CTA barrier (the next call re-arms it).
+__device__ __forceinline__ void stage_to_smem(void* dst, const void* src, uint32_t bytes) {
+  __shared__ alignas(8) unsigned long long stage_bar;
+  const uint32_t d = uint32_t(__cvta_generic_to_shared(dst));
+  const uint32_t bar = uint32_t(__cvta_generic_to_shared(&stage_bar));
+  const bool tma = bytes > 0 && bytes < (1u << 20) && ((d | uint32_t(reinterpret_cast<uintptr_t>(src)) | bytes) & 15u) == 0;
+  if (tma) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      for (uint32_t off = 0; off < bytes; off += 65536u) {
+        const uint32_t n = min(65536u, bytes - off);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(d + off), "l"(reinterpret_cast<const char*>(src) + off), "r"(n), "r"(bar)
+                     : "memory");
+      }
+    }
+    __syncthreads();  // the barrier is initialised before anyone polls it
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}"
+        ::"r"(bar) : "memory");
+    __syncthreads();  // every thread has seen the phase complete before the barrier is re-armed
+    if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+  } else {
+    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+    for (uint32_t i = threadIdx.x; i < bytes / 4u; i += blockDim.x) d32[i] = __ldg(s32 + i);
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ FP64 register pose helpers
@@ -480,8 +520,12 @@ __global__ void __launch_bounds__(NT, 1)
   const uint4* cells = SC ? sc : pk.cells;
   float* slots = SC ? reinterpret_cast<float*>(sc + n_cells + 1) : reinterpret_cast<float*>(smem_raw);
   if (SC) {
+#if GD_K1A_TMA_STAGE
+    stage_to_smem(sc, pk.cells, (n_cells + 1) * uint32_t(sizeof(uint4)));
+#else
     for (uint32_t i = threadIdx.x; i <= n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
     __syncthreads();
+#endif
   }
   float4* A = reinterpret_cast<float4*>(slots + size_t(warp) * slot_floats);
   const CoarseGrid cg{cells,
@@ -637,7 +681,7 @@ __global__ void __launch_bounds__(NT, 1)
     // quarter-turn units (see the loop below): (kept frame, c0) in upload_grid_f's order
     const bool qt = separable && pr.steps[0] % (4 * kQtGroups) == 0;
     const uint32_t nq = pr.steps[0] / 4;
-    static_assert(kQtGroups == 2, "upload_grid_f builds K1a's work units for two quarter-turn groups");
+    static_assert(kQtGroups == 2 || kQtGroups == 4, "64-bit ambiguity masks: 4 kQtGroups bits per unit");
     const uint32_t n_units = qt ? pr.n_kept : 0u;
     const uint32_t n_full = n_units & ~31u, n_rem = n_units - n_full;
     const uint32_t gsz = n_rem <= 1u ? 32u : 32u >> (32 - __clz(n_rem - 1u));  // lanes per shared unit
@@ -646,10 +690,10 @@ __global__ void __launch_bounds__(NT, 1)
     const bool twins = qt && pr.n_twin_frames > 0;
     auto unit_of = [&](uint32_t mu) -> uint32_t { return mu * 32u >= n_full ? n_full + (lane >> lgsz) : lane + 32u * mu; };
     auto amb_to_g = [&](uint32_t bit) -> uint32_t {
-      if (qt) {  // bit = 8 mu + 4 gi + q of the lane's unit mu
-        const uint32_t u = unit_of(bit >> 3);
+      if (qt) {  // bit = 4 kQtGroups mu + 4 gi + q of the lane's unit mu
+        const uint32_t u = unit_of(bit / (4u * kQtGroups));
         const uint32_t ue = __ldg(pr.frame_tab + n_frames + u);
-        return ((ue >> 16) + ((bit >> 2) & 1u) + (bit & 3u) * nq) * n_frames + (ue & 0xffffu);
+        return ((ue >> 16) + ((bit >> 2) & (kQtGroups - 1u)) + (bit & 3u) * nq) * n_frames + (ue & 0xffffu);
       }
       return separable ? (bit & 15u) * n_frames + lane + 32u * (bit >> 4) : lane + 32u * bit;
     };
@@ -844,7 +888,7 @@ __global__ void __launch_bounds__(NT, 1)
                   const uint32_t ia = c0 + gi + q * nq;
                   const float sc = (acc[4 * gi + q] - bsum) * inv_n_scale;
                   if (amn[4 * gi + q] <= ptol) {
-                    amb_mask |= 1ull << (8u * mu + 4u * gi + q);
+                    amb_mask |= 1ull << (4u * kQtGroups * mu + 4u * gi + q);
                   } else {
                     insert(sc, ia * n_frames + f);
                     lkey = fmaxf(lkey, sc);
@@ -1015,7 +1059,7 @@ __global__ void __launch_bounds__(NT, 1)
   if (field_in_smem) {
     double* sf = slots + size_t(blockDim.x >> 5) * slot_doubles;
     const uint32_t nv = pk.dims[0] * pk.dims[1] * pk.dims[2];
-    for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) sf[v] = pk_in.field[v];
+    stage_to_smem(sf, pk_in.field, nv * uint32_t(sizeof(double)));
     if (threadIdx.x == 0) pk.field = sf;
     __syncthreads();
   }
@@ -1180,16 +1224,13 @@ __global__ void __launch_bounds__(NT, 1)
   uint4* sc = reinterpret_cast<uint4*>(smem_raw);
   const uint4* cells = SC ? sc : pk.cells;
   float* slots = SC ? reinterpret_cast<float*>(sc + n_cells + 1) : reinterpret_cast<float*>(smem_raw);
-  if (SC) {
-    for (uint32_t i = threadIdx.x; i <= n_cells; i += blockDim.x) sc[i] = __ldg(pk.cells + i);
-    __syncthreads();
-  }
+  if (SC) stage_to_smem(sc, pk.cells, (n_cells + 1) * uint32_t(sizeof(uint4)));
   if (field_in_smem) {
     // the FP64 field (exact samples of the refinement, refresh and exact decisions) behind the
     // warp slots: shared-memory latency instead of L2 for every exact sample
     double* sf = reinterpret_cast<double*>(slots + size_t(blockDim.x >> 5) * slot_floats);
     const uint32_t nv = pk.dims[0] * pk.dims[1] * pk.dims[2];
-    for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) sf[v] = pk_in.field[v];
+    stage_to_smem(sf, pk_in.field, nv * uint32_t(sizeof(double)));
     if (threadIdx.x == 0) pk.field = sf;
     __syncthreads();
   }
@@ -2201,5 +2242,7 @@ cudaError_t launch_align_big(const DevPocket& pk, const DevParams& pr, const Dev
              : launch_persistent(align_coarse_kernel<8, GD_ALIGN_THREADS_L1, false>, pg, n_sms, stream, pk, pr, b,
                                  slot_a);
 }
+
+uint32_t k1a_qt_groups() { return uint32_t(kQtGroups); }
 
 }  // namespace gdk

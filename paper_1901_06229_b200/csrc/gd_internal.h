@@ -128,6 +128,9 @@ struct DevBatch {
 // `mid` — the executor keeps the alignment of chunk c+1 and the sweep of chunk c in flight together.
 // cub temp bytes of the item-order sort for n items
 size_t order_tmp_bytes(uint32_t n);
+// quarter-turn groups of one K1a work unit (the unit table's c0 step, upload_grid_f; gd_fast.cu)
+uint32_t k1a_qt_groups();
+
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                         cudaStream_t stream, int* launches, cudaEvent_t* ev = nullptr,
                         cudaStream_t stream_b = nullptr, cudaEvent_t mid = nullptr);
