@@ -209,6 +209,9 @@ std::pair<std::vector<DockResult>, RunMetrics> run_screening(const std::vector<L
   metrics.worker_wait_seconds.assign(n_dev, 0.0);
   std::vector<std::array<double, 4>> times(n_dev, std::array<double, 4>{0, 0, 0, 0});
   std::vector<std::exception_ptr> errors(n_dev);
+  // every lane's context exists before any docks (each sizes its host pool by the live contexts)
+  for (unsigned d = 0; d < n_dev && d < unsigned(n_cuda); ++d)
+    if (library.size() * d / n_dev < library.size() * (d + 1) / n_dev) device(int(d));
   const auto t0 = std::chrono::steady_clock::now();
   {
     std::vector<std::thread> threads;

@@ -869,6 +869,11 @@ def run_screening(library: Library, pocket: Pocket, params: DockParams = DockPar
     parts, errors = [None] * len(devs), [None] * len(devs)
     times = [{"busy": 0.0, "align": 0.0, "optimize": 0.0, "host_wait": 0.0} for _ in devs]
 
+    # every lane's context exists before any docks: each sizes its host pool by the live contexts
+    for i, d in enumerate(devs):
+        if bounds[i + 1] > bounds[i]:
+            _ctx_for(d)
+
     def work(i):
         try:
             shard = library.slice(bounds[i], bounds[i + 1])

@@ -40,10 +40,12 @@ constexpr int kSlots = 3;
 // Host worker pool for the executor's per-chunk validation, packing and unpacking: persistent
 // threads (the caller works too), so a chunk's host work does not pay thread start-up on the
 // critical path. One pool per context (a context is externally synchronized, so one job runs at a
-// time); its width is the host's share of this GPU: GD_HOST_THREADS if set, else the hardware
-// threads divided by max(visible GPUs, LOCAL_WORLD_SIZE) — one context per GPU, whether the GPUs
-// are driven by threads of one process (run_screening) or by one process each (torchrun), share
-// the cores instead of oversubscribing them.
+// time), created at the context's first batch; its width is the host's share of this context:
+// GD_HOST_THREADS if set, else the hardware threads divided by max(live contexts of this process,
+// LOCAL_WORLD_SIZE) — one context per GPU, whether the GPUs are driven by threads of one process
+// (run_screening creates every lane's context before docking) or by one process each (torchrun),
+// share the cores instead of oversubscribing them, and a lone context on a multi-GPU node gets
+// all of them.
 class HostPool {
  public:
   explicit HostPool(unsigned threads) {
@@ -83,15 +85,13 @@ class HostPool {
       if (v > 0) return unsigned(v);
     }
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    int devs = 1;
-    if (cudaGetDeviceCount(&devs) != cudaSuccess || devs < 1) {
-      cudaGetLastError();
-      devs = 1;
-    }
-    unsigned share = unsigned(devs);
+    unsigned share = std::max(1, live_contexts.load());
     if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) share = std::max(share, unsigned(std::max(1, std::atoi(e))));
     return std::max(1u, hw / share);
   }
+  // contexts alive in this process (gd_create / gd_destroy): the contexts of one process share the
+  // host cores, and the ranks of one node (LOCAL_WORLD_SIZE) share them between processes
+  static inline std::atomic<int> live_contexts{0};
 
  private:
   void work() {
@@ -561,6 +561,7 @@ int gd_create(int device, gd_ctx** out) {
   if (!out) return GD_ERR_ARGUMENT;
   *out = nullptr;
   auto* ctx = new gd_ctx();
+  HostPool::live_contexts.fetch_add(1);
   ctx->device = device;
   ctx->params = gd_default_params();
   cudaError_t e = cudaSetDevice(device);
@@ -592,6 +593,7 @@ int gd_create(int device, gd_ctx** out) {
 
 void gd_destroy(gd_ctx* ctx) {
   if (!ctx) return;
+  HostPool::live_contexts.fetch_sub(1);
   cudaSetDevice(ctx->device);
   cudaFree(ctx->d_field);
   cudaFree(ctx->d_cells);

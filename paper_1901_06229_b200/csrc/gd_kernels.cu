@@ -390,7 +390,7 @@ cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch
         e = launch_fast(pk, pr, bf, n_sms, stream, split ? mid : (ev && last ? ev[1] : nullptr),
                         split ? stream_b : nullptr);
         if (e != cudaSuccess) return e;
-        *launches += 2;
+        *launches += 3;  // K1a, K1r, K1b
       }
       // the restarts the fast sweeps handed over (usually none: one short launch)
       if ((e = launch_exact(split ? stream_b : stream, 0u, b.work_counter + 18, 1u)) != cudaSuccess) return e;
