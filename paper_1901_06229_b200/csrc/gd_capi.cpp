@@ -140,6 +140,9 @@ struct gd_ctx {
   double spacing = 1.0;
   double* d_field = nullptr;
   uint4* d_cells = nullptr;
+  float* d_field_f = nullptr;  // FP32 field + zero tail (K1b's coarse samples)
+  uint32_t f_count = 0;
+  float q_eps_f = 0.f;
   float q_eps = 0.f;
   float max_step = 0.f;
   float dz_bias = 3.f;
@@ -495,6 +498,10 @@ DevPocket dev_pocket(const gd_ctx* ctx) {
   pk.max_step = ctx->max_step;
   pk.coarse_scale = 1.0f;
   pk.dz_bias = ctx->dz_bias;
+  pk.field_f = ctx->d_field_f;
+  pk.f_dummy = ctx->dims[0] * ctx->dims[1] * ctx->dims[2];
+  pk.f_count = ctx->f_count;
+  pk.q_eps_f = ctx->q_eps_f;
   return pk;
 }
 
@@ -597,6 +604,7 @@ void gd_destroy(gd_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaFree(ctx->d_field);
   cudaFree(ctx->d_cells);
+  cudaFree(ctx->d_field_f);
   cudaFree(ctx->d_grid);
   cudaFree(ctx->d_grid_f);
   cudaFree(ctx->d_frames);
@@ -755,6 +763,22 @@ int gd_set_pocket(gd_ctx* ctx, const uint32_t dims[3], const double origin[3], d
   ctx->dz_bias = wide ? 6.0f : 3.0f;
   bool in_range = true;
   for (size_t i = 0; i < nv; ++i) in_range &= (field[i] >= 0.0 && field[i] <= 1.0);
+  {  // K1b's FP32 field: the clamped values, then zeros for the 8 corners of a sample outside
+    const size_t tail = size_t(dims[0]) * dims[1] + dims[0] + 2;
+    std::vector<float> ff((nv + tail + 3) & ~size_t(3), 0.f);
+    double qf = 0.0;
+    for (size_t i = 0; i < nv; ++i) {
+      const double v = clamp01(field[i]);
+      ff[i] = float(v);
+      qf = std::max(qf, std::fabs(double(ff[i]) - v));
+    }
+    cudaFree(ctx->d_field_f);
+    ctx->d_field_f = nullptr;
+    GD_CUDA(ctx, cudaMalloc(&ctx->d_field_f, ff.size() * sizeof(float)));
+    GD_CUDA(ctx, cudaMemcpy(ctx->d_field_f, ff.data(), ff.size() * sizeof(float), cudaMemcpyHostToDevice));
+    ctx->f_count = uint32_t(ff.size());
+    ctx->q_eps_f = float(qf * (1.0 + 1e-6) + 1e-12);
+  }
   GD_CUDA(ctx, cudaMalloc(&ctx->d_cells, cells.size() * sizeof(uint4)));
   GD_CUDA(ctx, cudaMemcpy(ctx->d_cells, cells.data(), cells.size() * sizeof(uint4), cudaMemcpyHostToDevice));
   // Coarse error model: quantisation q_err per sample (each face's decoded form

@@ -64,6 +64,9 @@ constexpr uint32_t kSweepCtr = 10;
 #ifndef GD_K1A_X2
 #define GD_K1A_X2 1  // K1a samples in f32x2 pairs (bit-identical to the scalar form)
 #endif
+#ifndef GD_K1B_FIELDF
+#define GD_K1B_FIELDF 1  // K1b's coarse samples from an FP32 field copy in shared memory
+#endif
 #ifndef GD_K1A_TMA_STAGE
 #define GD_K1A_TMA_STAGE 0  // K1a's cells by TMA bulk copy (measured 1.5 % slower overall than the LDG loop)
 #endif
@@ -203,6 +206,51 @@ __device__ __forceinline__ void coarse_sample_iv(const CoarseGrid& cg, float gx,
                                 fminf(fmaxf(gz, 0.f), 2.f * cg.hz - 1e-3f), am);
   hi += v;
   if (e < -ptol) lo += v;
+}
+
+// ------------------------------------------------------------------ K1b's FP32 field (GD_K1B_FIELDF)
+// The coarse samples of the sweep straight from an FP32 copy of the field (8 corners, 7 lerps): no
+// quantisation beyond the FP32 rounding of the values (q_eps_f), staged in shared memory when it
+// fits (55 KB for 24^3) so the candidates' samples do not wait on L2 (the quantised cells, 195 KB,
+// do not fit beside the warps' slots). A sample outside the grid reads the zero tail at `dummy`.
+struct CoarseGridF {
+  const float* f;       // shared (SC: a shared-window address in `base`) or global
+  uint32_t base;        // SC: shared address of f
+  float hx, hy, hz;     // half extents (dims-1)/2
+  uint32_t nx, nxy;     // nodes per row / per plane
+  uint32_t koff;        // 0x4B000000 * (1 + nx + nxy)
+  uint32_t dummy;       // first float of the zero tail
+};
+
+template <bool SC>
+__device__ __forceinline__ float load_f(const CoarseGridF& cg, uint32_t i) {
+  if (SC) {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(cg.base + 4u * i));
+    return v;
+  }
+  return __ldg(cg.f + i);
+}
+
+template <bool SC>
+__device__ __forceinline__ float sample_f(const CoarseGridF& cg, float gx, float gy, float gz, float& amin,
+                                          float& emin) {
+  const float e = fmaxf(fabsf(gx - cg.hx) - cg.hx, fmaxf(fabsf(gy - cg.hy) - cg.hy, fabsf(gz - cg.hz) - cg.hz));
+  emin = fminf(emin, e);
+  amin = fminf(amin, fabsf(e));
+  const float rx = __fadd_rz(gx, kMagic), ry = __fadd_rz(gy, kMagic), rz = __fadd_rz(gz, kMagic);
+  const float fx = gx - (rx - kMagic), fy = gy - (ry - kMagic), fz = gz - (rz - kMagic);
+  const uint32_t idx = __float_as_uint(rx) + __float_as_uint(ry) * cg.nx + __float_as_uint(rz) * cg.nxy - cg.koff;
+  const uint32_t i = e < 0.0f ? idx : cg.dummy;
+  const float c000 = load_f<SC>(cg, i), c100 = load_f<SC>(cg, i + 1), c010 = load_f<SC>(cg, i + cg.nx),
+              c110 = load_f<SC>(cg, i + cg.nx + 1);
+  const uint32_t j = i + cg.nxy;
+  const float c001 = load_f<SC>(cg, j), c101 = load_f<SC>(cg, j + 1), c011 = load_f<SC>(cg, j + cg.nx),
+              c111 = load_f<SC>(cg, j + cg.nx + 1);
+  const float x00 = fmaf(fx, c100 - c000, c000), x10 = fmaf(fx, c110 - c010, c010);
+  const float x01 = fmaf(fx, c101 - c001, c001), x11 = fmaf(fx, c111 - c011, c011);
+  const float y0 = fmaf(fy, x10 - x00, x00), y1 = fmaf(fy, x11 - x01, x01);
+  return fmaf(fz, y1 - y0, y0);
 }
 
 // ------------------------------------------------------------------ TMA staging
@@ -1221,6 +1269,25 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t n_cells = pk.cell_dims[0] * pk.cell_dims[1] * pk.cell_dims[2];
   // SC: the pocket cells are staged once per CTA into shared memory (every warp of every work item
   // reads them; a compile-time flag so the gather is an LDS.128, not a generic load)
+#if GD_K1B_FIELDF
+  // SC: the FP32 field (+ zero tail) behind the warp slots; the FP64 field after it when it fits
+  const uint4* cells = pk.cells;
+  float* slots = reinterpret_cast<float*>(smem_raw);
+  float* sff = slots + size_t(blockDim.x >> 5) * slot_floats;
+  if (SC) stage_to_smem(sff, pk.field_f, pk.f_count * uint32_t(sizeof(float)));
+  const CoarseGridF cgf{SC ? sff : pk.field_f,
+                        SC ? uint32_t(__cvta_generic_to_shared(sff)) : 0u,
+                        0.5f * float(pk.cell_dims[0]),
+                        0.5f * float(pk.cell_dims[1]),
+                        0.5f * float(pk.cell_dims[2]),
+                        pk.dims[0],
+                        pk.dims[0] * pk.dims[1],
+                        0x4B000000u * (1u + pk.dims[0] + pk.dims[0] * pk.dims[1]),
+                        pk.f_dummy};
+  if (field_in_smem) {
+    double* sf = reinterpret_cast<double*>(sff + (SC ? ((pk.f_count + 3u) & ~3u) : 0u));
+    const uint32_t nv = pk.dims[0] * pk.dims[1] * pk.dims[2];
+#else
   uint4* sc = reinterpret_cast<uint4*>(smem_raw);
   const uint4* cells = SC ? sc : pk.cells;
   float* slots = SC ? reinterpret_cast<float*>(sc + n_cells + 1) : reinterpret_cast<float*>(smem_raw);
@@ -1230,6 +1297,7 @@ __global__ void __launch_bounds__(NT, 1)
     // warp slots: shared-memory latency instead of L2 for every exact sample
     double* sf = reinterpret_cast<double*>(slots + size_t(blockDim.x >> 5) * slot_floats);
     const uint32_t nv = pk.dims[0] * pk.dims[1] * pk.dims[2];
+#endif
     stage_to_smem(sf, pk_in.field, nv * uint32_t(sizeof(double)));
     if (threadIdx.x == 0) pk.field = sf;
     __syncthreads();
@@ -1323,7 +1391,11 @@ __global__ void __launch_bounds__(NT, 1)
     const float ext_g = b.rs_ext[item] * pk.inv_spacing_f;
     const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
     const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
+#if GD_K1B_FIELDF
+    const float eps_s = pk.q_eps_f + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
+#else
     const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
+#endif
     const float inv_n_scale = pk.coarse_scale / float(n);
     double score = b.rs_align_score[item];
     // restarts this kernel does not decide go to the FP64 kernel, which repeats them in the
@@ -1405,7 +1477,12 @@ __global__ void __launch_bounds__(NT, 1)
             const float gz = float(__dmul_rn(__dsub_rn(pa.z, pk.origin[2]), pk.inv_spacing));
             A[pick<NS>(pos, s)] = make_float4(gx, gy, gz, pick<NS>(rho, s));
             float am = 1e30f;
+#if GD_K1B_FIELDF
+            float em_ = 1e30f;
+            put<NS>(cs, s, sample_f<SC>(cgf, gx, gy, gz, am, em_));
+#else
             put<NS>(cs, s, coarse_sample(cg, gx, gy, gz, am));
+#endif
             put<NS>(samb, s, am <= ptol);
           }
         }
@@ -1937,7 +2014,11 @@ __global__ void __launch_bounds__(NT, 1)
                   const float gx = fmaf(m00, pm.x, fmaf(m01, pm.y, fmaf(m02, pm.z, tvx)));
                   const float gy = fmaf(m10, pm.x, fmaf(m11, pm.y, fmaf(m12, pm.z, tvy)));
                   const float gz = fmaf(m20, pm.x, fmaf(m21, pm.y, fmaf(m22, pm.z, tvz)));
+#if GD_K1B_FIELDF
+                  part += sample_f<SC>(cgf, gx, gy, gz, amin, emin);
+#else
                   part += coarse_sample_e(cg, gx, gy, gz, amin, emin);
+#endif
                 }
               }
               for (uint32_t o = 1; o < gs; o <<= 1) {  // group reduction (pass 2)
@@ -2203,7 +2284,21 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   constexpr size_t kK1bStatic = 2048;  // the kernel's __shared__ DevPocket + per-warp counters, rounded up
+#if GD_K1B_FIELDF
+  SmemPlan pb{};
+  {  // the warps' slots, then the FP32 field if it fits beside NTB / 32 of them (SC)
+    int dv = 0, oi = 0;
+    cudaGetDevice(&dv);
+    cudaDeviceGetAttribute(&oi, cudaDevAttrMaxSharedMemoryPerBlockOptin, dv);
+    const size_t avail = size_t(oi) - kK1bStatic, slot_bytes = slot_b * sizeof(float);
+    const size_t ff_bytes = size_t((pk.f_count + 3u) & ~3u) * sizeof(float);
+    pb.warps = int(std::min<size_t>(NTB / 32, avail / slot_bytes));
+    pb.cells_in_smem = size_t(pb.warps) * slot_bytes + ff_bytes <= avail;
+    pb.smem = size_t(pb.warps) * slot_bytes + (pb.cells_in_smem ? ff_bytes : 0);
+  }
+#else
   SmemPlan pb = plan_smem(pk, slot_b * sizeof(float), NTB / 32, GD_K1B_MIN_WARPS_SC, kK1bStatic);
+#endif
   if (pb.warps < 1) return cudaErrorInvalidConfiguration;
   // the FP64 field goes to shared memory too when it fits beside the slots (24^3: 110 KB)
   int dev = 0, optin = 0;

@@ -43,6 +43,9 @@ struct DevPocket {
   float coarse_scale;    // scale of the decoded coarse values (1 with the current encoding)
   float dz_bias;         // B: bias of the cells' dD field (3, or 6 for second differences beyond 1)
   float max_step;        // max |v(i+1) - v(i)| along any axis: slope bound per grid unit
+  const float* field_f;  // FP32 copy of the field (K1b's coarse samples) + a zero tail of f_tail floats
+  uint32_t f_dummy, f_count;  // first float of the zero tail (samples outside the grid), total floats
+  float q_eps_f;         // max |float(v) - v| over the field (K1b's quantisation term)
 };
 
 // Search parameters as seen by the kernels.
