@@ -1270,7 +1270,8 @@ __global__ void __launch_bounds__(NT, 1)
   // SC: the pocket cells are staged once per CTA into shared memory (every warp of every work item
   // reads them; a compile-time flag so the gather is an LDS.128, not a generic load)
 #if GD_K1B_FIELDF
-  // SC: the FP32 field (+ zero tail) behind the warp slots; the FP64 field after it when it fits
+  // SC: the FP32 field (+ zero tail) behind the warp slots, the coarse samples' source; else the
+  // quantised cells through L1/L2. The FP64 field after it when it fits.
   const uint4* cells = pk.cells;
   float* slots = reinterpret_cast<float*>(smem_raw);
   float* sff = slots + size_t(blockDim.x >> 5) * slot_floats;
@@ -1392,7 +1393,8 @@ __global__ void __launch_bounds__(NT, 1)
     const float maxdim = float(max(pk.dims[0], max(pk.dims[1], pk.dims[2])));
     const float ptol = 1.5e-5f + 5e-7f * maxdim + 6e-6f * ext_g;
 #if GD_K1B_FIELDF
-    const float eps_s = pk.q_eps_f + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
+    // coarse per-sample error bound (FP32 field in shared memory, else the quantised cells)
+    const float eps_s = (SC ? pk.q_eps_f : pk.q_eps) + 3.0f * pk.max_step * ptol;
 #else
     const float eps_s = pk.q_eps + 3.0f * pk.max_step * ptol;  // coarse per-sample error bound
 #endif
@@ -1479,7 +1481,7 @@ __global__ void __launch_bounds__(NT, 1)
             float am = 1e30f;
 #if GD_K1B_FIELDF
             float em_ = 1e30f;
-            put<NS>(cs, s, sample_f<SC>(cgf, gx, gy, gz, am, em_));
+            put<NS>(cs, s, SC ? sample_f<SC>(cgf, gx, gy, gz, am, em_) : coarse_sample(cg, gx, gy, gz, am));
 #else
             put<NS>(cs, s, coarse_sample(cg, gx, gy, gz, am));
 #endif
@@ -2015,7 +2017,8 @@ __global__ void __launch_bounds__(NT, 1)
                   const float gy = fmaf(m10, pm.x, fmaf(m11, pm.y, fmaf(m12, pm.z, tvy)));
                   const float gz = fmaf(m20, pm.x, fmaf(m21, pm.y, fmaf(m22, pm.z, tvz)));
 #if GD_K1B_FIELDF
-                  part += sample_f<SC>(cgf, gx, gy, gz, amin, emin);
+                  // (a field too large for shared memory: the quantised cells through L1/L2 are faster)
+                  part += SC ? sample_f<SC>(cgf, gx, gy, gz, amin, emin) : coarse_sample_e(cg, gx, gy, gz, amin, emin);
 #else
                   part += coarse_sample_e(cg, gx, gy, gz, amin, emin);
 #endif
