@@ -1555,13 +1555,18 @@ int gd_dock_batch(gd_ctx* ctx, const gd_library* lib, gd_results* out) {
   {
     uint32_t fixed = 0;
     if (const char* e = std::getenv("GD_CHUNK")) fixed = std::max<uint32_t>(1, uint32_t(std::atoi(e)));
-    uint32_t next = fixed ? fixed : std::min<uint32_t>(1024, std::max<uint32_t>(256, L / 16));
-    uint32_t growth = 4;
+    // growth: chunk c+1 is packed while the GPU docks chunk c, so it may be at most (host packing
+    // rate / GPU rate) times larger without the GPU waiting: ~0.7 per host thread of the pool
+    // (~5 us per C2 ligand per thread vs ~3.7 us per ligand on the GPU), 4 at most. With few
+    // threads (one rank of eight on a node) the first chunk is smaller too.
+    const unsigned hw_pool = pool_of(ctx).threads();
+    uint32_t next = fixed ? fixed : std::min<uint32_t>(1024, std::max<uint32_t>(hw_pool >= 8 ? 256 : 128, L / 16));
+    double growth = std::min(4.0, std::max(1.5, 0.7 * double(hw_pool)));
     if (const char* e = std::getenv("GD_CHUNK0")) next = std::max<uint32_t>(1, uint32_t(std::atoi(e)));
-    if (const char* e = std::getenv("GD_CHUNK_GROWTH")) growth = std::max<uint32_t>(1, uint32_t(std::atoi(e)));
+    if (const char* e = std::getenv("GD_CHUNK_GROWTH")) growth = std::max(1.0, std::atof(e));
     while (bounds.back() < L) {
       bounds.push_back(bounds.back() + std::min(next, L - bounds.back()));
-      if (!fixed) next = std::min<uint32_t>(kMaxChunk, next * growth);
+      if (!fixed) next = uint32_t(std::min<double>(kMaxChunk, std::ceil(double(next) * growth)));
     }
   }
   const uint32_t n_chunks = uint32_t(bounds.size() - 1);
