@@ -92,7 +92,7 @@ __host__ __device__ constexpr uint32_t pair_cap() { return 32u * NS + 32u; }
 #define GD_ALIGN_THREADS 384
 #endif
 #ifndef GD_ALIGN_THREADS_L1
-#define GD_ALIGN_THREADS_L1 384  // K1a when the cells do not fit shared memory (read through L1)
+#define GD_ALIGN_THREADS_L1 512  // K1a when the cells do not fit shared memory (read through L1; C5: 512 > 384, 448, 640)
 #endif
 #ifndef GD_REFINE_THREADS
 #define GD_REFINE_THREADS 512  // K1r: 16 warps x 128 registers (1024 threads spill the FP64 scorer)
@@ -2257,8 +2257,8 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   const uint32_t slot_b = 6 * npad_max + 4 * pair_cap<NS>() + 8 * npad_max + 32 + 2 * npad_max + 2 * NS * npad_max +
                           kZCap + 4 + npad_max;
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
-  // cells in shared memory: issue-bound, 16 warps x 128 registers; cells through L1 (large grids):
-  // 12 warps x 151 registers (C5 +4 %)
+  // cells in shared memory: 12 warps x 168 registers (GD_ALIGN_THREADS); cells through L1 (large
+  // grids): 16 warps x 128 (GD_ALIGN_THREADS_L1)
   const SmemPlan pg = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS_L1 / 32, 8);
   cudaError_t e =
       pa.cells_in_smem
