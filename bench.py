@@ -236,6 +236,20 @@ def topk_digest(hits):
     return h.hexdigest()[:16]
 
 
+def host_topk(score, k):
+    """Indices of the k best ligands by (score desc, index asc), as the device top-k (K3) orders
+    them: a partition picks every ligand scoring at least the k-th best, a sort orders those."""
+    n = len(score)
+    k = min(k, n)
+    if k == 0:
+        return np.zeros(0, np.int64)
+    cand = np.arange(n)
+    if k < n:
+        kth = np.partition(-score, k - 1)[k - 1]
+        cand = np.flatnonzero(-score <= kth)
+    return cand[np.lexsort((cand, -score[cand]))][:k]
+
+
 def run_ours(args):
     import torch
     import paper_1901_06229_b200 as gd
@@ -356,7 +370,7 @@ def run_ours(args):
         barrier()
         t0 = time.perf_counter()
         res = ctx.dock(lib)
-        order = np.lexsort((np.arange(count), -res.best_score))[:topk]
+        order = host_topk(res.best_score, topk)
         e2e_hits = [(float(res.best_score[i]), int(i) + first, int(res.best_restart[i])) for i in order]
         if dist is not None:
             e2e_hits = gather_topk(e2e_hits, topk, gdev)
