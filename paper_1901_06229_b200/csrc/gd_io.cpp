@@ -19,7 +19,10 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <charconv>
+#include <cfloat>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -53,9 +56,23 @@ void parallel_chunks(size_t n, F&& f) {  // f(chunk, begin, end) over ~hardware_
   for (auto& x : th) x.join();
 }
 
+// Token offsets: written once by the tokeniser's threads, so not zero-filled first (a vector's
+// resize would memset ~8 bytes per token on one thread before the parallel pass).
+struct Offsets {
+  std::unique_ptr<uint64_t[]> p;
+  size_t n = 0;
+  void resize_uninit(size_t m) {
+    p.reset(new uint64_t[m ? m : 1]);
+    n = m;
+  }
+  size_t size() const { return n; }
+  uint64_t* data() { return p.get(); }
+  uint64_t operator[](size_t i) const { return p[i]; }
+};
+
 struct Tok {
   const char* text;
-  std::vector<uint64_t> start;  // token start offsets, stream order
+  Offsets start;  // token start offsets, stream order
   size_t len;
   uint64_t end_of(size_t i) const {
     uint64_t e = start[i];
@@ -95,7 +112,42 @@ struct TokStr {
 
 // std::stod / std::stoll with the reference's acceptance rule (whole token, no ERANGE,
 // io.cpp:56-82).
+// A plain decimal [-]d+[.d*][(e|E)[+-]d+] (or [-].d+...): std::from_chars rounds it correctly, as
+// strtod does, so the value is strtod's; anything else (a '+', hex, inf/nan, ...) and any result
+// strtod would flag (overflow, underflow, subnormal) takes strtod itself.
+bool plain_decimal(const char* p, size_t n, bool& zero_digits) {
+  size_t k = 0, digits = 0;
+  zero_digits = true;
+  if (k < n && p[k] == '-') ++k;
+  for (; k < n && p[k] >= '0' && p[k] <= '9'; ++k, ++digits) zero_digits &= p[k] == '0';
+  if (k < n && p[k] == '.') {
+    ++k;
+    for (; k < n && p[k] >= '0' && p[k] <= '9'; ++k, ++digits) zero_digits &= p[k] == '0';
+  }
+  if (digits == 0) return false;
+  if (k < n && (p[k] == 'e' || p[k] == 'E')) {
+    ++k;
+    if (k < n && (p[k] == '+' || p[k] == '-')) ++k;
+    const size_t e0 = k;
+    for (; k < n && p[k] >= '0' && p[k] <= '9'; ++k) {
+    }
+    if (k == e0) return false;
+  }
+  return k == n;
+}
+
 bool to_double(const Tok& tk, size_t i, double& v) {
+  {
+    const uint64_t b = tk.start[i], e = tk.end_of(i);
+    const char* p = tk.text + b;
+    bool zero_digits = false;
+    if (plain_decimal(p, size_t(e - b), zero_digits)) {
+      const auto r = std::from_chars(p, tk.text + e, v);
+      if (r.ec == std::errc() && r.ptr == tk.text + e && std::isfinite(v) &&
+          (std::fabs(v) >= DBL_MIN || (v == 0.0 && zero_digits)))
+        return true;
+    }
+  }
   const TokStr s(tk, i);
   errno = 0;
   char* end = nullptr;
@@ -104,6 +156,18 @@ bool to_double(const Tok& tk, size_t i, double& v) {
 }
 
 bool to_index(const Tok& tk, size_t i, uint64_t& v) {
+  {  // plain digits (at most 18: no overflow) are strtoll's value
+    const uint64_t b = tk.start[i], e = tk.end_of(i);
+    if (e > b && e - b <= 18) {
+      uint64_t x = 0;
+      uint64_t k = b;
+      for (; k < e && tk.text[k] >= '0' && tk.text[k] <= '9'; ++k) x = 10 * x + uint64_t(tk.text[k] - '0');
+      if (k == e) {
+        v = x;
+        return true;
+      }
+    }
+  }
   const TokStr s(tk, i);
   errno = 0;
   char* end = nullptr;
@@ -195,7 +259,7 @@ int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, u
       for (auto& x : th) x.join();
     }
     for (size_t t = 0; t < nt; ++t) ntok[t + 1] += ntok[t];
-    tk.start.resize(ntok[nt]);
+    tk.start.resize_uninit(ntok[nt]);
     {
       std::vector<std::thread> th;
       for (size_t t = 0; t < nt; ++t) th.emplace_back([&, t] { scan(t, tk.start.data() + ntok[t]); });
@@ -481,11 +545,16 @@ int gd_parse_pocket(const char* text, size_t len, gd_pocketbuf** out, char* err,
     return GD_ERR_PARSE;
   };
   Tok tk{text, {}, len};
-  bool in = false;
-  for (size_t i = 0; i < len; ++i) {
-    const bool sp = is_space(text[i]);
-    if (!sp && !in) tk.start.push_back(i);
-    in = !sp;
+  {
+    std::vector<uint64_t> st;
+    bool in = false;
+    for (size_t i = 0; i < len; ++i) {
+      const bool sp = is_space(text[i]);
+      if (!sp && !in) st.push_back(i);
+      in = !sp;
+    }
+    tk.start.resize_uninit(st.size());
+    std::copy(st.begin(), st.end(), tk.start.data());
   }
   const uint64_t T = tk.start.size();
   uint64_t i = 0;

@@ -9,6 +9,7 @@ timeout 600 python bench.py --ligands 1250 --no-cpu > $O/bench_c2_1250.json 2> $
 timeout 900 python bench.py --gpus 2 --no-cpu > $O/bench_c2_gpus2.json 2>> $O/bench.err
 timeout 900 python bench.py --gpus 4 --no-cpu --no-regimes > $O/bench_c2_gpus4.json 2>> $O/bench.err
 lscpu > $O/lscpu.txt 2>&1
+timeout 300 python tools/bench_ingest.py 100000 > $O/ingest.json 2> $O/ingest.err
 for t in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $t python tools/sanitize_case.py > $O/sanitizer_$t.txt 2>&1
 done
