@@ -173,3 +173,38 @@ def test_metrics_csv_matches_reference(reference, i):
     m = METRICS[i]
     for cfg in (gd.NodeConfig(), gd.NodeConfig(4, 4, 8, "real"), gd.NodeConfig(8, 2, 16, "synthetic")):
         assert gd.write_metrics(m, cfg).encode() == reference.write_metrics(m, cfg)
+
+
+def _number_tokens():
+    rng = np.random.default_rng(11)
+    toks = ["-0", "0", "0.0", "-0.000", ".5", "5.", "-.5", "1.e5", "1e+05", "1E-5", "007", "00.0100",
+            "2.2250738585072014e-308", "2.2250738585072011e-308", "4.9406564584124654e-324", "1e-320",
+            "1.7976931348623157e308", "1.7976931348623159e308", "123456789012345678901234567890",
+            "0.1000000000000000055511151231257827", "9007199254740993", "1e-400", "-1e-400", "1e400",
+            "+2", "0x1.8p1", "1e", "1e+", ".", "-", "1..2", "1e5.5"]
+    for _ in range(300):
+        mant = "".join(str(d) for d in rng.integers(0, 10, int(rng.integers(1, 25))))
+        dot = int(rng.integers(0, len(mant) + 1))
+        s = ("-" if rng.random() < 0.3 else "") + mant[:dot] + "." + mant[dot:]
+        if rng.random() < 0.5:
+            s += "e" + str(int(rng.integers(-330, 330)))
+        toks.append(s)
+    return toks
+
+
+def test_number_tokens_match_reference(reference):
+    """The parser's fast number paths (std::from_chars for plain decimals, a digit loop for counts)
+    give std::stod's / std::stoll's value or error on every token: tricky and random decimals."""
+    for t in _number_tokens():
+        text = f"ligand num\natoms 2\n{t} 0 0 0.5\n1.5 0 0 0.5\nbonds 1\n0 1\nrotamers 0\nend\n".encode()
+        try:
+            ref = reference.parse_library(text)
+            ref_err = None
+        except OracleError as e:
+            ref, ref_err = None, e
+        if ref_err is None:
+            _same_lib(gd.parse_library(text), ref)
+        else:
+            with pytest.raises((gd.ParseError, gd.ValidationError)) as got:
+                gd.parse_library(text)
+            assert str(got.value) == ref_err.msg, t
