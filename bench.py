@@ -253,7 +253,7 @@ def host_topk(score, k):
 def run_ours(args):
     import torch
     import paper_1901_06229_b200 as gd
-    from paper_1901_06229_b200.distributed import gather_topk, merge_hits
+    from paper_1901_06229_b200.distributed import gather_topk_array
 
     rank, world, local = dist_env()
     n_dev = max(1, torch.cuda.device_count())
@@ -305,10 +305,11 @@ def run_ours(args):
         the per-kernel event times of the last gd_run, and the merged global top-k."""
         def step():
             batch.run()
-            hits = [(s, i + first, r) for s, i, r in batch.topk(topk)]  # K3 + D2H of k records
+            hits = batch.topk_array(topk)  # K3 + D2H of k records (score, index, restart)
+            hits[:, 1] += first            # global ligand indices
             if dist is not None:  # the one exchange of the path: all-gather of the top-k records
                 with torch.cuda.stream(stream):
-                    hits = gather_topk(hits, topk, gdev)
+                    hits = gather_topk_array(hits, topk, gdev)
             return hits
 
         for _ in range(warmup):
@@ -331,7 +332,7 @@ def run_ours(args):
         k1b = statistics.mean(k["k1b_sweep"] for k in kms)
         k2 = statistics.mean(k["k2_finalize"] for k in kms)
         ms, k1a, k1b, k2 = max_over_ranks([statistics.mean(times), k1a, k1b, k2])
-        return ms, k1a, k1b, k2, hits
+        return ms, k1a, k1b, k2, [(float(s), int(i), int(r)) for s, i, r in hits]
 
     sm_hz_guess = 1965e6
     per_clk, peak_src = fp32_peak_per_clk()
@@ -371,9 +372,10 @@ def run_ours(args):
         t0 = time.perf_counter()
         res = ctx.dock(lib)
         order = host_topk(res.best_score, topk)
-        e2e_hits = [(float(res.best_score[i]), int(i) + first, int(res.best_restart[i])) for i in order]
+        e2e_hits = np.stack([res.best_score[order], (order + first).astype(np.float64),
+                             res.best_restart[order].astype(np.float64)], axis=1)
         if dist is not None:
-            e2e_hits = gather_topk(e2e_hits, topk, gdev)
+            e2e_hits = gather_topk_array(e2e_hits, topk, gdev)
         t1 = time.perf_counter()
         if it > 0:
             e2e_times.append(t1 - t0)
@@ -382,6 +384,7 @@ def run_ours(args):
     h2d = int(sum_over_ranks([float(e2e_stats.get("h2d_bytes", 0))])[0])
     d2h = int(sum_over_ranks([float(e2e_stats.get("d2h_bytes", 0))])[0])
     assert np.array_equal(chk.best_score, res.best_score), "staged vs e2e results differ"
+    e2e_hits = [(float(s), int(i), int(r)) for s, i, r in e2e_hits]
     assert e2e_hits == hits, "e2e top-k differs from the device top-k"
 
     # ---- sweep regimes beside the headline (1 GPU): the live-commit sweep at clash 0.1 and the

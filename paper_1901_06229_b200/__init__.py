@@ -811,11 +811,17 @@ class Batch:
         self.ctx._check(self.ctx._lib.gd_fetch(self._h, C.byref(r)))
         return out
 
-    def topk(self, k: int):
+    def topk_array(self, k: int) -> np.ndarray:
+        """gd_topk (K3): the k best ligands of the batch as an (n, 3) float64 array (best score,
+        ligand index within the batch, best restart), ordered by (score desc, index asc)."""
         hits = (_Hit * max(1, k))()
         n = C.c_uint32()
         self.ctx._check(self.ctx._lib.gd_topk(self._h, k, hits, C.byref(n)))
-        return [(hits[i].best_score, hits[i].ligand, hits[i].restart) for i in range(n.value)]
+        rec = np.frombuffer(hits, dtype=np.dtype([("s", "<f8"), ("l", "<u4"), ("r", "<u4")]), count=n.value)
+        return np.stack([rec["s"], rec["l"].astype(np.float64), rec["r"].astype(np.float64)], axis=1)
+
+    def topk(self, k: int):
+        return [(float(s), int(i), int(r)) for s, i, r in self.topk_array(k)]
 
     def free(self):
         if self._h:
