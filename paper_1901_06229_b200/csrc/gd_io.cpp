@@ -23,6 +23,7 @@
 #include <cfloat>
 #include <cstring>
 #include <memory>
+#include <utility>
 #include <string>
 #include <thread>
 #include <vector>
@@ -37,9 +38,33 @@ struct gd_pocketbuf {
   std::vector<double> field;
 };
 
+// Allocator whose resize leaves trivially-constructible elements uninitialised: the parser writes
+// every element of the big arrays in its parallel pass (a failed parse discards the buffer), so a
+// zero fill on one thread first would only cost time (~170 MB per 100k C2 ligands).
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = UninitAlloc<U>;
+  };
+  UninitAlloc() = default;
+  template <class U>
+  UninitAlloc(const UninitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+
 struct gd_libbuf {
-  std::vector<uint32_t> atom_off, bond_off, rot_off, name_off, bonds, rots;
-  std::vector<double> xyz, radius, dihedrals;
+  std::vector<uint32_t> atom_off, bond_off, rot_off, name_off;
+  std::vector<uint32_t, UninitAlloc<uint32_t>> bonds, rots;
+  std::vector<double, UninitAlloc<double>> xyz, radius;
+  std::vector<double> dihedrals;
   std::string names;
 };
 
@@ -274,7 +299,8 @@ int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, u
   auto tok_err = [&](uint64_t i, const std::string& m) {
     return m + line_suffix(tk.line_of(tk.start[i]));
   };
-  // (2) record headers, sequential
+  // (2) record headers: the reference's walk (with its errors) — sequential, resumable at any
+  // record start, bounded by `limit`; `stop` once it has reported an error
   std::vector<Rec> recs;
   Err e;
   uint64_t i = 0, na = 0, nb = 0, nr = 0, nn = 0;
@@ -303,9 +329,12 @@ int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, u
     }
     return true;
   };
-  while (i < T) {
+  bool stop = false;
+  auto seq_walk = [&](uint64_t limit) {
+  while (i < T && i < limit) {
     if (!tok_is(tk, i, "ligand")) {
       e.set(i, GD_ERR_PARSE, tok_err(i, "expected 'ligand', got '" + tk.str(i) + "'"));
+      stop = true;
       break;
     }
     Rec r;
@@ -313,9 +342,13 @@ int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, u
     if (i + 1 >= T) {
       const Err x = at_eof("ligand name");
       e.set(x.pos, x.code, x.msg);
+      stop = true;
       break;
     }
-    if (!keyword(i + 2, "atoms") || !count(i + 3, "atom count", r.n)) break;
+    if (!keyword(i + 2, "atoms") || !count(i + 3, "atom count", r.n)) {
+      stop = true;
+      break;
+    }
     // body sizes; a count the text cannot hold ends at the end of input inside the record
     uint64_t p = i + 4 + 4 * std::min<uint64_t>(r.n, T);
     if (p > T) {  // numbers run out: the reference fails on the first missing one
@@ -326,10 +359,12 @@ int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, u
       r.n = have / 4;  // the complete atoms still get their numbers checked below
       r.m = r.k = 0;
       recs.push_back(r);
+      stop = true;
       break;
     }
     if (!keyword(p, "bonds") || !count(p + 1, "bond count", r.m)) {
       recs.push_back(Rec::of(r.tok, r.n, 0, 0));
+      stop = true;
       break;
     }
     p += 2;
@@ -338,11 +373,13 @@ int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, u
       const Err x = at_eof(have % 2 ? "bond atom j" : "bond atom i");
       e.set(x.pos, x.code, x.msg);
       recs.push_back(Rec::of(r.tok, r.n, have / 2, 0));
+      stop = true;
       break;
     }
     p += 2 * r.m;
     if (!keyword(p, "rotamers") || !count(p + 1, "rotamer count", r.k)) {
       recs.push_back(Rec::of(r.tok, r.n, r.m, 0));
+      stop = true;
       break;
     }
     p += 2;
@@ -351,15 +388,77 @@ int gd_parse_library(const char* text, size_t len, gd_libbuf** out, char* err, u
       const Err x = at_eof(have % 2 ? "rotamer atom j" : "rotamer atom i");
       e.set(x.pos, x.code, x.msg);
       recs.push_back(Rec::of(r.tok, r.n, r.m, have / 2));
+      stop = true;
       break;
     }
     p += 2 * r.k;
     if (!keyword(p, "end")) {
       recs.push_back(r);
+      stop = true;
       break;
     }
     recs.push_back(r);
     i = p + 1;
+  }
+  };
+  // The walk in parallel: every thread follows the record chain from the first plausible record
+  // start ("ligand" NAME "atoms") of its token slice, structure only (no error text). A slice's
+  // chain is adopted when the reference walk arrives at one of its record starts — a walk from a
+  // true record start is deterministic, so the records are the ones it would find — and the
+  // reference walk crosses the rest itself (a slice whose chain began at a false start, or stopped
+  // at a malformed record, which it then reports exactly as before).
+  {
+    constexpr uint64_t NONE = ~0ull;
+    auto walk_one = [&](uint64_t at, Rec& r) -> uint64_t {
+      uint64_t n = 0, m = 0, k = 0;
+      if (at + 3 >= T || !tok_is(tk, at, "ligand") || !tok_is(tk, at + 2, "atoms") || !to_index(tk, at + 3, n) ||
+          n > T)
+        return NONE;
+      uint64_t p = at + 4 + 4 * n;
+      if (p + 1 >= T || !tok_is(tk, p, "bonds") || !to_index(tk, p + 1, m) || m > T) return NONE;
+      p += 2 + 2 * m;
+      if (p + 1 >= T || !tok_is(tk, p, "rotamers") || !to_index(tk, p + 1, k) || k > T) return NONE;
+      p += 2 + 2 * k;
+      if (p >= T || !tok_is(tk, p, "end")) return NONE;
+      r = Rec::of(at, n, m, k);
+      return p + 1;
+    };
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(hw, size_t(T / 65536) + 1));
+    std::vector<uint64_t> cut(nt + 1);
+    for (size_t t = 0; t <= nt; ++t) cut[t] = T * t / nt;
+    std::vector<std::vector<Rec>> srec(nt);
+    std::vector<uint64_t> snext(nt, NONE);
+    {
+      std::vector<std::thread> th;
+      for (size_t t = 1; t < nt; ++t)
+        th.emplace_back([&, t] {
+          uint64_t j = cut[t];
+          while (j + 3 < T && j < cut[t + 1] && !(tok_is(tk, j, "ligand") && tok_is(tk, j + 2, "atoms"))) ++j;
+          while (j < cut[t + 1]) {
+            Rec r;
+            const uint64_t nx = walk_one(j, r);
+            if (nx == NONE) break;
+            srec[t].push_back(r);
+            j = nx;
+          }
+          snext[t] = j;
+        });
+      for (auto& x : th) x.join();
+    }
+    for (size_t t = 0; t < nt && !stop && i < T; ++t) {
+      if (i >= cut[t + 1]) continue;
+      if (t > 0 && !srec[t].empty()) {
+        const auto it = std::lower_bound(srec[t].begin(), srec[t].end(), i,
+                                         [](const Rec& r, uint64_t v) { return r.tok < v; });
+        if (it != srec[t].end() && it->tok == i) {
+          recs.insert(recs.end(), it, srec[t].end());
+          i = snext[t];
+        }
+      }
+      seq_walk(cut[t + 1]);
+    }
+    if (!stop) seq_walk(T);
   }
   // offsets (also for the partial record an early error left behind)
   for (Rec& r : recs) {

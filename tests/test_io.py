@@ -208,3 +208,40 @@ def test_number_tokens_match_reference(reference):
             with pytest.raises((gd.ParseError, gd.ValidationError)) as got:
                 gd.parse_library(text)
             assert str(got.value) == ref_err.msg, t
+
+
+@pytest.mark.parametrize("edit", ["none", "late_keyword", "late_count", "late_number", "early_keyword", "truncated"])
+def test_parallel_record_walk_matches_reference(reference, edit):
+    """The record-header walk runs per token slice in parallel (speculative chains adopted where the
+    reference walk meets them): a multi-slice library with keyword-like ligand names, and errors
+    planted in early / late slices, give the reference's arrays or its exact error."""
+    lib = gd.make_library(gd.LibrarySpec(3000, 40, 8, 9))
+    text = gd.serialize_library(lib)
+    for name, fake in (("lig_000007", "ligand"), ("lig_000100", "atoms"), ("lig_001500", "end"), ("lig_002200", "bonds")):
+        text = text.replace(f"ligand {name}\n", f"ligand {fake}\n")
+    marker = {"late_keyword": "ligand lig_002500\n", "late_count": "ligand lig_002700\n",
+              "late_number": "ligand lig_002900\n", "early_keyword": "ligand lig_000050\n"}.get(edit)
+    if marker:
+        at = text.index(marker) + len(marker)
+        body = text[at:]
+        if edit.endswith("keyword"):
+            body = body.replace("bonds", "bondz", 1)
+        elif edit == "late_count":
+            body = body.replace("rotamers 8", "rotamers x8", 1)
+        else:
+            body = body.replace(" ", " 1.5e", 1)
+        text = text[:at] + body
+    if edit == "truncated":
+        text = text[: len(text) - 37]
+    data = text.encode()
+    try:
+        ref = reference.parse_library(data)
+        ref_err = None
+    except OracleError as e:
+        ref, ref_err = None, e
+    if ref_err is None:
+        _same_lib(gd.parse_library(data), ref)
+    else:
+        with pytest.raises((gd.ParseError, gd.ValidationError)) as got:
+            gd.parse_library(data)
+        assert str(got.value) == ref_err.msg
