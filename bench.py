@@ -263,11 +263,6 @@ def run_ours(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        if backend == "nccl" and "NCCL_DEBUG" not in os.environ:
-            # communicator set-up lines (transport: NVLink / NVLS) on stderr, stdout keeps the one JSON line
-            os.environ["NCCL_DEBUG"] = "INFO"
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
