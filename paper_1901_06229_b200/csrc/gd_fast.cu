@@ -95,7 +95,12 @@ __host__ __device__ constexpr uint32_t pair_cap() { return 32u * NS + 32u; }
 #define GD_ALIGN_THREADS_L1 512  // K1a when the cells do not fit shared memory (read through L1; C5: 512 > 384, 448, 640)
 #endif
 #ifndef GD_REFINE_THREADS
-#define GD_REFINE_THREADS 512  // K1r: 16 warps x 128 registers (1024 threads spill the FP64 scorer)
+// K1r for <= 64 atoms: 32 warps x 64 registers (the FP64 scorer spills ~600 bytes, yet the extra
+// warps hide its latency chains better: C2 K1r -22 % against 16 warps x 128)
+#define GD_REFINE_THREADS 1024
+#endif
+#ifndef GD_REFINE_THREADS_NS4
+#define GD_REFINE_THREADS_NS4 512  // K1r otherwise (65..128 atoms, or the FP64 field not in shared memory)
 #endif
 #ifndef GD_FAST_THREADS_NS4
 #define GD_FAST_THREADS_NS4 256  // NS = 4: 255 registers (no spills) beat 16 warps at 128 (C4 clash 0.1 +15 %)
@@ -2270,21 +2275,29 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
     if ((e = cudaStreamWaitEvent(stream_b, mid, 0)) != cudaSuccess) return e;
     stream = stream_b;
   }
-  // K1r (exact alignment): 3 n doubles of pose + 3 n of scratch per warp, 32 warps, FP64 field in
-  // shared memory when it fits
+  // K1r (exact alignment): 3 n doubles of pose + 3 n of scratch per warp, FP64 field in shared
+  // memory when it fits. Small ligands with the field in shared memory: 32 warps (C2 K1r -22 %);
+  // otherwise 16 (with the field from L2, 32 warps were slower: C5 +5 %).
   {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const uint32_t slot_r = 6 * npad_max;
-    size_t smem_r = size_t(slot_r) * sizeof(double) * (GD_REFINE_THREADS / 32);
     const size_t fbytes = size_t(pk.dims[0]) * pk.dims[1] * pk.dims[2] * sizeof(double);
-    const uint32_t fs_r = smem_r + fbytes + 1024 <= size_t(optin) ? 1u : 0u;
-    if (fs_r) smem_r += fbytes;
-    auto kr = align_refine_kernel<NS, GD_REFINE_THREADS>;
-    if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_r))) != cudaSuccess) return e;
-    kr<<<n_sms, GD_REFINE_THREADS, smem_r, stream>>>(pk, pr, b, slot_r, fs_r);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    auto launch_r = [&](auto kr, int nt) -> bool {  // false: the field does not fit beside nt threads
+      size_t smem_r = size_t(slot_r) * sizeof(double) * size_t(nt / 32);
+      const uint32_t fs_r = smem_r + fbytes + 1024 <= size_t(optin) ? 1u : 0u;
+      if (!fs_r && nt != GD_REFINE_THREADS_NS4) return false;
+      if (fs_r) smem_r += fbytes;
+      if ((e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_r))) != cudaSuccess)
+        return true;
+      kr<<<n_sms, nt, smem_r, stream>>>(pk, pr, b, slot_r, fs_r);
+      e = cudaGetLastError();
+      return true;
+    };
+    if (!(NS <= 2 && launch_r(align_refine_kernel<NS, GD_REFINE_THREADS>, GD_REFINE_THREADS)))
+      launch_r(align_refine_kernel<NS, GD_REFINE_THREADS_NS4>, GD_REFINE_THREADS_NS4);
+    if (e != cudaSuccess) return e;
   }
   constexpr size_t kK1bStatic = 2048;  // the kernel's __shared__ DevPocket + per-warp counters, rounded up
 #if GD_K1B_FIELDF
