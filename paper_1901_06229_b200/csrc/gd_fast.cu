@@ -2356,4 +2356,9 @@ cudaError_t launch_align_big(const DevPocket& pk, const DevParams& pr, const Dev
 
 uint32_t k1a_qt_groups() { return uint32_t(kQtGroups); }
 
+bool k1a_cells_in_smem(const DevPocket& pk, uint32_t max_n) {
+  const uint32_t npad = (std::min(max_n, kFastMaxAtoms) + 3) & ~3u;
+  return plan_smem(pk, 4 * npad * sizeof(float), GD_ALIGN_THREADS / 32, 8).cells_in_smem;
+}
+
 }  // namespace gdk

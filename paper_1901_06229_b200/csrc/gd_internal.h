@@ -133,6 +133,8 @@ struct DevBatch {
 size_t order_tmp_bytes(uint32_t n);
 // quarter-turn groups of one K1a work unit (the unit table's c0 step, upload_grid_f; gd_fast.cu)
 uint32_t k1a_qt_groups();
+// K1a holds the pocket's cells in shared memory for ligands of up to max_n atoms (gd_fast.cu)
+bool k1a_cells_in_smem(const DevPocket& pk, uint32_t max_n);
 
 cudaError_t launch_dock(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                         cudaStream_t stream, int* launches, cudaEvent_t* ev = nullptr,
