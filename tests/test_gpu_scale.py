@@ -147,3 +147,21 @@ def test_only_large_ligands(pair):
     out = fast.dock(lib, pocket, p, trace=True)
     assert fast.stats()["align_exact_evals"] == 0  # (the FP64 kernel does not count candidates)
     _same(out, exact.dock(lib, pocket, p, trace=True))
+
+
+@pytest.mark.parametrize("grid", [None, ((47, 47, 47), 0.375)], ids=["cells_in_smem", "cells_in_l1"])
+def test_item_order_does_not_change_results(pair, grid, monkeypatch):
+    """The fast kernels claim items in Morton order of the start targets where K1a reads the cells
+    through L1 (C5-size grids), in ligand order where they fit shared memory; GD_NATURAL_ORDER=1
+    forces ligand order. Every output and decision bit is independent of the claim order."""
+    fast, _ = pair
+    pocket = gd.make_pocket(gd.PocketSpec(dims=grid[0], spacing=grid[1]) if grid else gd.PocketSpec())
+    lib = gd.make_library(gd.LibrarySpec(500, 40, 8, 17))
+    p = gd.DockParams(clash_factor=0.1)
+    chosen = fast.dock(lib, pocket, p, trace=True)
+    launches = fast.stats()["launches"]
+    monkeypatch.setenv("GD_NATURAL_ORDER", "1")
+    natural = fast.dock(lib, pocket, p, trace=True)
+    # the Morton order costs one key kernel: present on the L1 grid only
+    assert launches == fast.stats()["launches"] + (1 if grid else 0)
+    _same(chosen, natural)
