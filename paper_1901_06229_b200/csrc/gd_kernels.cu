@@ -458,10 +458,11 @@ __global__ void topk_emit(const unsigned long long* keys, const uint32_t* vals, 
 }
 
 // --------------------------------------------------------------------------------------------
-// Item order: the fast kernels claim (ligand, restart) items sorted by the Morton code of the
-// start target (32 buckets per axis of the pocket box). Work in flight at any moment then sits in
-// a small region of the pocket, so the cells its samples gather stay in L1 (C5's 1.56 MB of cells
-// do not fit shared memory; K1b reads the cells through L1 on every grid).
+// Item order: where K1a reads the cells through L1 (C5's 1.56 MB of cells do not fit shared
+// memory), the fast kernels claim (ligand, restart) items sorted by the Morton code of the start
+// target (32 buckets per axis of the pocket box). Work in flight at any moment then sits in a small
+// region of the pocket, so the cells its samples gather stay in L1. Where the cells fit shared
+// memory, launch_dock keeps ligand order (no sort).
 // --------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 5 bits -> every third bit
   v &= 31u;
