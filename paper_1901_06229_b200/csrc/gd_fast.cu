@@ -89,7 +89,13 @@ __host__ __device__ constexpr uint32_t pair_cap() { return 32u * NS + 32u; }
 #define GD_K1B_MIN_WARPS_SC 12  // K1b keeps the cells in shared memory only if this many warps still fit
 #endif
 #ifndef GD_ALIGN_THREADS
-#define GD_ALIGN_THREADS 384
+#define GD_ALIGN_THREADS 448  // K1a, cells in shared memory, 33..64 atoms: 14 warps x 128 registers (C2 -1.4 % vs 12, -1 % vs 16)
+#endif
+#ifndef GD_ALIGN_THREADS_NS1
+#define GD_ALIGN_THREADS_NS1 512  // the same for <= 32 atoms: 16 warps x 128 (C1 shape -0.6 % vs 12, -2.8 % vs 14)
+#endif
+#ifndef GD_ALIGN_THREADS_NS4
+#define GD_ALIGN_THREADS_NS4 384  // the same for 65..128 atoms (and NS = 8): 12 warps x 168 (C4: 14 warps +1 %)
 #endif
 #ifndef GD_ALIGN_THREADS_L1
 #define GD_ALIGN_THREADS_L1 512  // K1a when the cells do not fit shared memory (read through L1; C5: 512 > 384, 448, 640)
@@ -2262,7 +2268,8 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   const uint32_t slot_b = 6 * npad_max + 4 * pair_cap<NS>() + 8 * npad_max + 32 + 2 * npad_max + 2 * NS * npad_max +
                           kZCap + 4 + npad_max;
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
-  // cells in shared memory: 12 warps x 168 registers (GD_ALIGN_THREADS); cells through L1 (large
+  // cells in shared memory: 16 / 14 / 12 warps for NS = 1 / 2 / 4 (GD_ALIGN_THREADS_NS1, GD_ALIGN_THREADS,
+  // GD_ALIGN_THREADS_NS4); cells through L1 (large
   // grids): 16 warps x 128 (GD_ALIGN_THREADS_L1)
   const SmemPlan pg = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS_L1 / 32, 8);
   cudaError_t e =
@@ -2335,10 +2342,10 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
 
 cudaError_t launch_fast(const DevPocket& pk, const DevParams& pr, const DevBatch& b, int n_sms,
                         cudaStream_t stream, cudaEvent_t mid, cudaStream_t stream_b) {
-  if (b.max_n <= 32) return launch_ns<1, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream, mid, stream_b);
+  if (b.max_n <= 32) return launch_ns<1, GD_ALIGN_THREADS_NS1, GD_FAST_THREADS>(pk, pr, b, n_sms, stream, mid, stream_b);
   if (b.max_n <= 64) return launch_ns<2, GD_ALIGN_THREADS, GD_FAST_THREADS>(pk, pr, b, n_sms, stream, mid, stream_b);
   if (b.max_n <= 128)
-    return launch_ns<4, GD_ALIGN_THREADS, GD_FAST_THREADS_NS4>(pk, pr, b, n_sms, stream, mid, stream_b);
+    return launch_ns<4, GD_ALIGN_THREADS_NS4, GD_FAST_THREADS_NS4>(pk, pr, b, n_sms, stream, mid, stream_b);
   return cudaErrorNotSupported;  // launch_dock routes > 128 atoms to the exact kernel
 }
 
@@ -2346,10 +2353,10 @@ cudaError_t launch_align_big(const DevPocket& pk, const DevParams& pr, const Dev
                              cudaStream_t stream) {
   // (ligands beyond kAlignBigMaxAtoms are skipped by the kernel: the FP64 kernel aligns them)
   const uint32_t slot_a = 4 * ((std::min(b.max_n, kAlignBigMaxAtoms) + 3) & ~3u);
-  const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS / 32, 8);
+  const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS_NS4 / 32, 8);
   const SmemPlan pg = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS_L1 / 32, 8);
   return pa.cells_in_smem
-             ? launch_persistent(align_coarse_kernel<8, GD_ALIGN_THREADS, true>, pa, n_sms, stream, pk, pr, b, slot_a)
+             ? launch_persistent(align_coarse_kernel<8, GD_ALIGN_THREADS_NS4, true>, pa, n_sms, stream, pk, pr, b, slot_a)
              : launch_persistent(align_coarse_kernel<8, GD_ALIGN_THREADS_L1, false>, pg, n_sms, stream, pk, pr, b,
                                  slot_a);
 }
