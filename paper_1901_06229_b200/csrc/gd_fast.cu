@@ -92,7 +92,7 @@ __host__ __device__ constexpr uint32_t pair_cap() { return 32u * NS + 32u; }
 #define GD_ALIGN_THREADS 448  // K1a, cells in shared memory, 33..64 atoms: 14 warps x 128 registers (C2 -1.4 % vs 12, -1 % vs 16)
 #endif
 #ifndef GD_ALIGN_THREADS_NS1
-#define GD_ALIGN_THREADS_NS1 512  // the same for <= 32 atoms: 16 warps x 128 (C1 shape -0.6 % vs 12, -2.8 % vs 14)
+#define GD_ALIGN_THREADS_NS1 384  // the same for <= 32 atoms: 12 warps (16: C1 shape at 4k -0.6 %, but C1's 100-ligand batch +23 %: 1.35 items per warp)
 #endif
 #ifndef GD_ALIGN_THREADS_NS4
 #define GD_ALIGN_THREADS_NS4 384  // the same for 65..128 atoms (and NS = 8): 12 warps x 168 (C4: 14 warps +1 %)
@@ -2268,7 +2268,7 @@ static cudaError_t launch_ns(const DevPocket& pk, const DevParams& pr, const Dev
   const uint32_t slot_b = 6 * npad_max + 4 * pair_cap<NS>() + 8 * npad_max + 32 + 2 * npad_max + 2 * NS * npad_max +
                           kZCap + 4 + npad_max;
   const SmemPlan pa = plan_smem(pk, slot_a * sizeof(float), NTA / 32, 8);
-  // cells in shared memory: 16 / 14 / 12 warps for NS = 1 / 2 / 4 (GD_ALIGN_THREADS_NS1, GD_ALIGN_THREADS,
+  // cells in shared memory: 12 / 14 / 12 warps for NS = 1 / 2 / 4 (GD_ALIGN_THREADS_NS1, GD_ALIGN_THREADS,
   // GD_ALIGN_THREADS_NS4); cells through L1 (large
   // grids): 16 warps x 128 (GD_ALIGN_THREADS_L1)
   const SmemPlan pg = plan_smem(pk, slot_a * sizeof(float), GD_ALIGN_THREADS_L1 / 32, 8);
